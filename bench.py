@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""bench.py -- ms/token of the offloaded OPT-30B decode linear stack (BJ:2, BJ:10).
+
+One step = one decode token through all 48 OPT-30B layers (h=7168, ffn=28672):
+every QKV / O / fc1 / fc2 linear runs HeteGen's heterogeneous split (resident
+r=0, so every weight lives in pinned host memory; alpha from Eq. (5) with rates
+measured by hg_measure in this process; streamed rows copied in chunks over the
+host link into a device ring and GEMV'd on the GPU; the rest computed by the
+host thread pool), with the glue (LN, attention at position 0, ReLU, residual)
+on the GPU.  59,190,018,048 weight bytes per token per job.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--batch B]
+
+N > 1: launched under torchrun; rank p owns W rows [pN/P,(p+1)N/P) of every
+linear (column-sharded TP), outputs all-gathered with NCCL after each linear.
+--impl reference: the fp64 oracle (oracle/) on the host cores, on a bounded
+sample of the same workload (one layer's four linears), scaled to ms/token.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, F, LAYERS = 7168, 28672, 48
+SHAPES = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+NAMES = ("qkv", "o", "fc1", "fc2")
+STACK_BYTES = LAYERS * sum(2 * n * k for n, k in SHAPES.values())  # 59,190,018,048
+METRIC = "ms/token offloaded OPT-30B decode linears; HBM & H2D GB/s vs roofline"
+SEED = 1164 + 3  # base seed + config index (BJ:10 is configs[3])
+
+
+def env_rank():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
+        os.environ.get("LOCAL_RANK", "0"))
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------- clocks sampler
+class Clocks:
+    def __init__(self, index=0):
+        self.samples = []
+        self.proc = None
+        self.index = index
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([s.strip() for s in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for nm, v in zip(names, s[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- reference arm / cpu baseline
+def oracle_layer_sample(reps=1, batch=1, nthreads=None):
+    """Time the fp64 oracle on layer 0's four linears (1/48 of a token); returns seconds per sample."""
+    import numpy as np
+    import oracle
+    from harness import gen
+    nthreads = nthreads or os.cpu_count()
+    xs, Ws, bs = {}, {}, {}
+    for name in NAMES:
+        N, K = SHAPES[name]
+        xs[name], Ws[name], bs[name] = gen.linear_inputs(SEED, 0, name, batch, N, K)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for name in NAMES:
+            oracle.linear(xs[name], Ws[name], bs[name], nthreads=nthreads)
+        ts.append(time.perf_counter() - t0)
+    return ts, nthreads
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    ts, nthr = oracle_layer_sample(reps=args.warmup + args.steps, batch=args.batch)
+    timed = ts[args.warmup:]
+    ms_tok = statistics.median(timed) * LAYERS * 1e3
+    line = {
+        "impl": "reference", "metric": METRIC, "value": ms_tok, "unit": "ms/token", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_tok, "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "OPT-30B 48-layer decode linear stack (bounded sample: layer 0's 4 linears x48)",
+                   "batch": args.batch, "hidden": H, "ffn": F, "layers": LAYERS},
+        "cpu_baseline": {"value": ms_tok, "unit": "ms/token", "cores": nthr, "kind": "oracle",
+                         "sample": "one layer (qkv,o,fc1,fc2: 1.233 GB of weights) per step, fp64 naive C "
+                                   "loops, scaled x48 to a token"},
+        "e2e": {"value": ms_tok, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from harness import gen
+    from paper_2403_01164_b200 import hg
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ncores = os.cpu_count() or 1
+    per = max(1, ncores // world)
+    threads = args.threads or per
+    ctx = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
+                     chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
+                     max_k=F, max_n=3 * H, wrap_prefetch=1, collect_stats=0)
+    if world > 1:
+        uid = hg.hg_dist_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.hg_dist_init(world, rank, obj[0])
+    B = args.batch
+    G = 128
+
+    # ---- weights: this rank's row shard of every linear, pinned host (r = 0) ----
+    t_setup = time.perf_counter()
+    host, biases = [], []
+    for l in range(args.layers):
+        hl, bl = {}, {}
+        for name in NAMES:
+            N, K = SHAPES[name]
+            r0, r1 = rank * N // world, (rank + 1) * N // world
+            Wt = torch.empty((r1 - r0, K), dtype=torch.int16, pin_memory=True)
+            gen.uniform_bf16(SEED, gen.tensor_id(l, name, "W"), (r1 - r0) * K, gen.w_scale(K),
+                             offset=r0 * K, out=Wt.data_ptr())
+            b = gen.bf16_bits_to_f32(gen.uniform_bf16(SEED, gen.tensor_id(l, name, "bias"), r1 - r0,
+                                                      gen.BIAS_SCALE, offset=r0))
+            hl[name] = Wt
+            bl[name] = torch.from_numpy(b).cuda()
+        host.append(hl)
+        biases.append(bl)
+    t_setup = time.perf_counter() - t_setup
+
+    # ---- a1: measured rates -> alpha (Eq. 5), per-linear plans ----
+    fc1 = host[0]["fc1"]
+    rates = ctx.hg_measure(fc1, fc1.shape[0], H, B, under_load=True)
+    pk = peaks()
+    rd = rates.as_dict()
+    if args.alpha is not None:
+        mode, af = hg.FIXED, args.alpha
+    else:
+        mode, af = hg.EXACT, 0.0
+    layers = []
+    plans = {}
+    for l in range(args.layers):
+        descs = []
+        for name in NAMES:
+            N, K = SHAPES[name]
+            p = ctx.plan(rates, N // world, K, B, 0, mode, af)
+            plans[name] = p
+            descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name]))
+        layers.append(hg.opt_layer(H, F, descs))
+
+    h0 = gen.uniform_bf16(SEED + 1, 999, B * H, 1.0).reshape(B, H)
+    h_host = torch.empty((B, H), dtype=torch.int16, pin_memory=True)
+    h_host.numpy()[...] = h0.view(np.int16)
+    h_dev = h_host.cuda()
+    h_out = torch.empty_like(h_host, pin_memory=True)
+    s = torch.cuda.Stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step_device():
+        ctx.hg_stack(layers, h_dev, B, stream=s)
+
+    def step_e2e():
+        with torch.cuda.stream(s):
+            h_dev.copy_(h_host, non_blocking=True)
+        ctx.hg_stack(layers, h_dev, B, stream=s)
+        with torch.cuda.stream(s):
+            h_out.copy_(h_dev, non_blocking=True)
+
+    # ---- warm-up ----
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    # ---- timed region (device events on the launching stream; max over ranks) ----
+    clocks = Clocks(local)
+    clocks.start()
+    ctx.hg_reset_stats()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e0.record(s)
+    for _ in range(args.steps):
+        step_device()
+    e1.record(s)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - w0
+    barrier()
+    launches = ctx.hg_stats().gpu_launches
+    ck = clocks.stop()
+    dev_s = e0.elapsed_time(e1) * 1e-3
+
+    # ---- e2e: public API with host buffers, H2D of the step input + D2H of the result ----
+    barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(s)
+    for _ in range(args.steps):
+        step_e2e()
+    e3.record(s)
+    torch.cuda.synchronize()
+    e2e_s = e2.elapsed_time(e3) * 1e-3
+
+    # ---- lane breakdown + dominant-kernel roofline: one instrumented step ----
+    sctx_stats = None
+    ctx_stats = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
+                           chunk_bytes=args.chunk_mb << 20, ring_bytes=min(args.ring_mb, 4096) << 20,
+                           max_k=F, max_n=3 * H, wrap_prefetch=1, collect_stats=1) if args.breakdown else None
+    if ctx_stats is not None:
+        if world > 1:
+            ctx_stats.close()
+            ctx_stats = None
+        else:
+            for _ in range(2):
+                ctx_stats.hg_stack(layers, h_dev, B, stream=s)
+            torch.cuda.synchronize()
+            sctx_stats = ctx_stats.hg_stats().as_dict()
+            ctx_stats.close()
+
+    times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    dev_s, e2e_s, wall = times.tolist()
+    ms_tok = dev_s / args.steps * 1e3
+    e2e_ms = e2e_s / args.steps * 1e3
+
+    # ---- roofline numbers ----
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    plan_tot = {"t_roof": 0.0, "t_pred": 0.0, "bytes_str": 0, "bytes_cpu": 0}
+    for name in NAMES:
+        p = plans[name]
+        plan_tot["t_roof"] += p.t_roof * args.layers
+        plan_tot["t_pred"] += p.t_pred * args.layers
+        plan_tot["bytes_str"] += 2 * p.K * p.n_str * args.layers
+        plan_tot["bytes_cpu"] += 2 * p.K * p.n_cpu * args.layers
+    # stack roofline: the link runs ahead across linears, so lanes add up over the stack
+    t_link_roof = plan_tot["bytes_str"] / rd["b_link"]
+    t_cpu_roof = plan_tot["bytes_cpu"] / rd["b_cpu"]
+    t_hbm_roof = 2 * plan_tot["bytes_str"] / (hbm_peak * 1e9)
+    # best achievable over alpha: all host bytes shared by link + CPU at their peaks
+    shard_bytes = STACK_BYTES / world * args.layers / LAYERS
+    t_opt = shard_bytes / (rd["b_link"] + rd["b_cpu"])
+    roof = None
+    if sctx_stats and sctx_stats["gpu_busy_s"] > 0:
+        gbps = sctx_stats["bytes_str"] / sctx_stats["gpu_busy_s"] / 1e9
+        roof = {"bound": "hbm", "kernel": "gemv_bf16_kernel (streamed chunks)", "achieved": round(gbps, 1),
+                "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4), "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback 6650 GB/s",
+                "note": "algorithmic bytes = streamed W bytes read by the chunk GEMVs / summed CUDA-event "
+                        "kernel time, from an instrumented pass after the timed region"}
+    lanes = None
+    if sctx_stats:
+        wall_i = sctx_stats["wall_s"] or 1
+        lanes = {"link_GBps": round(sctx_stats["bytes_str"] / max(sctx_stats["link_busy_s"], 1e-9) / 1e9, 2),
+                 "link_peak_GBps": round(rd["b_link"] / 1e9, 2),
+                 "cpu_GBps": round(sctx_stats["bytes_cpu"] / max(sctx_stats["cpu_busy_s"], 1e-9) / 1e9, 2),
+                 "cpu_peak_GBps": round(rd["b_cpu"] / 1e9, 2),
+                 "busy_frac": {"cpu": round(sctx_stats["cpu_busy_s"] / wall_i, 3),
+                               "link": round(sctx_stats["link_busy_s"] / wall_i, 3),
+                               "gpu": round(sctx_stats["gpu_busy_s"] / wall_i, 4)},
+                 "x_wait_ms": round(sctx_stats["x_wait_s"] * 1e3, 2)}
+    line = {
+        "metric": METRIC, "value": round(ms_tok, 3), "unit": "ms/token", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_tok, 3),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded counter-based generator; random-init OPT-30B-shaped weights)",
+        "config": {"workload": "OPT-30B 48-layer decode linear stack (qkv,o,fc1,fc2 x48), batch %d" % B,
+                   "batch": B, "hidden": H, "ffn": F, "layers": args.layers, "r_resident": 0.0,
+                   "alpha_mode": "fixed" if args.alpha is not None else "Eq5 exact (measured rates)",
+                   "alpha": plans["fc1"].alpha_eff, "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
+                   "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": threads,
+                   "l2": "inputs larger than L2: %.1f GB of weights streamed/computed per step" % (shard_bytes / 1e9)},
+        "gpu_launches": int(launches),
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms/token", "h2d_bytes_per_step": B * H * 2,
+                "d2h_bytes_per_step": B * H * 2},
+        "roofline": roof,
+        "path_roofline": {"bound": "host-link + host-CPU (+HBM)",
+                          "t_roof_ms_at_plan_alpha": round(max(t_link_roof, t_cpu_roof, t_hbm_roof) * 1e3, 3),
+                          "t_opt_ms_best_alpha": round(t_opt * 1e3, 3),
+                          "frac_of_roof_at_plan": round(max(t_link_roof, t_cpu_roof, t_hbm_roof) * 1e3 / ms_tok, 4),
+                          "frac_of_best": round(t_opt * 1e3 / ms_tok, 4),
+                          "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3)},
+        "rates_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rd.items()},
+        "lanes": lanes,
+        "clocks": ck,
+        "wall_ms_per_step": round(wall / args.steps * 1e3, 3),
+        "setup_s": round(t_setup, 1),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ts, nthr = oracle_layer_sample(reps=2, batch=B)
+        line["cpu_baseline"] = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr,
+                                "kind": "oracle",
+                                "sample": "layer 0's four linears (1.233 GB), fp64 naive C loops on all host "
+                                          "cores, best of 2, scaled x48 to a token"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=8)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--layers", type=int, default=LAYERS, help="(development only; the metric needs 48)")
+    ap.add_argument("--alpha", type=float, default=None)
+    ap.add_argument("--chunk-mb", type=int, default=16)
+    ap.add_argument("--ring-mb", type=int, default=4096)
+    ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--no-breakdown", dest="breakdown", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return main_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

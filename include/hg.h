@@ -1,0 +1,290 @@
+/*
+ * hg.h -- C ABI of the B200-native HeteGen heterogeneous offloaded linear.
+ *
+ * HeteGen (arXiv 2403.01164, /root/reference/PAPER.md, cited "P:<line>")
+ * splits each linear of small-batch LLM decode between the CPU and the GPU
+ * ("heterogeneous tensor parallelism", Sec. 3.1), chooses the split
+ * ratio alpha from measured speeds (Eqs. 4-9), and
+ * overlaps CPU compute with the parameter transfer (Sec. 4.2).
+ * This library is that hot path for one B200 (and a column-sharded multi-GPU
+ * form).  Rows of W [N,K] (= output columns of y) are partitioned
+ *
+ *     [0, n_res)              resident in HBM, GEMV on the GPU
+ *     [n_res, n_res+n_str)    streamed from pinned host memory in chunks
+ *                             over the host link, GEMV per arriving chunk
+ *     [n_res+n_str, N)        computed by host CPU threads
+ *
+ * and the three partial outputs land in their own columns of y (the paper's
+ * concatenation).  n_str = G * floor(alpha * (N-n_res)/G + 0.5):
+ * alpha is the GPU's share of the host-resident (offloaded) rows (
+ * DESIGN.md readings R1-R4).
+ *
+ * Conventions shared by every entry point
+ * ---------------------------------------
+ * Types / layouts: W is [N,K] row-major bf16 (nn.Linear.weight layout), x is
+ *   [B,K] row-major bf16, y is [B,N] row-major fp32, bias is fp32 [N].  bf16 is
+ *   passed as `const void *` (uint16 bit patterns).  `stream` is a cudaStream_t
+ *   passed as `void *` (NULL = legacy default stream).
+ * Ownership: the caller owns every buffer it passes (x, W_dev, W_host, bias, y,
+ *   h) and keeps it alive until `stream` has passed the call.  The library owns
+ *   only its context internals (streams, events, device ring, pinned bounce
+ *   buffers, thread pool) and never frees or retains caller memory.
+ * Validation happens before anything is enqueued; an argument error leaves no
+ *   partial work.  Pointer kinds are checked with cudaPointerGetAttributes:
+ *   W_host must be page-locked host memory (HG_ENOTPINNED), device pointers must
+ *   be device memory of the context's device (HG_ENOTDEVICE); every pointer
+ *   16-byte aligned and K % 8 == 0 (HG_EALIGN); N % G == 0, n_res % G == 0,
+ *   0 <= alpha <= 1 (not NaN), 1 <= batch <= HG_MAX_BATCH (HG_EINVAL).
+ * Synchronisation: hg_linear / hg_layer / hg_stack are host-blocking for the
+ *   CPU slice (they return after the CPU rows are computed and their
+ *   host->device copy is enqueued) and stream-ordered for the GPU side: y (or h)
+ *   is complete when `stream` passes the call.
+ * Errors: no C++ exception crosses the ABI.  A CUDA/NCCL failure mid-call
+ *   returns HG_ECUDA / HG_ENCCL and puts the context in an error state (later
+ *   calls return HG_ESTATE until hg_destroy).  Host waits are bounded
+ *   (HG_ETIMEOUT, hg_config.timeout_s).  hg_last_error() gives a thread-local
+ *   message for the last failure on the calling thread.
+ * Threading: one context per (device, host thread); a context is not
+ *   re-entrant.  hg_plan is pure and thread-safe.
+ */
+#ifndef HG_H_
+#define HG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define HG_API __attribute__((visibility("default")))
+#else
+#define HG_API
+#endif
+
+#define HG_MAX_BATCH 8
+#define HG_ABI_VERSION 1
+
+typedef enum {
+    HG_OK = 0,
+    HG_EINVAL = -1,      /* bad shape / value argument                      */
+    HG_ENOTPINNED = -2,  /* host pointer is pageable (not page-locked)      */
+    HG_ENOTDEVICE = -3,  /* pointer is not device memory of this context    */
+    HG_EALIGN = -4,      /* pointer not 16-byte aligned or K % 8 != 0       */
+    HG_ECUDA = -5,       /* CUDA runtime/driver error (context now unusable) */
+    HG_ENCCL = -6,       /* NCCL error (context now unusable)               */
+    HG_ENOMEM = -7,      /* allocation failed                               */
+    HG_ESTATE = -8,      /* context in error state / not initialised        */
+    HG_ETIMEOUT = -9,    /* a bounded host wait expired                     */
+    HG_EUNSUPPORTED = -10
+} hg_status;
+
+/* How hg_plan derives alpha.  V_X are "parameter size divided by processing
+ * time": bytes of weight per second.  T'_X = W/V_X is the duration of the
+ * whole operation on lane X, W = 2*K*(N-n_res) bytes. */
+typedef enum {
+    HG_ALPHA_EXACT = 0,  /* Eq. (5): 1/(V_CPU/V_COM + V_CPU/V_GPU + 1)         */
+    HG_ALPHA_APPROX = 1, /* Eq. (6): V_COM/(V_COM + V_CPU)                    */
+    HG_ALPHA_TPRIME = 2, /* Eq. (7): T'_CPU/(T'_CPU + T'_COM)                  */
+    HG_ALPHA_ASYNC = 3,  /* Eq. (9): T'_CPU/(T'_CPU + max(T'_PIN, T'_TRANS))      */
+    HG_ALPHA_FIXED = 4   /* alpha given by the caller                                     */
+} hg_alpha_mode;
+
+/* Measured lane speeds (bytes of weight / s) and roofline peaks (bytes / s).
+ * v_pin = +inf when host weights are page-locked once at load (reading R7). */
+typedef struct {
+    double v_cpu;   /* host-thread GEMV rate over W bytes                     (V_CPU) */
+    double v_gpu;   /* device GEMV rate over W bytes                          (V_GPU) */
+    double v_link;  /* host->device copy rate of pinned W chunks      (V_COM=V_TRANS) */
+    double v_pin;   /* page-lock rate (+inf when pre-pinned)                  (V_PIN) */
+    double b_hbm;   /* HBM roofline peak                                             */
+    double b_link;  /* host-link roofline peak                                       */
+    double b_cpu;   /* host-DRAM roofline peak for the CPU lane's threads            */
+} hg_rates;
+
+/* The per-linear plan.  Integers are exact;
+ * times are seconds for one call at batch `batch`. */
+typedef struct {
+    int64_t N, K;
+    int64_t batch;
+    int64_t n_res, n_str, n_cpu; /* row partition, n_res+n_str+n_cpu == N                  */
+    int64_t granule;             /* G: every slice is a multiple of G rows                */
+    int64_t chunk_rows;          /* C = G*max(1, floor(chunk_bytes/(G*K*2)))              */
+    int64_t n_chunks;            /* ceil(n_str / C)                                       */
+    double alpha_req;            /* alpha from the mode (Eq. 5/6/7/9 or fixed)            */
+    double alpha_eff;            /* n_str / (N - n_res), 0 when N == n_res                */
+    double t_cpu, t_link, t_gpu; /* lane times at the measured rates                      */
+    double t_eq4;                /* paper's serial form: max(t_cpu, t_link + GEMV(str))   */
+    double t_pred;               /* pipelined form: max(t_cpu, t_link + t_tail, t_gpu)    */
+    double t_hbm;                /* (2K n_res + 2*2K n_str) / b_hbm                        */
+    double t_roof;               /* max(t_hbm, 2K n_str / b_link, 2K n_cpu / b_cpu)        */
+} hg_plan_t;
+
+typedef struct {
+    int64_t granule;     /* G (default 128; tests use 1)                                 */
+    int64_t chunk_bytes; /* streamed chunk target (default 16 MiB)                       */
+    int64_t ring_bytes;  /* device staging ring for streamed chunks (default 1 GiB)      */
+    int64_t max_k;       /* largest K the context will see (default 65536)               */
+    int64_t max_n;       /* largest N (default 131072)                                   */
+    int32_t cpu_threads; /* host GEMV threads incl. the caller (0 = all online cores)    */
+    int32_t cpu_first;   /* first core to pin pool threads to (-1 = no pinning)          */
+    int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
+    int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
+    double timeout_s;    /* bound on every host wait (default 60 s)                      */
+} hg_config;
+
+/* Lane breakdown of the last hg_linear / hg_layer / hg_stack call (Table 2
+ * analogue).  Busy times from CUDA events (link, gpu) and host
+ * clocks (cpu); fractions are busy / wall. */
+typedef struct {
+    double wall_s;          /* host wall time of the call (enqueue to GPU completion)   */
+    double cpu_busy_s;      /* host GEMV time (sum over linears)                        */
+    double link_busy_s;     /* H2D chunk copy time (collect_stats=1)                    */
+    double gpu_busy_s;      /* GEMV kernel time, resident + streamed (collect_stats=1)  */
+    double x_wait_s;        /* host time waiting for activations to reach the host     */
+    int64_t bytes_res;      /* W bytes read by resident GEMVs                           */
+    int64_t bytes_str;      /* W bytes streamed over the link                           */
+    int64_t bytes_cpu;      /* W bytes read by the CPU lane                             */
+    int64_t n_chunks;       /* streamed chunks consumed                                 */
+    int64_t n_linears;
+    int64_t gpu_launches;   /* kernels this library launched                            */
+} hg_stats_t;
+
+typedef struct hg_ctx hg_ctx;
+
+/* One heterogeneous linear of a layer: this rank's rows of W.
+ *   W_dev  [n_res, K] device (NULL iff n_res == 0)
+ *   W_host [N_local - n_res, K] page-locked host (NULL iff n_res == N_local)
+ *   bias   [N_local] device fp32 or NULL
+ * plan: a plan from hg_plan for (N_local, K) (alpha_mode and rates are only
+ * consulted through it). */
+typedef struct {
+    const void *W_dev;
+    const void *W_host;
+    const float *bias;
+    hg_plan_t plan;
+} hg_linear_desc;
+
+/* One OPT pre-LN decoder layer (reading R22).  lin[0..3] =
+ * {qkv [3H,H], o [H,H], fc1 [F,H], fc2 [H,F]}; with P ranks each rank's
+ * descriptors hold its row shard (N/P rows).  LN parameters are device fp32 [H]
+ * or NULL (gamma = 1, beta = 0). */
+typedef struct {
+    int64_t hidden, ffn;
+    hg_linear_desc lin[4];
+    const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+} hg_opt_layer;
+
+/* Optional per-step device copies of a layer's intermediates (teacher-forced
+ * parity tests).  Every pointer is device memory or NULL (skipped). */
+typedef struct {
+    void *a;      /* bf16 [B,H]   LN1(h)                        input of qkv */
+    float *y_qkv; /* fp32 [B,3H]                                             */
+    void *v;      /* bf16 [B,H]   attention output at position 0 input of o  */
+    float *y_o;   /* fp32 [B,H]                                              */
+    void *h1;     /* bf16 [B,H]   h + y_o                                    */
+    void *a2;     /* bf16 [B,H]   LN2(h1)                       input of fc1 */
+    float *y_fc1; /* fp32 [B,F]                                              */
+    void *u;      /* bf16 [B,F]   ReLU(y_fc1)                   input of fc2 */
+    float *y_fc2; /* fp32 [B,H]                                              */
+} hg_layer_trace;
+
+/* ---------------------------------------------------------------- lifetime */
+HG_API int hg_abi_version(void);
+HG_API const char *hg_last_error(void);
+HG_API hg_status hg_config_default(hg_config *cfg);
+
+/* Create a context on CUDA device `device` (>= 0), or a host-only context
+ * (device = -1: thread pool and hg_host_gemv only, no CUDA calls at all). */
+HG_API hg_status hg_create(hg_ctx **ctx, int device, const hg_config *cfg);
+HG_API hg_status hg_destroy(hg_ctx *ctx);
+
+/* ---------------------------------------------------------------- a1: plan */
+/* Pure function, no device work.  Fills *out for one
+ * linear of N rows x K, batch, n_res resident rows.  alpha_fixed is used only by
+ * HG_ALPHA_FIXED.  Errors: HG_EINVAL for N % G, n_res % G, n_res > N, K <= 0,
+ * granule < 1, chunk_bytes < 1, a non-positive / NaN rate used by the mode, or
+ * alpha outside [0,1]. */
+HG_API hg_status hg_plan(const hg_rates *rates, int64_t N, int64_t K, int batch, int64_t n_res,
+                         int mode, double alpha_fixed, int64_t granule, int64_t chunk_bytes,
+                         hg_plan_t *out);
+
+/* Probe the lane speeds on this context (Fig. 1's "parameter size divided by
+ * processing time"; the alpha benchmark's measurements).
+ *   W_host: page-locked [N, K] bf16 weight to measure on (a real linear).
+ *   flags bit 0: measure the CPU lane while the link is busy (shared host DRAM).
+ * Fills v_cpu, v_gpu, v_link, b_link (large-chunk copy), b_cpu (host read rate
+ * of the pool threads), b_hbm (device read rate); v_pin = +inf. */
+HG_API hg_status hg_measure(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch,
+                            int flags, hg_rates *out);
+
+/* ---------------------------------------------------------------- a2-a6: one linear */
+/* y[:, 0:N) = x . W^T (+ bias) with the rows of W split by `alpha`:
+ *   x_dev [batch, K] bf16 device; W_dev [n_res, K] device (NULL iff n_res == 0);
+ *   W_host [N - n_res, K] page-locked host (NULL iff n_res == N);
+ *   bias_dev [N] fp32 device or NULL; y_dev [batch, N] fp32 device.
+ * Partition from the same function hg_plan exports, with the context's granule
+ * and chunk_bytes. */
+HG_API hg_status hg_linear(hg_ctx *ctx, const void *x_dev, int batch, int64_t N, int64_t K,
+                           const void *W_dev, int64_t n_res, const void *W_host, double alpha,
+                           const float *bias_dev, float *y_dev, void *stream);
+
+/* Same, with an explicit plan (from hg_plan with this N, K). */
+HG_API hg_status hg_linear_planned(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
+                                   const void *W_dev, const void *W_host, const float *bias_dev,
+                                   float *y_dev, void *stream);
+
+/* ---------------------------------------------------------------- a7: layer / stack */
+/* One OPT decoder layer in place on h_dev [batch, hidden] bf16 device.  Linear
+ * outputs are fp32; bf16 storage after LN, attention, ReLU and residual adds
+ * (reading R22).  trace may be NULL. */
+HG_API hg_status hg_layer(hg_ctx *ctx, const hg_opt_layer *layer, void *h_dev, int batch,
+                          hg_layer_trace *trace, void *stream);
+
+/* n_layers layers back to back (one decode step of the linear stack).  The
+ * copy stream runs ahead across linears and layers into the device ring
+ * (prefetching; "pin the next weight"); with
+ * cfg.wrap_prefetch it continues into layer 0 of the next call. */
+HG_API hg_status hg_stack(hg_ctx *ctx, const hg_opt_layer *layers, int n_layers, void *h_dev,
+                          int batch, void *stream);
+
+/* ---------------------------------------------------------------- lanes alone */
+/* Device GEMV alone (the resident/streamed kernel): y[b*ldy + j] = x[b,:].W[j,:] (+bias[j]),
+ * j < n.  All device pointers.  Same kernel and reduction order hg_linear uses. */
+HG_API hg_status hg_gemv(hg_ctx *ctx, const void *x_dev, int batch, int64_t n, int64_t K,
+                         const void *W_dev, const float *bias_dev, float *y_dev, int64_t ldy,
+                         void *stream);
+
+/* CPU lane alone: y_host[b*n + j] = x_host[b,:] . W_host[j,:] (+ bias_host[j]) on
+ * the context's thread pool.  All host pointers (need not be pinned).  Works on
+ * host-only contexts. */
+HG_API hg_status hg_host_gemv(hg_ctx *ctx, const void *x_host, int batch, int64_t n, int64_t K,
+                              const void *W_host, const float *bias_host, float *y_host);
+
+/* Name of the host GEMV code path selected at run time ("avx512bf16", "avx2", "scalar"). */
+HG_API const char *hg_host_isa(void);
+
+/* ---------------------------------------------------------------- a8: multi-GPU */
+/* Column-sharded tensor parallelism (BJ:5; not in the paper, which uses one GPU,
+ * P:315).  Rank p owns W rows [pN/P, (p+1)N/P) of every linear; after each
+ * linear the shards are all-gathered over NVLink with NCCL.
+ *   hg_dist_unique_id: fills 128 bytes (ncclUniqueId) on rank 0, to be broadcast
+ *   by the caller (e.g. through torch.distributed); hg_dist_init creates the
+ *   communicator on every rank.  NCCL is loaded at run time (HG_ENCCL if absent). */
+HG_API hg_status hg_dist_unique_id(void *id128);
+HG_API hg_status hg_dist_init(hg_ctx *ctx, int nranks, int rank, const void *id128);
+/* This rank's shard linear, then all-gather: y_full_dev [batch, N_full] fp32.
+ * plan is this rank's plan for (N_full/P, K). */
+HG_API hg_status hg_linear_sharded(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
+                                   const void *W_dev, const void *W_host, const float *bias_dev,
+                                   float *y_full_dev, void *stream);
+
+/* ---------------------------------------------------------------- stats */
+HG_API hg_status hg_stats(hg_ctx *ctx, hg_stats_t *out);
+HG_API hg_status hg_reset_stats(hg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HG_H_ */

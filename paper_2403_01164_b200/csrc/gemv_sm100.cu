@@ -1,0 +1,256 @@
+// gemv_sm100.cu -- device GEMV for the resident and streamed slices
+// (SURVEY 8(a) a3/a4): y[b, j] = sum_k x[b,k] * W[j,k] (+ bias[j]), B = 1..8.
+//
+// The GPU share of a heterogeneous linear ("The GPU, in turn, generates
+// results once the communication process is completed"), run over HBM-resident
+// rows and over each streamed chunk as it lands in the device ring.  At batch
+// 1-8 the arithmetic intensity is B flop/byte, >= 30x below the B200 ridge, so
+// the kernel is an HBM stream: 128-bit non-allocating loads of W along K, x
+// staged once per CTA in shared memory, fp32 FMAs, warp-shuffle reductions.
+//
+// Deterministic split-K: the K axis is cut into S slices whose length depends
+// on K only (gemv_geom).  Every output element is the same sequence of fp32
+// operations whichever launch computes it (resident GEMV, any chunk, any n),
+// so all GPU partitions are bit-identical (SURVEY 8(c) c4 "split invariance").
+// The S partials of a row tile are summed in slice order by the last CTA to
+// finish that tile (counter + threadfence), in the same kernel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "hg_internal.h"
+
+namespace hg {
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int64_t kSliceMax = 4096;  // elements of K per slice (8 KB of one W row)
+
+template <int B>
+struct Tile {
+    static constexpr int RT = B <= 4 ? 4 : 2;  // W rows per warp (share each x load)
+    static constexpr int U = B <= 4 ? 2 : 2;   // 16-byte W loads in flight per row per lane
+    static constexpr int ROWS = kWarps * RT;   // rows per CTA
+};
+
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ float lo_f(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float hi_f(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
+__device__ __forceinline__ void fma8(float &acc, const uint4 &w, const float (&xf)[8]) {
+    acc = fmaf(lo_f(w.x), xf[0], acc);
+    acc = fmaf(hi_f(w.x), xf[1], acc);
+    acc = fmaf(lo_f(w.y), xf[2], acc);
+    acc = fmaf(hi_f(w.y), xf[3], acc);
+    acc = fmaf(lo_f(w.z), xf[4], acc);
+    acc = fmaf(hi_f(w.z), xf[5], acc);
+    acc = fmaf(lo_f(w.w), xf[6], acc);
+    acc = fmaf(hi_f(w.w), xf[7], acc);
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// grid = (ceil(n / ROWS), S); block = 256; dynamic smem = B * ks * 2 bytes.
+template <int B>
+__global__ void __launch_bounds__(kThreads)
+    gemv_bf16_kernel(const uint4 *__restrict__ x, int64_t K, const uint4 *__restrict__ W, int64_t n,
+                     const float *__restrict__ bias, float *__restrict__ y, int64_t ldy, int64_t ks,
+                     int S, float *__restrict__ ws, int *__restrict__ counters) {
+    using T = Tile<B>;
+    extern __shared__ uint4 xs[];  // [B][kv]
+    __shared__ int s_last;
+
+    const int s = blockIdx.y;
+    const int64_t k0 = (int64_t)s * ks;
+    const int64_t klen = (K - k0) < ks ? (K - k0) : ks;
+    const int kv = (int)(klen >> 3);  // uint4 per row in this slice
+    const int64_t Kv = K >> 3;
+
+    for (int i = threadIdx.x; i < B * kv; i += kThreads) {
+        const int b = i / kv, j = i - b * kv;
+        xs[i] = x[b * Kv + (k0 >> 3) + j];
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t row0 = (int64_t)blockIdx.x * T::ROWS + warp * T::RT;
+    const uint4 *wp[T::RT];
+#pragma unroll
+    for (int r = 0; r < T::RT; ++r) {
+        int64_t rr = row0 + r < n ? row0 + r : n - 1;
+        wp[r] = W + rr * Kv + (k0 >> 3);
+    }
+    float acc[T::RT][B];
+#pragma unroll
+    for (int r = 0; r < T::RT; ++r)
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[r][b] = 0.f;
+
+    for (int j = lane; j < kv; j += 32 * T::U) {
+        uint4 wv[T::U][T::RT];
+#pragma unroll
+        for (int u = 0; u < T::U; ++u)
+#pragma unroll
+            for (int r = 0; r < T::RT; ++r)
+                if (j + 32 * u < kv) wv[u][r] = ldg_stream(wp[r] + j + 32 * u);
+#pragma unroll
+        for (int u = 0; u < T::U; ++u) {
+            if (j + 32 * u < kv) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const uint4 xv = xs[b * kv + j + 32 * u];
+                    const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
+                                         lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+#pragma unroll
+                    for (int r = 0; r < T::RT; ++r) fma8(acc[r][b], wv[u][r], xf);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < T::RT; ++r)
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[r][b] = warp_sum(acc[r][b]);
+
+    if (S == 1) {
+        if (lane == 0) {
+#pragma unroll
+            for (int r = 0; r < T::RT; ++r) {
+                const int64_t row = row0 + r;
+                if (row < n) {
+                    const float bb = bias ? bias[row] : 0.f;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) y[b * ldy + row] = acc[r][b] + bb;
+                }
+            }
+        }
+        return;
+    }
+    // split-K: partial of slice s -> ws[(s*B + b)*n + row]
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < T::RT; ++r) {
+            const int64_t row = row0 + r;
+            if (row < n) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) ws[((int64_t)s * B + b) * n + row] = acc[r][b];
+            }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int prev = atomicAdd(&counters[blockIdx.x], 1);
+        s_last = (prev == S - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    for (int i = threadIdx.x; i < B * T::ROWS; i += kThreads) {
+        const int b = i / T::ROWS;
+        const int64_t row = (int64_t)blockIdx.x * T::ROWS + (i - b * T::ROWS);
+        if (row < n) {
+            float sum = 0.f;
+            for (int q = 0; q < S; ++q) sum += __ldcg(&ws[((int64_t)q * B + b) * n + row]);
+            y[b * ldy + row] = sum + (bias ? bias[row] : 0.f);
+        }
+    }
+    if (threadIdx.x == 0) counters[blockIdx.x] = 0;  // ready for the next launch on this stream
+}
+
+template <int B>
+int launch_b(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
+             int64_t ldy, float *ws, int *counters, cudaStream_t st) {
+    const GemvGeom g = gemv_geom(K, B);
+    const size_t smem = (size_t)B * (size_t)g.ks * 2;
+    dim3 grid((unsigned)((n + Tile<B>::ROWS - 1) / Tile<B>::ROWS), (unsigned)g.s);
+    gemv_bf16_kernel<B><<<grid, kThreads, smem, st>>>(
+        (const uint4 *)x, K, (const uint4 *)W, n, bias, y, ldy, g.ks, g.s, ws, counters);
+    return (int)cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- read-BW probe
+__global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float *sink) {
+    uint32_t acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        uint4 v = ldg_stream(p + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9e3779b9u) sink[0] = (float)acc;  // practically never; keeps loads live
+}
+
+}  // namespace
+
+GemvGeom gemv_geom(int64_t K, int batch) {
+    GemvGeom g;
+    const int64_t s0 = (K + kSliceMax - 1) / kSliceMax;
+    int64_t ks = (K + s0 - 1) / s0;
+    ks = (ks + 7) / 8 * 8;
+    g.ks = ks;
+    g.s = (int)((K + ks - 1) / ks);
+    g.rows_per_cta = kWarps * (batch <= 4 ? 4 : 2);
+    return g;
+}
+
+int64_t gemv_ws_floats(int64_t n, int64_t K, int batch) {
+    const GemvGeom g = gemv_geom(K, batch);
+    return g.s > 1 ? (int64_t)g.s * batch * n : 0;
+}
+
+int64_t gemv_counters(int64_t n, int64_t K, int batch) {
+    const GemvGeom g = gemv_geom(K, batch);
+    return (n + g.rows_per_cta - 1) / g.rows_per_cta;
+}
+
+int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
+                float *y, int64_t ldy, float *ws, int *counters, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (batch) {
+        case 1: return launch_b<1>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 2: return launch_b<2>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 3: return launch_b<3>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 4: return launch_b<4>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 5: return launch_b<5>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 6: return launch_b<6>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 7: return launch_b<7>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 8: return launch_b<8>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        default: return (int)cudaErrorInvalidValue;
+    }
+}
+
+template <int B>
+int prepare_b() {
+    return (int)cudaFuncSetAttribute(gemv_bf16_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)(B * kSliceMax * 2));
+}
+
+int gemv_prepare() {
+    int e = 0;
+    e |= prepare_b<1>(); e |= prepare_b<2>(); e |= prepare_b<3>(); e |= prepare_b<4>();
+    e |= prepare_b<5>(); e |= prepare_b<6>(); e |= prepare_b<7>(); e |= prepare_b<8>();
+    return e;
+}
+
+int launch_read_bw(const void *p, int64_t bytes, float *sink, void *stream) {
+    int64_t nvec = bytes / 16;
+    read_bw_kernel<<<148 * 8, 512, 0, (cudaStream_t)stream>>>((const uint4 *)p, nvec, sink);
+    return (int)cudaGetLastError();
+}
+
+}  // namespace hg

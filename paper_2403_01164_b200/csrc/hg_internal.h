@@ -1,0 +1,88 @@
+// hg_internal.h -- declarations shared by the library's translation units.
+// Not part of the ABI (include/hg.h is).
+#pragma once
+
+#include <cstdarg>
+#include <cstdint>
+
+#include "hg.h"
+
+namespace hg {
+
+// ---------------------------------------------------------------- errors
+// Thread-local last-error message; returns `st` so call sites can `return set_error(...)`.
+hg_status set_error(hg_status st, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+
+// ---------------------------------------------------------------- plan.cpp
+hg_status partition_rows(int64_t N, int64_t n_res, double alpha, int64_t G, int64_t *n_str,
+                         int64_t *n_cpu);
+int64_t chunk_rows_for(int64_t K, int64_t G, int64_t chunk_bytes);
+
+// ---------------------------------------------------------------- gemv_sm100.cu
+// Deterministic split-K geometry: depends on K only, so every output element is
+// reduced in the same order whichever launch (resident / chunk) computes it.
+struct GemvGeom {
+    int64_t ks;      // k-slice length (elements, multiple of 256 unless == K)
+    int s;           // number of k-slices
+    int rows_per_cta;
+};
+GemvGeom gemv_geom(int64_t K, int batch);
+// Workspace floats and counters needed for one launch over n rows.
+int64_t gemv_ws_floats(int64_t n, int64_t K, int batch);
+int64_t gemv_counters(int64_t n, int64_t K, int batch);
+// Launch: y[b*ldy + j] = sum_k x[b,k] W[j,k] (+bias[j]), j < n.  Returns a CUDA error code (int).
+int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
+                float *y, int64_t ldy, float *ws, int *counters, void *stream);
+
+// ---------------------------------------------------------------- glue_sm100.cu
+int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,
+                const float *bias, void *stream);
+int launch_layernorm(const void *h, int64_t H, int batch, const float *g, const float *b, void *out,
+                     void *stream);
+int launch_slice_to_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch,
+                         void *out, void *stream);
+int launch_residual_ln(const void *h, const float *y, int64_t H, int batch, void *h1,
+                       const float *g, const float *b, void *a2, void *stream);
+int launch_relu_bf16(const float *y, int64_t n, int batch, void *out, void *stream);
+int launch_residual(const void *h1, const float *y, int64_t H, int batch, void *out, void *stream);
+int launch_gather_permute(const float *gbuf, int P, int batch, int64_t n_local, float *y,
+                          void *stream);
+int launch_read_bw(const void *p, int64_t bytes, float *sink, void *stream);
+
+// ---------------------------------------------------------------- host_gemv*.cpp
+// One block of rows [r0, r1) of the CPU lane: y[b*ldy + (r - r0) + yoff] ...
+typedef void (*host_rows_fn)(const uint16_t *x, int batch, int64_t K, const uint16_t *W,
+                             int64_t r0, int64_t r1, const float *bias, float *y, int64_t ldy);
+void host_rows_avx512bf16(const uint16_t *x, int batch, int64_t K, const uint16_t *W, int64_t r0,
+                          int64_t r1, const float *bias, float *y, int64_t ldy);
+void host_rows_avx2(const uint16_t *x, int batch, int64_t K, const uint16_t *W, int64_t r0,
+                    int64_t r1, const float *bias, float *y, int64_t ldy);
+void host_rows_scalar(const uint16_t *x, int batch, int64_t K, const uint16_t *W, int64_t r0,
+                      int64_t r1, const float *bias, float *y, int64_t ldy);
+host_rows_fn host_rows_select(const char **name);
+// Host read-bandwidth kernel (probe): returns a checksum so the loads are not elided.
+uint64_t host_read_avx512(const void *p, int64_t bytes);
+
+// ---------------------------------------------------------------- threadpool.cpp
+class ThreadPool;
+ThreadPool *pool_create(int nthreads, int first_core);
+void pool_destroy(ThreadPool *p);
+int pool_size(const ThreadPool *p);
+// Run fn(arg, worker_index) on every worker (the caller is worker 0); returns when all finished.
+void pool_run(ThreadPool *p, void (*fn)(void *, int), void *arg);
+
+}  // namespace hg
+
+namespace hg {
+// ---------------------------------------------------------------- dist.cpp (NCCL, dlopen'ed)
+struct Dist;
+hg_status dist_unique_id(void *id128);
+Dist *dist_create(int nranks, int rank, const void *id128, hg_status *st);
+void dist_destroy(Dist *d);
+int dist_nranks(const Dist *d);
+int dist_rank(const Dist *d);
+hg_status dist_allgather(Dist *d, const float *send, float *recv, size_t count_per_rank,
+                         void *stream);
+// gemv kernel attributes (dynamic smem) for the current device
+int gemv_prepare();
+}  // namespace hg

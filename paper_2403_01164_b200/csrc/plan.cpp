@@ -1,0 +1,124 @@
+// plan.cpp -- hg_plan: split ratio alpha, integer row partition, chunk schedule,
+// predicted and roofline times.
+//
+// Pure host arithmetic in IEEE fp64.  Compiled with -ffp-contract=off so that
+// "alpha * m + 0.5" is one rounded multiply and one rounded add (no FMA), the
+// contract the oracle and the tests fix for the integer partition (DESIGN.md
+// reading R3).
+#include <cmath>
+#include <cstring>
+
+#include "hg.h"
+#include "hg_internal.h"
+
+namespace hg {
+
+// Eq. (5), second form: alpha = 1 / (V_CPU/V_COM + V_CPU/V_GPU + 1).
+// This form stays finite when a rate is +inf (a free lane).
+static double alpha_exact(double v_cpu, double v_gpu, double v_com) {
+    return 1.0 / (v_cpu / v_com + v_cpu / v_gpu + 1.0);
+}
+// Eq. (6): GPU term dropped.
+static double alpha_approx(double v_cpu, double v_com) { return v_com / (v_com + v_cpu); }
+// Eq. (7) with whole-operation durations T'.
+static double alpha_tprime(double t_cpu, double t_com) { return t_cpu / (t_cpu + t_com); }
+// Eq. (9): communication split into pinning and transfer.
+static double alpha_async(double t_cpu, double t_pin, double t_trans) {
+    return t_cpu / (t_cpu + (t_pin > t_trans ? t_pin : t_trans));
+}
+
+static bool pos_rate(double v) { return v > 0.0 && !std::isnan(v); }
+
+hg_status partition_rows(int64_t N, int64_t n_res, double alpha, int64_t G, int64_t *n_str,
+                         int64_t *n_cpu) {
+    if (G < 1 || N < 0 || N % G != 0 || n_res % G != 0 || n_res < 0 || n_res > N)
+        return set_error(HG_EINVAL, "partition: need N %% G == 0, n_res %% G == 0, 0 <= n_res <= N "
+                                    "(N=%lld n_res=%lld G=%lld)",
+                         (long long)N, (long long)n_res, (long long)G);
+    if (!(alpha >= 0.0 && alpha <= 1.0))
+        return set_error(HG_EINVAL, "partition: alpha %g outside [0,1]", alpha);
+    const int64_t m = (N - n_res) / G;           // granules of offloaded rows
+    volatile double prod = alpha * (double)m;   // one rounded multiply
+    volatile double sum = prod + 0.5;           // one rounded add
+    const int64_t g_str = (int64_t)std::floor(sum);
+    *n_str = G * g_str;
+    *n_cpu = N - n_res - *n_str;
+    return HG_OK;
+}
+
+int64_t chunk_rows_for(int64_t K, int64_t G, int64_t chunk_bytes) {
+    int64_t per_granule = G * K * 2;
+    int64_t g = chunk_bytes / per_granule;
+    return G * (g < 1 ? 1 : g);
+}
+
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" HG_API hg_status hg_plan(const hg_rates *r, int64_t N, int64_t K, int batch,
+                                    int64_t n_res, int mode, double alpha_fixed, int64_t granule,
+                                    int64_t chunk_bytes, hg_plan_t *out) {
+    if (!r || !out) return set_error(HG_EINVAL, "hg_plan: NULL argument");
+    if (K <= 0 || N <= 0 || granule < 1 || chunk_bytes < 1 || batch < 1 || batch > HG_MAX_BATCH)
+        return set_error(HG_EINVAL, "hg_plan: bad shape (N=%lld K=%lld batch=%d G=%lld chunk=%lld)",
+                         (long long)N, (long long)K, batch, (long long)granule,
+                         (long long)chunk_bytes);
+    if (!pos_rate(r->v_cpu) || !pos_rate(r->v_gpu) || !pos_rate(r->v_link) ||
+        !pos_rate(r->v_pin) || !pos_rate(r->b_hbm) || !pos_rate(r->b_link) ||
+        !pos_rate(r->b_cpu))
+        return set_error(HG_EINVAL, "hg_plan: every rate must be > 0 (inf allowed)");
+    if (N % granule || n_res % granule || n_res < 0 || n_res > N)
+        return set_error(HG_EINVAL, "hg_plan: N and n_res must be multiples of G with n_res <= N");
+
+    const double host_bytes = 2.0 * (double)K * (double)(N - n_res);
+    double a = 0.0;
+    if (N == n_res) {
+        a = 0.0;  // nothing offloaded: alpha has no rows to act on
+    } else {
+        switch (mode) {
+            case HG_ALPHA_EXACT: a = alpha_exact(r->v_cpu, r->v_gpu, r->v_link); break;
+            case HG_ALPHA_APPROX: a = alpha_approx(r->v_cpu, r->v_link); break;
+            case HG_ALPHA_TPRIME:
+                a = alpha_tprime(host_bytes / r->v_cpu, host_bytes / r->v_link);
+                break;
+            case HG_ALPHA_ASYNC:
+                a = alpha_async(host_bytes / r->v_cpu, host_bytes / r->v_pin,
+                                host_bytes / r->v_link);
+                break;
+            case HG_ALPHA_FIXED: a = alpha_fixed; break;
+            default: return set_error(HG_EINVAL, "hg_plan: unknown alpha mode %d", mode);
+        }
+    }
+    int64_t n_str = 0, n_cpu = 0;
+    hg_status st = partition_rows(N, n_res, a, granule, &n_str, &n_cpu);
+    if (st != HG_OK) return st;
+
+    hg_plan_t p;
+    std::memset(&p, 0, sizeof p);
+    p.N = N;
+    p.K = K;
+    p.batch = batch;
+    p.n_res = n_res;
+    p.n_str = n_str;
+    p.n_cpu = n_cpu;
+    p.granule = granule;
+    p.chunk_rows = chunk_rows_for(K, granule, chunk_bytes);
+    p.n_chunks = (n_str + p.chunk_rows - 1) / p.chunk_rows;
+    p.alpha_req = a;
+    p.alpha_eff = (N == n_res) ? 0.0 : (double)n_str / (double)(N - n_res);
+
+    const double row = 2.0 * (double)K;  // bytes of W per output row
+    p.t_cpu = row * (double)n_cpu / r->v_cpu;
+    p.t_link = row * (double)n_str / r->v_link;
+    p.t_gpu = row * (double)(n_res + n_str) / r->v_gpu;
+    const int64_t last = n_str - (p.n_chunks > 0 ? (p.n_chunks - 1) * p.chunk_rows : 0);
+    const double t_tail = row * (double)last / r->v_gpu;
+    p.t_eq4 = std::fmax(p.t_cpu, p.t_link + row * (double)n_str / r->v_gpu);
+    p.t_pred = std::fmax(p.t_cpu, std::fmax(p.t_link + t_tail, p.t_gpu));
+    p.t_hbm = (row * (double)n_res + 2.0 * row * (double)n_str) / r->b_hbm;
+    p.t_roof = std::fmax(p.t_hbm, std::fmax(row * (double)n_str / r->b_link,
+                                            row * (double)n_cpu / r->b_cpu));
+    *out = p;
+    return HG_OK;
+}

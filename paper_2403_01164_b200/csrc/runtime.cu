@@ -1,0 +1,999 @@
+// runtime.cu -- the heterogeneous offloaded linear on one B200.
+//
+// Per linear (Fig. 5c "hybrid heterogeneous parallelism"):
+//   a2  x -> pinned host bounce (D2H on the caller's stream, event ev_x)
+//   a3  resident GEMV over W_dev rows [0, n_res)                       (HBM-bound)
+//   a4  streamed rows: the copy stream moves chunk c of W_host into a slot of a
+//       device ring (cudaMemcpyAsync, copy engine) while the compute stream
+//       runs the GEMV of chunk c-1; per-slot events order arrival -> GEMV ->
+//       slot reuse.  The copy stream runs ahead across linears (prefetching,
+//       P:127; "pin the next weight in the upcoming layer").
+//   a5  CPU rows: once x is on the host, the thread pool computes them
+//       ("while CPU computation is underway, model parameters are
+//       conveyed to the GPU")
+//   a6  join: y_cpu -> device, added with bias into its columns of y (concat)
+//   a7  layer glue on the GPU between linears
+//   a8  (P>1) all-gather of the row shards over NVLink (NCCL)
+#include <cuda_runtime.h>
+#include <immintrin.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <vector>
+
+#include "hg.h"
+#include "hg_internal.h"
+
+namespace hg {
+
+static thread_local char g_err[512] = "";
+
+hg_status set_error(hg_status st, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof g_err, fmt, ap);
+    va_end(ap);
+    return st;
+}
+
+namespace {
+
+using clk = std::chrono::steady_clock;
+inline double secs(clk::time_point a, clk::time_point b) {
+    return std::chrono::duration<double>(b - a).count();
+}
+
+struct ChunkReq {
+    const uint8_t *src;
+    int64_t bytes;
+    bool operator==(const ChunkReq &o) const { return src == o.src && bytes == o.bytes; }
+};
+
+struct Inflight {
+    ChunkReq req;
+    int slot;
+};
+
+struct HostJob {
+    host_rows_fn fn;
+    const uint16_t *x;
+    int batch;
+    int64_t K, n;
+    const uint16_t *W;
+    const float *bias;
+    float *y;
+    int64_t ldy;
+    int64_t block;
+    std::atomic<int64_t> next;
+};
+
+void host_job_run(void *a, int) {
+    HostJob *j = (HostJob *)a;
+    const int64_t nblk = (j->n + j->block - 1) / j->block;
+    for (;;) {
+        const int64_t b = j->next.fetch_add(1, std::memory_order_relaxed);
+        if (b >= nblk) break;
+        const int64_t r0 = b * j->block;
+        const int64_t r1 = r0 + j->block < j->n ? r0 + j->block : j->n;
+        j->fn(j->x, j->batch, j->K, j->W, r0, r1, j->bias, j->y, j->ldy);
+    }
+}
+
+// One heterogeneous linear, internal form.
+struct Lin {
+    hg_plan_t plan;
+    const void *x;      // device bf16 [B, K]
+    const void *W_dev;  // device [n_res, K]
+    const uint8_t *W_host;  // pinned [N - n_res, K]
+    const float *bias;  // device [N] or null
+    float *y;           // device, row stride ldy
+    int64_t ldy;
+};
+
+}  // namespace
+}  // namespace hg
+
+using namespace hg;
+
+struct hg_ctx {
+    int device = -1;
+    hg_config cfg;
+    ThreadPool *pool = nullptr;
+    host_rows_fn host_fn = nullptr;
+    bool error = false;
+
+    // ---- CUDA resources (device contexts only)
+    cudaStream_t copy = nullptr;
+    uint8_t *ring = nullptr;
+    int64_t slot_bytes = 0;
+    int nslots = 0;
+    std::vector<cudaEvent_t> ev_arrived, ev_free;
+    std::vector<char> slot_used;
+    std::deque<Inflight> inflight;
+    int64_t next_seq = 0;
+    std::vector<ChunkReq> future;
+    size_t fpos = 0;
+    bool fwrap = false;
+
+    uint16_t *x_host = nullptr;   // pinned [max_batch, max_k]
+    float *ycpu_host = nullptr;   // pinned [max_batch, max_n]
+    float *ycpu_dev = nullptr;    // device [max_batch, max_n]
+    cudaEvent_t ev_x = nullptr, ev_ycpu = nullptr, ev_done = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool have_last = false;
+
+    float *ws = nullptr;
+    int64_t ws_floats = 0;
+    int *counters = nullptr;
+    int64_t n_counters = 0;
+    float *sink = nullptr;
+
+    // layer scratch
+    void *act = nullptr;
+    float *yscr = nullptr;
+    void *h1 = nullptr;
+    int64_t act_elems = 0, yscr_elems = 0, h1_elems = 0;
+
+    // multi-GPU
+    Dist *dist = nullptr;
+    float *ylocal = nullptr, *gbuf = nullptr;
+    int64_t ylocal_elems = 0, gbuf_elems = 0;
+
+    // stats
+    hg_stats_t st;
+    std::vector<cudaEvent_t> tev;
+    size_t tev_used = 0;
+    std::vector<std::pair<size_t, size_t>> copy_ev, gemv_ev;
+    cudaEvent_t ev_call0 = nullptr, ev_call1 = nullptr;
+    bool call_timed = false;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- helpers
+#define HG_CK(ctx, expr)                                                                     \
+    do {                                                                                     \
+        cudaError_t e_ = (cudaError_t)(expr);                                                \
+        if (e_ != cudaSuccess) {                                                             \
+            (ctx)->error = true;                                                             \
+            return set_error(HG_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,            \
+                             cudaGetErrorString(e_));                                        \
+        }                                                                                    \
+    } while (0)
+
+#define HG_TRY(expr)                      \
+    do {                                  \
+        hg_status s_ = (expr);            \
+        if (s_ != HG_OK) return s_;       \
+    } while (0)
+
+inline bool aligned(const void *p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+hg_status check_ptr(hg_ctx *c, const void *p, bool want_device, const char *what) {
+    if (!p) return set_error(HG_EINVAL, "%s is NULL", what);
+    cudaPointerAttributes at;
+    cudaError_t e = cudaPointerGetAttributes(&at, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(want_device ? HG_ENOTDEVICE : HG_ENOTPINNED, "%s: %s", what,
+                         cudaGetErrorString(e));
+    }
+    if (want_device) {
+        if (at.type != cudaMemoryTypeDevice || at.device != c->device)
+            return set_error(HG_ENOTDEVICE, "%s is not device memory of device %d", what, c->device);
+    } else {
+        if (at.type != cudaMemoryTypeHost)
+            return set_error(HG_ENOTPINNED, "%s is not page-locked host memory", what);
+    }
+    return HG_OK;
+}
+
+hg_status kerr(hg_ctx *c, int e, const char *what) {
+    if (e != 0) {
+        c->error = true;
+        return set_error(HG_ECUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)e));
+    }
+    return HG_OK;
+}
+
+hg_status wait_event(hg_ctx *c, cudaEvent_t ev, double *waited) {
+    const auto t0 = clk::now();
+    for (int spin = 0;; ++spin) {
+        cudaError_t e = cudaEventQuery(ev);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) {
+            c->error = true;
+            return set_error(HG_ECUDA, "event wait: %s", cudaGetErrorString(e));
+        }
+        for (int i = 0; i < 16; ++i) _mm_pause();
+        if ((spin & 1023) == 1023 && secs(t0, clk::now()) > c->cfg.timeout_s) {
+            c->error = true;
+            return set_error(HG_ETIMEOUT, "event wait exceeded %.1f s", c->cfg.timeout_s);
+        }
+    }
+    if (waited) *waited += secs(t0, clk::now());
+    return HG_OK;
+}
+
+// timing events (collect_stats)
+cudaEvent_t tev_get(hg_ctx *c, size_t *idx) {
+    if (c->tev_used == c->tev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+        c->tev.push_back(e);
+    }
+    *idx = c->tev_used;
+    return c->tev[c->tev_used++];
+}
+
+// ---------------------------------------------------------------- chunk ring
+hg_status issue_copy(hg_ctx *c, const ChunkReq &r) {
+    const int slot = (int)(c->next_seq % c->nslots);
+    if (c->slot_used[slot]) HG_CK(c, cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
+    size_t i0 = 0, i1 = 0;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (c->cfg.collect_stats) {
+        e0 = tev_get(c, &i0);
+        if (e0) HG_CK(c, cudaEventRecord(e0, c->copy));
+    }
+    HG_CK(c, cudaMemcpyAsync(c->ring + (int64_t)slot * c->slot_bytes, r.src, (size_t)r.bytes,
+                             cudaMemcpyHostToDevice, c->copy));
+    HG_CK(c, cudaEventRecord(c->ev_arrived[slot], c->copy));
+    if (c->cfg.collect_stats && e0) {
+        e1 = tev_get(c, &i1);
+        if (e1) {
+            HG_CK(c, cudaEventRecord(e1, c->copy));
+            c->copy_ev.push_back({i0, i1});
+        }
+    }
+    c->slot_used[slot] = 1;
+    c->inflight.push_back({r, slot});
+    ++c->next_seq;
+    return HG_OK;
+}
+
+bool future_next(hg_ctx *c, ChunkReq *out) {
+    if (c->future.empty()) return false;
+    if (c->fpos >= c->future.size()) {
+        if (!c->fwrap) return false;
+        c->fpos = 0;
+    }
+    *out = c->future[c->fpos++];
+    return true;
+}
+
+hg_status pump(hg_ctx *c) {
+    ChunkReq r;
+    while ((int)c->inflight.size() < c->nslots && future_next(c, &r)) HG_TRY(issue_copy(c, r));
+    return HG_OK;
+}
+
+// The slot holding `r`, with `stream` ordered after its arrival.
+hg_status acquire(hg_ctx *c, const ChunkReq &r, cudaStream_t stream, int *slot) {
+    while (!c->inflight.empty() && !(c->inflight.front().req == r)) {
+        // a prefetched chunk nobody will consume (the call sequence changed): free its slot
+        HG_CK(c, cudaEventRecord(c->ev_free[c->inflight.front().slot], c->copy));
+        c->inflight.pop_front();
+    }
+    if (c->inflight.empty()) {
+        // not prefetched: the planned sequence diverged -> restart it here
+        c->future.clear();
+        c->fpos = 0;
+        HG_TRY(issue_copy(c, r));
+    }
+    *slot = c->inflight.front().slot;
+    HG_CK(c, cudaStreamWaitEvent(stream, c->ev_arrived[*slot], 0));
+    return HG_OK;
+}
+
+hg_status release(hg_ctx *c, int slot, cudaStream_t stream) {
+    HG_CK(c, cudaEventRecord(c->ev_free[slot], stream));
+    c->inflight.pop_front();
+    return HG_OK;
+}
+
+void push_chunks(std::vector<ChunkReq> &v, const hg_plan_t &p, const void *W_host) {
+    const uint8_t *base = (const uint8_t *)W_host;
+    const int64_t row = 2 * p.K;
+    for (int64_t i = 0; i < p.n_chunks; ++i) {
+        const int64_t r0 = i * p.chunk_rows;
+        const int64_t r1 = (i + 1) * p.chunk_rows < p.n_str ? (i + 1) * p.chunk_rows : p.n_str;
+        v.push_back({base + r0 * row, (r1 - r0) * row});
+    }
+}
+
+void set_future(hg_ctx *c, std::vector<ChunkReq> &&list, bool wrap) {
+    if (wrap && c->fwrap && list.size() == c->future.size() &&
+        std::equal(list.begin(), list.end(), c->future.begin()))
+        return;  // same stack as last call: keep streaming where we are
+    c->future = std::move(list);
+    c->fpos = 0;
+    c->fwrap = wrap;
+}
+
+// ---------------------------------------------------------------- GEMV launch
+hg_status gemv(hg_ctx *c, const void *x, int B, int64_t K, const void *W, int64_t n,
+               const float *bias, float *y, int64_t ldy, cudaStream_t s) {
+    if (n <= 0) return HG_OK;
+    if (gemv_ws_floats(n, K, B) > c->ws_floats || gemv_counters(n, K, B) > c->n_counters)
+        return set_error(HG_EINVAL, "GEMV of %lld rows x K=%lld exceeds the context workspace "
+                                    "(raise max_n / max_k)", (long long)n, (long long)K);
+    size_t i0 = 0, i1 = 0;
+    cudaEvent_t e0 = nullptr;
+    if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
+    HG_TRY(kerr(c, launch_gemv(x, B, K, W, n, bias, y, ldy, c->ws, c->counters, s), "gemv launch"));
+    c->st.gpu_launches++;
+    if (e0) {
+        cudaEvent_t e1 = tev_get(c, &i1);
+        if (e1) {
+            HG_CK(c, cudaEventRecord(e1, s));
+            c->gemv_ev.push_back({i0, i1});
+        }
+    }
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------- one linear
+hg_status stream_guard(hg_ctx *c, cudaStream_t s) {
+    if (c->have_last && c->last_stream != s) HG_CK(c, cudaStreamWaitEvent(s, c->ev_done, 0));
+    c->last_stream = s;
+    c->have_last = true;
+    return HG_OK;
+}
+
+hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
+    const hg_plan_t &p = L.plan;
+    const int B = (int)p.batch;
+    const int64_t K = p.K;
+    HG_TRY(pump(c));
+    if (p.n_cpu > 0) {  // a2: activation to the host first, so the CPU lane starts early
+        HG_CK(c, cudaMemcpyAsync(c->x_host, L.x, (size_t)B * K * 2, cudaMemcpyDeviceToHost, s));
+        HG_CK(c, cudaEventRecord(c->ev_x, s));
+    }
+    if (p.n_res > 0) {  // a3
+        HG_TRY(gemv(c, L.x, B, K, L.W_dev, p.n_res, L.bias, L.y, L.ldy, s));
+        c->st.bytes_res += 2 * K * p.n_res;
+    }
+    if (p.n_str > 0) {  // a4
+        std::vector<ChunkReq> mine;
+        push_chunks(mine, p, L.W_host);
+        for (int64_t i = 0; i < p.n_chunks; ++i) {
+            int slot = 0;
+            HG_TRY(acquire(c, mine[i], s, &slot));
+            const int64_t r0 = p.n_res + i * p.chunk_rows;
+            const int64_t rows = mine[i].bytes / (2 * K);
+            HG_TRY(gemv(c, L.x, B, K, c->ring + (int64_t)slot * c->slot_bytes, rows,
+                        L.bias ? L.bias + r0 : nullptr, L.y + r0, L.ldy, s));
+            HG_TRY(release(c, slot, s));
+            HG_TRY(pump(c));
+        }
+        c->st.bytes_str += 2 * K * p.n_str;
+        c->st.n_chunks += p.n_chunks;
+    }
+    if (p.n_cpu > 0) {  // a5 + a6
+        HG_TRY(wait_event(c, c->ev_x, &c->st.x_wait_s));
+        HG_TRY(wait_event(c, c->ev_ycpu, nullptr));  // bounce buffer free (previous H2D done)
+        const auto t0 = clk::now();
+        HostJob job;
+        job.fn = c->host_fn;
+        job.x = c->x_host;
+        job.batch = B;
+        job.K = K;
+        job.n = p.n_cpu;
+        job.W = (const uint16_t *)(L.W_host + 2 * K * p.n_str);
+        job.bias = nullptr;  // bias joins on the device
+        job.y = c->ycpu_host;
+        job.ldy = p.n_cpu;
+        job.block = 16;
+        job.next.store(0);
+        pool_run(c->pool, host_job_run, &job);
+        c->st.cpu_busy_s += secs(t0, clk::now());
+        c->st.bytes_cpu += 2 * K * p.n_cpu;
+        HG_CK(c, cudaMemcpyAsync(c->ycpu_dev, c->ycpu_host, (size_t)B * p.n_cpu * 4,
+                                 cudaMemcpyHostToDevice, s));
+        HG_CK(c, cudaEventRecord(c->ev_ycpu, s));
+        const int64_t col0 = p.n_res + p.n_str;
+        HG_TRY(kerr(c, launch_join(L.y, L.ldy, col0, p.n_cpu, B, c->ycpu_dev, L.bias, s), "join"));
+        c->st.gpu_launches++;
+    }
+    c->st.n_linears++;
+    return HG_OK;
+}
+
+hg_status validate_plan(hg_ctx *c, const hg_plan_t &p) {
+    if (p.batch < 1 || p.batch > HG_MAX_BATCH) return set_error(HG_EINVAL, "batch %lld", (long long)p.batch);
+    if (p.K <= 0 || p.K % 8) return set_error(HG_EALIGN, "K=%lld must be a positive multiple of 8", (long long)p.K);
+    if (p.K > c->cfg.max_k || p.N > c->cfg.max_n)
+        return set_error(HG_EINVAL, "N=%lld K=%lld exceed context max_n/max_k", (long long)p.N, (long long)p.K);
+    if (p.granule < 1 || p.N % p.granule || p.n_res % p.granule || p.n_res < 0 || p.n_str < 0 ||
+        p.n_cpu < 0 || p.n_res + p.n_str + p.n_cpu != p.N || p.chunk_rows < 1 ||
+        p.n_chunks != (p.n_str + p.chunk_rows - 1) / p.chunk_rows)
+        return set_error(HG_EINVAL, "inconsistent plan");
+    if (p.chunk_rows * p.K * 2 > c->slot_bytes)
+        return set_error(HG_EINVAL, "chunk of %lld rows x K=%lld exceeds the ring slot (%lld B)",
+                         (long long)p.chunk_rows, (long long)p.K, (long long)c->slot_bytes);
+    return HG_OK;
+}
+
+hg_status validate_lin(hg_ctx *c, const hg_plan_t &p, const void *x, const void *W_dev,
+                       const void *W_host, const float *bias, const float *y) {
+    HG_TRY(validate_plan(c, p));
+    HG_TRY(check_ptr(c, x, true, "x"));
+    if (!aligned(x, 16)) return set_error(HG_EALIGN, "x not 16-byte aligned");
+    if (p.n_res > 0) {
+        HG_TRY(check_ptr(c, W_dev, true, "W_dev"));
+        if (!aligned(W_dev, 16)) return set_error(HG_EALIGN, "W_dev not 16-byte aligned");
+    }
+    if (p.n_res < p.N) {
+        HG_TRY(check_ptr(c, W_host, false, "W_host"));
+        if (!aligned(W_host, 16)) return set_error(HG_EALIGN, "W_host not 16-byte aligned");
+    }
+    if (bias) {
+        HG_TRY(check_ptr(c, bias, true, "bias"));
+        if (!aligned(bias, 4)) return set_error(HG_EALIGN, "bias not 4-byte aligned");
+    }
+    HG_TRY(check_ptr(c, y, true, "y"));
+    if (!aligned(y, 4)) return set_error(HG_EALIGN, "y not 4-byte aligned");
+    return HG_OK;
+}
+
+hg_status begin_call(hg_ctx *c, cudaStream_t s) {
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_CK(c, cudaSetDevice(c->device));
+    if (c->cfg.collect_stats) {
+        // reuse the timing events of the previous call: wait for it to finish
+        if (c->have_last) HG_CK(c, cudaEventSynchronize(c->ev_done));
+        c->tev_used = 0;
+        c->copy_ev.clear();
+        c->gemv_ev.clear();
+    }
+    const int64_t launches = c->st.gpu_launches;
+    std::memset(&c->st, 0, sizeof c->st);
+    c->st.gpu_launches = launches;  // cumulative (hg_reset_stats zeroes it)
+    HG_TRY(stream_guard(c, s));
+    HG_CK(c, cudaEventRecord(c->ev_call0, s));
+    c->st.wall_s = -1;
+    return HG_OK;
+}
+
+hg_status end_call(hg_ctx *c, cudaStream_t s) {
+    HG_CK(c, cudaEventRecord(c->ev_call1, s));
+    HG_CK(c, cudaEventRecord(c->ev_done, s));
+    c->call_timed = true;
+    return HG_OK;
+}
+
+hg_status ensure(hg_ctx *c, void **p, int64_t *have, int64_t need_bytes) {
+    if (*have >= need_bytes) return HG_OK;
+    if (*p) {
+        HG_CK(c, cudaDeviceSynchronize());
+        cudaFree(*p);
+        *p = nullptr;
+    }
+    HG_CK(c, cudaMalloc(p, (size_t)need_bytes));
+    *have = need_bytes;
+    return HG_OK;
+}
+
+// all-gather this rank's [B, n_local] shard into y [B, P*n_local]
+hg_status gather(hg_ctx *c, const float *ylocal, int B, int64_t n_local, float *y, cudaStream_t s) {
+    const int P = dist_nranks(c->dist);
+    if (B == 1) return dist_allgather(c->dist, ylocal, y, (size_t)n_local, s);
+    HG_TRY(ensure(c, (void **)&c->gbuf, &c->gbuf_elems, (int64_t)P * B * n_local * 4));
+    HG_TRY(dist_allgather(c->dist, ylocal, c->gbuf, (size_t)B * n_local, s));
+    HG_TRY(kerr(c, launch_gather_permute(c->gbuf, P, B, n_local, y, s), "gather permute"));
+    c->st.gpu_launches++;
+    return HG_OK;
+}
+
+// One linear of a layer: sharded (P > 1: local rows then all-gather) or not.
+hg_status layer_linear(hg_ctx *c, const hg_linear_desc &d, const void *x, float *y, int64_t N_full,
+                       cudaStream_t s) {
+    const int P = dist_nranks(c->dist);
+    Lin L{d.plan, x, d.W_dev, (const uint8_t *)d.W_host, d.bias, y, N_full};
+    if (P == 1) return run_linear(c, L, s);
+    HG_TRY(ensure(c, (void **)&c->ylocal, &c->ylocal_elems, d.plan.batch * d.plan.N * 4));
+    L.y = c->ylocal;
+    L.ldy = d.plan.N;
+    HG_TRY(run_linear(c, L, s));
+    return gather(c, c->ylocal, (int)d.plan.batch, d.plan.N, y, s);
+}
+
+hg_status validate_layer(hg_ctx *c, const hg_opt_layer &l, int B) {
+    const int P = dist_nranks(c->dist);
+    const int64_t H = l.hidden, F = l.ffn;
+    const int64_t Ns[4] = {3 * H, H, F, H}, Ks[4] = {H, H, H, F};
+    if (H <= 0 || F <= 0) return set_error(HG_EINVAL, "layer: hidden/ffn must be > 0");
+    for (int i = 0; i < 4; ++i) {
+        const hg_linear_desc &d = l.lin[i];
+        if (d.plan.N * P != Ns[i] || d.plan.K != Ks[i] || d.plan.batch != B)
+            return set_error(HG_EINVAL, "layer linear %d: plan (N=%lld K=%lld B=%lld) does not match "
+                                        "(N=%lld/%d K=%lld B=%d)", i, (long long)d.plan.N,
+                             (long long)d.plan.K, (long long)d.plan.batch, (long long)Ns[i], P,
+                             (long long)Ks[i], B);
+        HG_TRY(validate_plan(c, d.plan));
+        if (d.plan.n_res > 0) HG_TRY(check_ptr(c, d.W_dev, true, "layer W_dev"));
+        if (d.plan.n_res < d.plan.N) HG_TRY(check_ptr(c, d.W_host, false, "layer W_host"));
+        if (d.bias) HG_TRY(check_ptr(c, d.bias, true, "layer bias"));
+    }
+    return HG_OK;
+}
+
+void trace_copy(hg_ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (dst) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+}
+
+hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_trace *tr,
+                    cudaStream_t s) {
+    const int64_t H = l.hidden, F = l.ffn;
+    HG_TRY(ensure(c, &c->act, &c->act_elems, (int64_t)B * (F > H ? F : H) * 2));
+    HG_TRY(ensure(c, (void **)&c->yscr, &c->yscr_elems, (int64_t)B * (F > 3 * H ? F : 3 * H) * 4));
+    HG_TRY(ensure(c, &c->h1, &c->h1_elems, (int64_t)B * H * 2));
+    // a = LN1(h)
+    HG_TRY(kerr(c, launch_layernorm(h, H, B, l.ln1_g, l.ln1_b, c->act, s), "ln1"));
+    if (tr) trace_copy(c, tr->a, c->act, (size_t)B * H * 2, s);
+    // qkv
+    HG_TRY(layer_linear(c, l.lin[0], c->act, c->yscr, 3 * H, s));
+    if (tr && tr->y_qkv) trace_copy(c, tr->y_qkv, c->yscr, (size_t)B * 3 * H * 4, s);
+    // attention at decode position 0: context = v
+    HG_TRY(kerr(c, launch_slice_to_bf16(c->yscr, 3 * H, 2 * H, H, B, c->act, s), "v"));
+    if (tr) trace_copy(c, tr->v, c->act, (size_t)B * H * 2, s);
+    // o
+    HG_TRY(layer_linear(c, l.lin[1], c->act, c->yscr, H, s));
+    if (tr) trace_copy(c, tr->y_o, c->yscr, (size_t)B * H * 4, s);
+    // h1 = h + o ; a2 = LN2(h1)
+    HG_TRY(kerr(c, launch_residual_ln(h, c->yscr, H, B, c->h1, l.ln2_g, l.ln2_b, c->act, s), "res+ln2"));
+    if (tr) {
+        trace_copy(c, tr->h1, c->h1, (size_t)B * H * 2, s);
+        trace_copy(c, tr->a2, c->act, (size_t)B * H * 2, s);
+    }
+    // fc1 + ReLU
+    HG_TRY(layer_linear(c, l.lin[2], c->act, c->yscr, F, s));
+    if (tr) trace_copy(c, tr->y_fc1, c->yscr, (size_t)B * F * 4, s);
+    HG_TRY(kerr(c, launch_relu_bf16(c->yscr, F, B, c->act, s), "relu"));
+    if (tr) trace_copy(c, tr->u, c->act, (size_t)B * F * 2, s);
+    // fc2 + residual
+    HG_TRY(layer_linear(c, l.lin[3], c->act, c->yscr, H, s));
+    if (tr) trace_copy(c, tr->y_fc2, c->yscr, (size_t)B * H * 4, s);
+    HG_TRY(kerr(c, launch_residual(c->h1, c->yscr, H, B, h, s), "residual"));
+    c->st.gpu_launches += 5;
+    return HG_OK;
+}
+
+}  // namespace
+
+// =====================================================================================
+// ABI
+// =====================================================================================
+extern "C" {
+
+HG_API int hg_abi_version(void) { return HG_ABI_VERSION; }
+HG_API const char *hg_last_error(void) { return g_err; }
+
+HG_API hg_status hg_config_default(hg_config *cfg) {
+    if (!cfg) return set_error(HG_EINVAL, "NULL cfg");
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->granule = 128;
+    cfg->chunk_bytes = 16ll << 20;
+    cfg->ring_bytes = 1ll << 30;
+    cfg->max_k = 65536;
+    cfg->max_n = 131072;
+    cfg->cpu_threads = 0;
+    cfg->cpu_first = -1;
+    cfg->collect_stats = 0;
+    cfg->wrap_prefetch = 0;
+    cfg->timeout_s = 60.0;
+    return HG_OK;
+}
+
+HG_API const char *hg_host_isa(void) {
+    const char *name = "?";
+    host_rows_select(&name);
+    return name;
+}
+
+HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
+    if (!out) return set_error(HG_EINVAL, "NULL ctx pointer");
+    *out = nullptr;
+    hg_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else hg_config_default(&cfg);
+    if (cfg.granule < 1 || cfg.chunk_bytes < 1 || cfg.max_k < 8 || cfg.max_n < 1 ||
+        !(cfg.timeout_s > 0))
+        return set_error(HG_EINVAL, "bad config");
+    hg_ctx *c = new hg_ctx;
+    c->cfg = cfg;
+    c->device = device;
+    std::memset(&c->st, 0, sizeof c->st);
+    int nthr = cfg.cpu_threads > 0 ? cfg.cpu_threads : (int)sysconf(_SC_NPROCESSORS_ONLN);
+    c->pool = pool_create(nthr, cfg.cpu_first);
+    c->host_fn = host_rows_select(nullptr);
+    if (device < 0) {
+        *out = c;
+        return HG_OK;
+    }
+    hg_status st = HG_OK;
+    auto fail = [&](hg_status s) {
+        hg_destroy(c);
+        return s;
+    };
+#define CREATE_CK(expr)                                                                        \
+    do {                                                                                       \
+        cudaError_t e_ = (expr);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            st = set_error(e_ == cudaErrorMemoryAllocation ? HG_ENOMEM : HG_ECUDA, "%s: %s",    \
+                           #expr, cudaGetErrorString(e_));                                     \
+            return fail(st);                                                                   \
+        }                                                                                      \
+    } while (0)
+    CREATE_CK(cudaSetDevice(device));
+    if (gemv_prepare() != 0) return fail(set_error(HG_ECUDA, "gemv attributes"));
+    CREATE_CK(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    c->slot_bytes = cfg.chunk_bytes;
+    const int64_t min_slot = cfg.granule * cfg.max_k * 2;
+    if (c->slot_bytes < min_slot) c->slot_bytes = min_slot;
+    c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
+    c->nslots = (int)(cfg.ring_bytes / c->slot_bytes);
+    if (c->nslots < 2) c->nslots = 2;
+    CREATE_CK(cudaMalloc((void **)&c->ring, (size_t)c->nslots * c->slot_bytes));
+    c->ev_arrived.resize(c->nslots);
+    c->ev_free.resize(c->nslots);
+    c->slot_used.assign(c->nslots, 0);
+    for (int i = 0; i < c->nslots; ++i) {
+        CREATE_CK(cudaEventCreateWithFlags(&c->ev_arrived[i], cudaEventDisableTiming));
+        CREATE_CK(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
+    }
+    CREATE_CK(cudaHostAlloc((void **)&c->x_host, (size_t)HG_MAX_BATCH * cfg.max_k * 2, cudaHostAllocDefault));
+    CREATE_CK(cudaHostAlloc((void **)&c->ycpu_host, (size_t)HG_MAX_BATCH * cfg.max_n * 4, cudaHostAllocDefault));
+    CREATE_CK(cudaMalloc((void **)&c->ycpu_dev, (size_t)HG_MAX_BATCH * cfg.max_n * 4));
+    CREATE_CK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
+    CREATE_CK(cudaEventCreateWithFlags(&c->ev_ycpu, cudaEventDisableTiming));
+    CREATE_CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    CREATE_CK(cudaEventCreate(&c->ev_call0));
+    CREATE_CK(cudaEventCreate(&c->ev_call1));
+    c->ws_floats = gemv_ws_floats(cfg.max_n, cfg.max_k, HG_MAX_BATCH);
+    if (c->ws_floats < 1) c->ws_floats = 1;
+    CREATE_CK(cudaMalloc((void **)&c->ws, (size_t)c->ws_floats * 4));
+    c->n_counters = gemv_counters(cfg.max_n, 8, 1) + 1;  // worst case: smallest rows-per-CTA
+    CREATE_CK(cudaMalloc((void **)&c->counters, (size_t)c->n_counters * 4));
+    CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
+    CREATE_CK(cudaMalloc((void **)&c->sink, 256));
+    CREATE_CK(cudaDeviceSynchronize());
+#undef CREATE_CK
+    *out = c;
+    return HG_OK;
+}
+
+HG_API hg_status hg_destroy(hg_ctx *c) {
+    if (!c) return HG_OK;
+    if (c->device >= 0) {
+        cudaSetDevice(c->device);
+        cudaDeviceSynchronize();
+        if (c->dist) dist_destroy(c->dist);
+        for (auto e : c->ev_arrived) if (e) cudaEventDestroy(e);
+        for (auto e : c->ev_free) if (e) cudaEventDestroy(e);
+        for (auto e : c->tev) cudaEventDestroy(e);
+        for (cudaEvent_t e : {c->ev_x, c->ev_ycpu, c->ev_done, c->ev_call0, c->ev_call1})
+            if (e) cudaEventDestroy(e);
+        if (c->copy) cudaStreamDestroy(c->copy);
+        for (void *p : {(void *)c->ring, (void *)c->ycpu_dev, (void *)c->ws, (void *)c->counters,
+                        (void *)c->sink, c->act, (void *)c->yscr, c->h1, (void *)c->ylocal,
+                        (void *)c->gbuf})
+            if (p) cudaFree(p);
+        if (c->x_host) cudaFreeHost(c->x_host);
+        if (c->ycpu_host) cudaFreeHost(c->ycpu_host);
+    }
+    if (c->pool) pool_destroy(c->pool);
+    delete c;
+    return HG_OK;
+}
+
+HG_API hg_status hg_linear_planned(hg_ctx *c, const hg_plan_t *p, const void *x, const void *W_dev,
+                                   const void *W_host, const float *bias, float *y, void *stream) {
+    if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(validate_lin(c, *p, x, W_dev, W_host, bias, y));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(begin_call(c, s));
+    std::vector<ChunkReq> list;
+    push_chunks(list, *p, W_host);
+    set_future(c, std::move(list), false);
+    Lin L{*p, x, W_dev, (const uint8_t *)W_host, bias, y, p->N};
+    HG_TRY(run_linear(c, L, s));
+    return end_call(c, s);
+}
+
+HG_API hg_status hg_linear(hg_ctx *c, const void *x, int batch, int64_t N, int64_t K,
+                           const void *W_dev, int64_t n_res, const void *W_host, double alpha,
+                           const float *bias, float *y, void *stream) {
+    if (!c) return set_error(HG_EINVAL, "NULL ctx");
+    if (K % 8) return set_error(HG_EALIGN, "K %% 8 != 0");
+    hg_rates r = {1, 1, 1, 1, 1, 1, 1};
+    hg_plan_t p;
+    HG_TRY(hg_plan(&r, N, K, batch, n_res, HG_ALPHA_FIXED, alpha, c->cfg.granule, c->cfg.chunk_bytes, &p));
+    return hg_linear_planned(c, &p, x, W_dev, W_host, bias, y, stream);
+}
+
+HG_API hg_status hg_linear_sharded(hg_ctx *c, const hg_plan_t *p, const void *x, const void *W_dev,
+                                   const void *W_host, const float *bias, float *y_full,
+                                   void *stream) {
+    if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
+    if (!c->dist) return set_error(HG_ESTATE, "hg_dist_init not called");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(validate_lin(c, *p, x, W_dev, W_host, bias, y_full));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(begin_call(c, s));
+    std::vector<ChunkReq> list;
+    push_chunks(list, *p, W_host);
+    set_future(c, std::move(list), false);
+    hg_linear_desc d{W_dev, W_host, bias, *p};
+    HG_TRY(layer_linear(c, d, x, y_full, p->N * dist_nranks(c->dist), s));
+    return end_call(c, s);
+}
+
+HG_API hg_status hg_layer(hg_ctx *c, const hg_opt_layer *l, void *h, int batch,
+                          hg_layer_trace *trace, void *stream) {
+    if (!c || !l) return set_error(HG_EINVAL, "NULL argument");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(validate_layer(c, *l, batch));
+    HG_TRY(check_ptr(c, h, true, "h"));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(begin_call(c, s));
+    std::vector<ChunkReq> list;
+    for (int i = 0; i < 4; ++i) push_chunks(list, l->lin[i].plan, l->lin[i].W_host);
+    set_future(c, std::move(list), false);
+    HG_TRY(run_layer(c, *l, h, batch, trace, s));
+    return end_call(c, s);
+}
+
+HG_API hg_status hg_stack(hg_ctx *c, const hg_opt_layer *layers, int n_layers, void *h, int batch,
+                          void *stream) {
+    if (!c || !layers || n_layers < 1) return set_error(HG_EINVAL, "bad arguments");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_CK(c, cudaSetDevice(c->device));
+    for (int l = 0; l < n_layers; ++l) HG_TRY(validate_layer(c, layers[l], batch));
+    HG_TRY(check_ptr(c, h, true, "h"));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(begin_call(c, s));
+    std::vector<ChunkReq> list;
+    for (int l = 0; l < n_layers; ++l)
+        for (int i = 0; i < 4; ++i) push_chunks(list, layers[l].lin[i].plan, layers[l].lin[i].W_host);
+    set_future(c, std::move(list), c->cfg.wrap_prefetch != 0);
+    for (int l = 0; l < n_layers; ++l) HG_TRY(run_layer(c, layers[l], h, batch, nullptr, s));
+    return end_call(c, s);
+}
+
+HG_API hg_status hg_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t K, const void *W,
+                         const float *bias, float *y, int64_t ldy, void *stream) {
+    if (!c) return set_error(HG_EINVAL, "NULL ctx");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    if (batch < 1 || batch > HG_MAX_BATCH || n < 0 || K <= 0 || ldy < n)
+        return set_error(HG_EINVAL, "hg_gemv: bad shape");
+    if (K % 8) return set_error(HG_EALIGN, "K %% 8 != 0");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(check_ptr(c, x, true, "x"));
+    HG_TRY(check_ptr(c, W, true, "W"));
+    HG_TRY(check_ptr(c, y, true, "y"));
+    if (bias) HG_TRY(check_ptr(c, bias, true, "bias"));
+    if (!aligned(x, 16) || !aligned(W, 16)) return set_error(HG_EALIGN, "x/W not 16-byte aligned");
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(stream_guard(c, s));
+    HG_TRY(gemv(c, x, batch, K, W, n, bias, y, ldy, s));
+    HG_CK(c, cudaEventRecord(c->ev_done, s));
+    return HG_OK;
+}
+
+HG_API hg_status hg_host_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t K,
+                              const void *W, const float *bias, float *y) {
+    if (!c || !x || !W || !y) return set_error(HG_EINVAL, "NULL argument");
+    if (batch < 1 || batch > HG_MAX_BATCH || n < 0 || K <= 0)
+        return set_error(HG_EINVAL, "hg_host_gemv: bad shape");
+    if (K % 8) return set_error(HG_EALIGN, "K %% 8 != 0");
+    HostJob job;
+    job.fn = c->host_fn;
+    job.x = (const uint16_t *)x;
+    job.batch = batch;
+    job.K = K;
+    job.n = n;
+    job.W = (const uint16_t *)W;
+    job.bias = bias;
+    job.y = y;
+    job.ldy = n;
+    job.block = 16;
+    job.next.store(0);
+    pool_run(c->pool, host_job_run, &job);
+    return HG_OK;
+}
+
+HG_API hg_status hg_dist_unique_id(void *id128) {
+    if (!id128) return set_error(HG_EINVAL, "NULL id");
+    return dist_unique_id(id128);
+}
+
+HG_API hg_status hg_dist_init(hg_ctx *c, int nranks, int rank, const void *id128) {
+    if (!c || !id128 || nranks < 1 || rank < 0 || rank >= nranks)
+        return set_error(HG_EINVAL, "bad arguments");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    if (c->dist) return set_error(HG_ESTATE, "already initialised");
+    HG_CK(c, cudaSetDevice(c->device));
+    hg_status st = HG_OK;
+    c->dist = dist_create(nranks, rank, id128, &st);
+    return st;
+}
+
+HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
+    if (!c || !out) return set_error(HG_EINVAL, "NULL argument");
+    if (c->device >= 0 && c->call_timed) {
+        HG_CK(c, cudaSetDevice(c->device));
+        HG_CK(c, cudaEventSynchronize(c->ev_done));
+        float ms = 0;
+        HG_CK(c, cudaEventElapsedTime(&ms, c->ev_call0, c->ev_call1));
+        c->st.wall_s = ms * 1e-3;
+        if (c->cfg.collect_stats) {
+            HG_CK(c, cudaStreamSynchronize(c->copy));
+            double link = 0, gpu = 0;
+            for (auto &pr : c->copy_ev) {
+                if (cudaEventElapsedTime(&ms, c->tev[pr.first], c->tev[pr.second]) == cudaSuccess)
+                    link += ms * 1e-3;
+            }
+            for (auto &pr : c->gemv_ev) {
+                if (cudaEventElapsedTime(&ms, c->tev[pr.first], c->tev[pr.second]) == cudaSuccess)
+                    gpu += ms * 1e-3;
+            }
+            cudaGetLastError();
+            c->st.link_busy_s = link;
+            c->st.gpu_busy_s = gpu;
+        }
+    }
+    *out = c->st;
+    return HG_OK;
+}
+
+HG_API hg_status hg_reset_stats(hg_ctx *c) {
+    if (!c) return set_error(HG_EINVAL, "NULL ctx");
+    std::memset(&c->st, 0, sizeof c->st);
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------- measurement
+HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K, int batch,
+                            int flags, hg_rates *out) {
+    if (!c || !W_host || !out) return set_error(HG_EINVAL, "NULL argument");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    if (N <= 0 || K <= 0 || K % 8 || batch < 1 || batch > HG_MAX_BATCH || K > c->cfg.max_k ||
+        N > c->cfg.max_n)
+        return set_error(HG_EINVAL, "hg_measure: bad shape");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(check_ptr(c, W_host, false, "W_host"));
+    HG_CK(c, cudaDeviceSynchronize());
+    c->inflight.clear();  // the ring is reused below; any prefetch state is dropped
+    c->future.clear();
+    c->fpos = 0;
+    std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
+
+    const int64_t wbytes = 2 * N * K;
+    const int64_t ring_bytes = (int64_t)c->nslots * c->slot_bytes;
+    cudaEvent_t e0, e1;
+    HG_CK(c, cudaEventCreate(&e0));
+    HG_CK(c, cudaEventCreate(&e1));
+    float ms = 0;
+    const uint8_t *src = (const uint8_t *)W_host;
+
+    // link: chunk-sized copies (v_link) and one large copy (b_link)
+    const int64_t C = chunk_rows_for(K, c->cfg.granule, c->cfg.chunk_bytes);
+    const int64_t chunk = std::min<int64_t>(C * K * 2, wbytes);
+    int64_t total = 0;
+    // warm-up: first DMA over these pages and ring addresses is not representative
+    HG_CK(c, cudaMemcpyAsync(c->ring, src, std::min<int64_t>(wbytes, ring_bytes), cudaMemcpyHostToDevice,
+                             c->copy));
+    HG_CK(c, cudaEventRecord(e0, c->copy));
+    for (int64_t off = 0; off + chunk <= wbytes && total < (512ll << 20); off += chunk) {
+        HG_CK(c, cudaMemcpyAsync(c->ring + (total % (ring_bytes - chunk + 1)) / 256 * 256, src + off,
+                                 chunk, cudaMemcpyHostToDevice, c->copy));
+        total += chunk;
+    }
+    HG_CK(c, cudaEventRecord(e1, c->copy));
+    HG_CK(c, cudaEventSynchronize(e1));
+    HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
+    out->v_link = (double)total / (ms * 1e-3);
+    const int64_t big = std::min<int64_t>(std::min<int64_t>(wbytes, ring_bytes), 512ll << 20);
+    HG_CK(c, cudaEventRecord(e0, c->copy));
+    HG_CK(c, cudaMemcpyAsync(c->ring, src, big, cudaMemcpyHostToDevice, c->copy));
+    HG_CK(c, cudaEventRecord(e1, c->copy));
+    HG_CK(c, cudaEventSynchronize(e1));
+    HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
+    out->b_link = (double)big / (ms * 1e-3);
+
+    // GPU: GEMV over the rows now in the ring (>= L2 size when the weight allows)
+    const int64_t rows = std::min<int64_t>(N, big / (2 * K));
+    HG_CK(c, cudaMemset(c->ycpu_dev, 0, (size_t)batch * K * 2));  // x = 0 (values irrelevant)
+    float best = 1e30f;
+    for (int it = 0; it < 5; ++it) {
+        HG_CK(c, cudaEventRecord(e0, c->copy));
+        HG_TRY(kerr(c, launch_gemv(c->ycpu_dev, batch, K, c->ring, rows, nullptr,
+                                   c->ycpu_dev + (size_t)batch * K, rows, c->ws, c->counters,
+                                   c->copy), "gemv probe"));
+        HG_CK(c, cudaEventRecord(e1, c->copy));
+        HG_CK(c, cudaEventSynchronize(e1));
+        HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    out->v_gpu = (double)rows * K * 2 / (best * 1e-3);
+    best = 1e30f;
+    for (int it = 0; it < 5; ++it) {
+        HG_CK(c, cudaEventRecord(e0, c->copy));
+        HG_TRY(kerr(c, launch_read_bw(c->ring, ring_bytes, c->sink, c->copy), "read probe"));
+        HG_CK(c, cudaEventRecord(e1, c->copy));
+        HG_CK(c, cudaEventSynchronize(e1));
+        HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
+        best = std::min(best, ms);
+    }
+    out->b_hbm = (double)ring_bytes / (best * 1e-3);
+
+    // CPU lane: the pool's GEMV over the whole weight; optionally under link load
+    std::vector<uint16_t> xh((size_t)batch * K, 0x3f80);
+    std::vector<float> yh((size_t)batch * N);
+    if (flags & 1) {  // keep the link busy for the duration of the CPU probe
+        for (int64_t off = 0, n = 0; n < 64; ++n, off = (off + chunk) % (wbytes - chunk + 1))
+            HG_CK(c, cudaMemcpyAsync(c->ring, src + off / 256 * 256, chunk, cudaMemcpyHostToDevice, c->copy));
+    }
+    double best_cpu = 1e30;
+    for (int it = 0; it < 3; ++it) {
+        auto t0 = clk::now();
+        HG_TRY(hg_host_gemv(c, xh.data(), batch, N, K, W_host, nullptr, yh.data()));
+        best_cpu = std::min(best_cpu, secs(t0, clk::now()));
+    }
+    out->v_cpu = (double)wbytes / best_cpu;
+    // host read bandwidth of the pool (b_cpu)
+    struct RJ { const uint8_t *p; int64_t bytes, block; std::atomic<int64_t> next; std::atomic<uint64_t> sum; };
+    RJ rj;
+    rj.p = src;
+    rj.bytes = wbytes;
+    rj.block = 1 << 20;
+    const char *isa = hg_host_isa();
+    double best_rd = 1e30;
+    for (int it = 0; it < 3; ++it) {
+        rj.next.store(0);
+        rj.sum.store(0);
+        auto t0 = clk::now();
+        pool_run(c->pool, [](void *a, int) {
+            RJ *r = (RJ *)a;
+            const int64_t nb = (r->bytes + r->block - 1) / r->block;
+            uint64_t s = 0;
+            for (;;) {
+                int64_t b = r->next.fetch_add(1);
+                if (b >= nb) break;
+                int64_t len = std::min(r->block, r->bytes - b * r->block);
+                if (!strcmp(hg_host_isa(), "avx512bf16")) s ^= host_read_avx512(r->p + b * r->block, len);
+                else for (int64_t i = 0; i < len; i += 64) s += r->p[b * r->block + i];
+            }
+            r->sum.fetch_xor(s);
+        }, &rj);
+        best_rd = std::min(best_rd, secs(t0, clk::now()));
+    }
+    (void)isa;
+    out->b_cpu = (double)wbytes / best_rd;
+    out->v_pin = INFINITY;
+    HG_CK(c, cudaStreamSynchronize(c->copy));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return HG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,279 @@
+"""Thin ctypes binding over libhg.so (include/hg.h).
+
+Argument marshalling only: every step of the hot path runs inside libhg.so
+(CUDA kernels for sm_100a, the copy-engine pipeline and the host thread pool).
+Tensors are passed as raw pointers (`tensor.data_ptr()`), streams as
+`stream.cuda_stream`.  There is no fallback: if libhg.so is missing this module
+raises at import.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libhg.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} not found: build the CUDA library first (python -c 'import __graft_entry__ as g; g.build()' "
+        "or python tools/build.py). There is no CPU fallback.")
+
+_lib = ctypes.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- status codes
+HG_OK, HG_EINVAL, HG_ENOTPINNED, HG_ENOTDEVICE, HG_EALIGN = 0, -1, -2, -3, -4
+HG_ECUDA, HG_ENCCL, HG_ENOMEM, HG_ESTATE, HG_ETIMEOUT, HG_EUNSUPPORTED = -5, -6, -7, -8, -9, -10
+STATUS_NAMES = {0: "HG_OK", -1: "HG_EINVAL", -2: "HG_ENOTPINNED", -3: "HG_ENOTDEVICE", -4: "HG_EALIGN",
+                -5: "HG_ECUDA", -6: "HG_ENCCL", -7: "HG_ENOMEM", -8: "HG_ESTATE", -9: "HG_ETIMEOUT",
+                -10: "HG_EUNSUPPORTED"}
+HG_MAX_BATCH = 8
+EXACT, APPROX, TPRIME, ASYNC, FIXED = 0, 1, 2, 3, 4
+
+
+class HgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(st: int):
+    if st != HG_OK:
+        raise HgError(st, _lib.hg_last_error().decode(errors="replace"))
+
+
+# ---------------------------------------------------------------- structs (mirror hg.h)
+class Rates(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in ("v_cpu", "v_gpu", "v_link", "v_pin", "b_hbm", "b_link", "b_cpu")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class Plan(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_int64) for n in ("N", "K", "batch", "n_res", "n_str", "n_cpu", "granule",
+                                               "chunk_rows", "n_chunks")]
+                + [(n, ctypes.c_double) for n in ("alpha_req", "alpha_eff", "t_cpu", "t_link", "t_gpu",
+                                                  "t_eq4", "t_pred", "t_hbm", "t_roof")])
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class Config(ctypes.Structure):
+    _fields_ = [("granule", ctypes.c_int64), ("chunk_bytes", ctypes.c_int64), ("ring_bytes", ctypes.c_int64),
+                ("max_k", ctypes.c_int64), ("max_n", ctypes.c_int64), ("cpu_threads", ctypes.c_int32),
+                ("cpu_first", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
+                ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = ([(n, ctypes.c_double) for n in ("wall_s", "cpu_busy_s", "link_busy_s", "gpu_busy_s", "x_wait_s")]
+                + [(n, ctypes.c_int64) for n in ("bytes_res", "bytes_str", "bytes_cpu", "n_chunks", "n_linears",
+                                                 "gpu_launches")])
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class LinearDesc(ctypes.Structure):
+    _fields_ = [("W_dev", ctypes.c_void_p), ("W_host", ctypes.c_void_p), ("bias", ctypes.c_void_p),
+                ("plan", Plan)]
+
+
+class OptLayer(ctypes.Structure):
+    _fields_ = [("hidden", ctypes.c_int64), ("ffn", ctypes.c_int64), ("lin", LinearDesc * 4),
+                ("ln1_g", ctypes.c_void_p), ("ln1_b", ctypes.c_void_p), ("ln2_g", ctypes.c_void_p),
+                ("ln2_b", ctypes.c_void_p)]
+
+
+class LayerTrace(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_void_p) for n in ("a", "y_qkv", "v", "y_o", "h1", "a2", "y_fc1", "u", "y_fc2")]
+
+
+_vp, _i32, _i64, _dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
+_P = ctypes.POINTER
+_sig = {
+    "hg_abi_version": (ctypes.c_int, []),
+    "hg_last_error": (ctypes.c_char_p, []),
+    "hg_config_default": (_i32, [_P(Config)]),
+    "hg_create": (_i32, [_P(_vp), _i32, _P(Config)]),
+    "hg_destroy": (_i32, [_vp]),
+    "hg_plan": (_i32, [_P(Rates), _i64, _i64, _i32, _i64, _i32, _dbl, _i64, _i64, _P(Plan)]),
+    "hg_measure": (_i32, [_vp, _vp, _i64, _i64, _i32, _i32, _P(Rates)]),
+    "hg_linear": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _i64, _vp, _dbl, _vp, _vp, _vp]),
+    "hg_linear_planned": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hg_layer": (_i32, [_vp, _P(OptLayer), _vp, _i32, _P(LayerTrace), _vp]),
+    "hg_stack": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _vp]),
+    "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
+    "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
+    "hg_host_isa": (ctypes.c_char_p, []),
+    "hg_dist_unique_id": (_i32, [_vp]),
+    "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
+    "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hg_stats": (_i32, [_vp, _P(Stats)]),
+    "hg_reset_stats": (_i32, [_vp]),
+}
+for _name, (_res, _args) in _sig.items():
+    _f = getattr(_lib, _name)
+    _f.restype, _f.argtypes = _res, _args
+
+EXPORTED = tuple(_sig)
+
+
+def _ptr(t):
+    """data pointer of a torch tensor / numpy array / int / None."""
+    if t is None:
+        return None
+    if isinstance(t, int):
+        return t
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if hasattr(t, "ctypes"):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if isinstance(s, int):
+        return s
+    return s.cuda_stream
+
+
+# ---------------------------------------------------------------- free functions (same names as the ABI)
+def hg_abi_version() -> int:
+    return _lib.hg_abi_version()
+
+
+def hg_host_isa() -> str:
+    return _lib.hg_host_isa().decode()
+
+
+def hg_config_default() -> Config:
+    c = Config()
+    _check(_lib.hg_config_default(ctypes.byref(c)))
+    return c
+
+
+def make_rates(v_cpu, v_gpu, v_link, v_pin=math.inf, b_hbm=None, b_link=None, b_cpu=None) -> Rates:
+    return Rates(v_cpu, v_gpu, v_link, v_pin, b_hbm or v_gpu, b_link or v_link, b_cpu or v_cpu)
+
+
+def hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed=0.0, granule=128, chunk_bytes=16 << 20) -> Plan:
+    if isinstance(rates, dict):
+        rates = Rates(**rates)
+    p = Plan()
+    _check(_lib.hg_plan(ctypes.byref(rates), N, K, batch, n_res, mode, float(alpha_fixed), granule,
+                        chunk_bytes, ctypes.byref(p)))
+    return p
+
+
+def hg_dist_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.hg_dist_unique_id(buf))
+    return buf.raw
+
+
+class Context:
+    """Owns one hg_ctx (device >= 0, or -1 for a host-only context)."""
+
+    def __init__(self, device: int = 0, **cfg):
+        c = hg_config_default()
+        for k, v in cfg.items():
+            setattr(c, k, v)
+        self.config = c
+        self._h = _vp()
+        _check(_lib.hg_create(ctypes.byref(self._h), device, ctypes.byref(c)))
+        self.device = device
+
+    def close(self):
+        if self._h:
+            _lib.hg_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- a1-a6
+    def plan(self, rates, N, K, batch, n_res, mode=EXACT, alpha_fixed=0.0) -> Plan:
+        return hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed, self.config.granule, self.config.chunk_bytes)
+
+    def hg_linear(self, x, batch, N, K, W_dev, n_res, W_host, alpha, bias, y, stream=None):
+        _check(_lib.hg_linear(self._h, _ptr(x), batch, N, K, _ptr(W_dev), n_res, _ptr(W_host), float(alpha),
+                              _ptr(bias), _ptr(y), _stream(stream)))
+
+    def hg_linear_planned(self, plan, x, W_dev, W_host, bias, y, stream=None):
+        _check(_lib.hg_linear_planned(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(W_host),
+                                      _ptr(bias), _ptr(y), _stream(stream)))
+
+    def hg_linear_sharded(self, plan, x, W_dev, W_host, bias, y_full, stream=None):
+        _check(_lib.hg_linear_sharded(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(W_host),
+                                      _ptr(bias), _ptr(y_full), _stream(stream)))
+
+    def hg_layer(self, layer: OptLayer, h, batch, trace: LayerTrace | None = None, stream=None):
+        _check(_lib.hg_layer(self._h, ctypes.byref(layer), _ptr(h), batch,
+                             ctypes.byref(trace) if trace is not None else None, _stream(stream)))
+
+    def hg_stack(self, layers, h, batch, stream=None):
+        arr = (OptLayer * len(layers))(*layers)
+        _check(_lib.hg_stack(self._h, arr, len(layers), _ptr(h), batch, _stream(stream)))
+
+    def hg_gemv(self, x, batch, n, K, W, bias, y, ldy=None, stream=None):
+        _check(_lib.hg_gemv(self._h, _ptr(x), batch, n, K, _ptr(W), _ptr(bias), _ptr(y),
+                            n if ldy is None else ldy, _stream(stream)))
+
+    def hg_host_gemv(self, x, batch, n, K, W, bias, y):
+        _check(_lib.hg_host_gemv(self._h, _ptr(x), batch, n, K, _ptr(W), _ptr(bias), _ptr(y)))
+
+    def hg_measure(self, W_host, N, K, batch, under_load=True) -> Rates:
+        r = Rates()
+        _check(_lib.hg_measure(self._h, _ptr(W_host), N, K, batch, 1 if under_load else 0, ctypes.byref(r)))
+        return r
+
+    def hg_dist_init(self, nranks, rank, uid: bytes):
+        buf = ctypes.create_string_buffer(uid, 128)
+        _check(_lib.hg_dist_init(self._h, nranks, rank, buf))
+
+    def hg_stats(self) -> Stats:
+        s = Stats()
+        _check(_lib.hg_stats(self._h, ctypes.byref(s)))
+        return s
+
+    def hg_reset_stats(self):
+        _check(_lib.hg_reset_stats(self._h))
+
+
+def linear_desc(plan: Plan, W_dev=None, W_host=None, bias=None) -> LinearDesc:
+    return LinearDesc(_ptr(W_dev), _ptr(W_host), _ptr(bias), plan)
+
+
+def opt_layer(hidden, ffn, descs, ln1_g=None, ln1_b=None, ln2_g=None, ln2_b=None) -> OptLayer:
+    L = OptLayer()
+    L.hidden, L.ffn = hidden, ffn
+    for i, d in enumerate(descs):
+        L.lin[i] = d
+    L.ln1_g, L.ln1_b, L.ln2_g, L.ln2_b = (_ptr(t) for t in (ln1_g, ln1_b, ln2_g, ln2_b))
+    return L
+
+
+def layer_trace(**bufs) -> LayerTrace:
+    t = LayerTrace()
+    for k, v in bufs.items():
+        setattr(t, k, _ptr(v))
+    return t

@@ -1,0 +1,106 @@
+"""GPU parity of hg_layer / hg_stack.
+
+Teacher-forced per linear: each linear's fp32 output is compared with the
+oracle fed the GPU's own bf16 input to that linear (from the layer trace); each
+glue step likewise.  bf16 glue outputs may differ from the fp64 oracle by the
+rounding of an fp32 intermediate, so they use the same elementwise tolerance.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from harness import gen
+from paper_2403_01164_b200 import hg
+from gpu_util import bits, dev, dev_f32, pinned
+
+pytestmark = pytest.mark.gpu
+
+NAMES = ("qkv", "o", "fc1", "fc2")
+
+
+def make_layer(ctx, H, F, B, layer=0, seed=21, r=0.0, alpha=0.5, keep=None):
+    shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+    descs, Wd, bd = [], {}, {}
+    keep = keep if keep is not None else []
+    for name in NAMES:
+        N, K = shapes[name]
+        _, W, b = gen.linear_inputs(seed, layer, name, 1, N, K)
+        Wd[name], bd[name] = W, b
+        n_res = oracle.resident_rows(r, N, ctx.config.granule)
+        p = ctx.plan(hg.make_rates(1, 1, 1), N, K, B, n_res, hg.FIXED, alpha)
+        W_dev = dev(W[:n_res]) if n_res else None
+        W_host = pinned(W[n_res:]) if n_res < N else None
+        bias = dev_f32(b)
+        keep += [W_dev, W_host, bias]
+        descs.append(hg.linear_desc(p, W_dev, W_host, bias))
+    return hg.opt_layer(H, F, descs), Wd, bd
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=32768, max_n=65536)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("B,r,alpha", [(1, 0.0, 0.5), (3, 0.5, 0.3), (8, 0.25, 1.0), (2, 0.0, 0.0)])
+def test_layer_teacher_forced(ctx, B, r, alpha):
+    H, F = 512, 2048
+    keep = []
+    L, Wd, bd = make_layer(ctx, H, F, B, r=r, alpha=alpha, keep=keep)
+    h0 = gen.uniform_bf16(5, 999, B * H, 1.0).reshape(B, H)
+    h = dev(h0)
+    tr = {k: torch.zeros(B, n, dtype=torch.int16, device="cuda") for k, n in
+          (("a", H), ("v", H), ("h1", H), ("a2", H), ("u", F))}
+    tr.update({k: torch.zeros(B, n, device="cuda") for k, n in
+               (("y_qkv", 3 * H), ("y_o", H), ("y_fc1", F), ("y_fc2", H))})
+    ctx.hg_layer(L, h, B, hg.layer_trace(**tr))
+    torch.cuda.synchronize()
+    T = {k: (bits(v) if v.dtype == torch.int16 else v.cpu().numpy()) for k, v in tr.items()}
+    out = bits(h)
+    # linears, teacher-forced on the GPU's own inputs
+    for name, xin, yk in (("qkv", "a", "y_qkv"), ("o", "v", "y_o"), ("fc1", "a2", "y_fc1"), ("fc2", "u", "y_fc2")):
+        ok, worst = oracle.within_tol(T[yk], oracle.linear(T[xin], Wd[name], bd[name]))
+        assert ok, (name, worst)
+    # glue, teacher-forced
+    chk = lambda got, ref: oracle.within_tol(oracle.bf16_to_f64(got), oracle.bf16_to_f64(ref))[0]
+    assert chk(T["a"], oracle.layernorm(h0))
+    assert chk(T["v"], oracle.attention_pos0(T["y_qkv"], H))
+    assert chk(T["h1"], oracle.residual(h0, T["y_o"]))
+    assert chk(T["a2"], oracle.layernorm(T["h1"]))
+    assert chk(T["u"], oracle.relu_bf16(T["y_fc1"]))
+    assert chk(out, oracle.residual(T["h1"], T["y_fc2"]))
+    # end to end (secondary, looser report): the full fp64 oracle layer
+    full = oracle.layer(h0, Wd, bd, H)
+    assert oracle.within_tol(oracle.bf16_to_f64(out), oracle.bf16_to_f64(full["out"]), rtol=5e-2)[0]
+
+
+def test_stack_two_layers_matches_two_layer_calls(ctx):
+    """hg_stack (cross-linear prefetch) gives the same bits as layer-by-layer calls."""
+    H, F, B = 256, 1024, 2
+    keep = []
+    layers = [make_layer(ctx, H, F, B, layer=l, alpha=0.6, keep=keep)[0] for l in range(3)]
+    h0 = gen.uniform_bf16(6, 998, B * H, 1.0).reshape(B, H)
+    h_a, h_b = dev(h0), dev(h0)
+    ctx.hg_stack(layers, h_a, B)
+    for L in layers:
+        ctx.hg_layer(L, h_b, B)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(h_a), bits(h_b))
+
+
+def test_stack_wrap_prefetch_repeatable():
+    H, F, B = 256, 1024, 1
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=32 << 20, max_k=4096, max_n=8192,
+                    wrap_prefetch=1) as c:
+        keep = []
+        layers = [make_layer(c, H, F, B, layer=l, alpha=0.7, keep=keep)[0] for l in range(2)]
+        h0 = gen.uniform_bf16(7, 997, B * H, 1.0).reshape(B, H)
+        outs = []
+        for _ in range(3):
+            h = dev(h0)
+            c.hg_stack(layers, h, B)
+            torch.cuda.synchronize()
+            outs.append(bits(h))
+        assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])

@@ -1,0 +1,194 @@
+"""GPU parity for the device GEMV and the heterogeneous linear
+through the C ABI, against the fp64 oracle on identical generated inputs.
+
+Tolerance (BJ:5, R13): elementwise |y - y_ref| <= 1e-2 * max(1, |y_ref|).
+Bit-exact: small-integer inputs (fp32 sums exact), identity / one-hot / zero W,
+and GPU split invariance (every partition with n_cpu = 0 gives identical bits).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from harness import gen
+from paper_2403_01164_b200 import hg
+from gpu_util import bits, dev, dev_f32, pinned, split_weight
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=65536, max_n=65536)
+    yield c
+    c.close()
+
+
+@pytest.fixture(scope="module")
+def ctx_g1():
+    c = hg.Context(0, granule=1, chunk_bytes=4096, ring_bytes=1 << 20, max_k=1024, max_n=4096)
+    yield c
+    c.close()
+
+
+def _gemv(ctx, x, W, b, B):
+    N, K = W.shape
+    y = torch.full((B, N), float("nan"), device="cuda")
+    ctx.hg_gemv(dev(x), B, N, K, dev(W), None if b is None else dev_f32(b), y)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("B", range(1, 9))
+@pytest.mark.parametrize("N,K", [(1, 8), (33, 768), (300, 4104), (129, 7168), (70, 28672)])
+def test_gemv_parity(ctx, B, N, K):
+    x, W, b = gen.linear_inputs(7, 0, "fc1", B, N, K)
+    y = _gemv(ctx, x, W, b, B)
+    ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+    assert ok, worst
+
+
+@pytest.mark.parametrize("B", [1, 3, 8])
+@pytest.mark.parametrize("K", [256, 8192])
+def test_gemv_small_integer_exact(ctx, B, K):
+    m = 16 if K <= 256 else 2  # keep every partial sum < 2^24
+    x, W, b = gen.linear_inputs(8, 0, "o", B, 77, K, integer=m)
+    y = _gemv(ctx, x, W, b, B)
+    assert np.array_equal(y.astype(np.float64), oracle.linear(x, W, b))
+
+
+def _linear(ctx, x, W, b, B, n_res, alpha, stream=None):
+    N, K = W.shape
+    W_dev, W_host = split_weight(W, n_res)
+    y = torch.full((B, N), float("nan"), device="cuda")
+    ctx.hg_linear(dev(x), B, N, K, W_dev, n_res, W_host, alpha, None if b is None else dev_f32(b), y,
+                  stream=stream)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+def test_c1_opt125m_fc1_alpha_half(ctx):
+    """BJ:7: OPT-125M fc1 768->3072, batch 1, alpha = 0.5 -> partition (0, 1536, 1536)."""
+    x, W, b = gen.linear_inputs(1164, 0, "fc1", 1, 3072, 768)
+    p = ctx.plan(hg.make_rates(1, 1, 1), 3072, 768, 1, 0, hg.FIXED, 0.5)
+    assert (p.n_res, p.n_str, p.n_cpu) == (0, 1536, 1536)
+    y = _linear(ctx, x, W, b, 1, 0, 0.5)
+    ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+    assert ok, worst
+
+
+@pytest.mark.parametrize("B", [1, 2, 5, 8])
+@pytest.mark.parametrize("n_res,alpha", [(0, 0.0), (0, 1.0), (0, 0.37), (1024, 0.5), (2048, 0.0),
+                                         (2048, 1.0), (3072, 0.5)])
+def test_linear_partitions(ctx, B, n_res, alpha):
+    x, W, b = gen.linear_inputs(2, 0, "fc2", B, 3072, 1000)
+    y = _linear(ctx, x, W, b, B, n_res, alpha)
+    ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+    assert ok, worst
+
+
+def test_linear_no_bias_many_chunks(ctx):
+    # 1 MiB chunks at K=4096 -> 128-row chunks; 20 chunks ride a 64-slot ring
+    x, W, _ = gen.linear_inputs(3, 0, "qkv", 2, 3840, 4096, bias=False)
+    y = _linear(ctx, x, W, None, 2, 256, 0.8)
+    assert oracle.within_tol(y, oracle.linear(x, W))[0]
+
+
+def test_split_invariance_gpu_bit_exact(ctx):
+    """All partitions with n_cpu = 0 run the same kernel and reduction order: identical bits."""
+    x, W, b = gen.linear_inputs(4, 0, "fc1", 3, 2048, 7168)
+    ref = _linear(ctx, x, W, b, 3, 2048, 0.0)  # fully resident
+    for n_res in (0, 128, 1024, 1920):
+        y = _linear(ctx, x, W, b, 3, n_res, 1.0)  # the rest streamed
+        assert np.array_equal(y, ref), n_res
+    assert np.array_equal(_gemv(ctx, x, W, b, 3), ref)
+
+
+def test_cpu_rows_equal_host_lane(ctx):
+    x, W, b = gen.linear_inputs(5, 0, "fc1", 2, 1024, 512)
+    y = _linear(ctx, x, W, b, 2, 0, 0.0)  # everything on the CPU lane
+    yh = np.zeros((2, 1024), np.float32)
+    with hg.Context(-1, cpu_threads=3) as hc:
+        hc.hg_host_gemv(x, 2, 1024, 512, W, b, yh)
+    assert np.array_equal(y, yh)
+
+
+@pytest.mark.parametrize("n_res,alpha", [(0, 0.5), (512, 0.3), (0, 0.0), (0, 1.0)])
+def test_linear_small_integer_exact(ctx, n_res, alpha):
+    x, W, b = gen.linear_inputs(6, 0, "o", 4, 1024, 256, integer=16)
+    y = _linear(ctx, x, W, b, 4, n_res, alpha)
+    assert np.array_equal(y.astype(np.float64), oracle.linear(x, W, b))
+
+
+def test_identity_onehot_zero_weights(ctx):
+    K = 1024
+    x, _, b = gen.linear_inputs(9, 0, "o", 3, K, K)
+    eye = np.zeros((K, K), np.uint16)
+    eye[np.arange(K), np.arange(K)] = 0x3F80
+    y = _linear(ctx, x, eye, None, 3, 256, 0.5)
+    assert np.array_equal(y.astype(np.float64), oracle.bf16_to_f64(x))
+    perm = np.random.default_rng(0).integers(0, K, size=K)
+    oh = np.zeros((K, K), np.uint16)
+    oh[np.arange(K), perm] = 0x3F80
+    y = _linear(ctx, x, oh, None, 3, 0, 0.25)
+    assert np.array_equal(y.astype(np.float64), oracle.bf16_to_f64(x)[:, perm])
+    y = _linear(ctx, x, np.zeros((K, K), np.uint16), b, 3, 384, 0.5)
+    assert np.array_equal(y, np.broadcast_to(b, y.shape))
+
+
+def test_brute_force_all_partitions_tiny(ctx_g1):
+    """G = 1, N = 12, K = 16: every (n_res, alpha-grid) partition matches the oracle."""
+    N, K = 12, 16
+    x, W, b = gen.linear_inputs(10, 0, "fc1", 2, N, K, integer=8)
+    ref = oracle.linear(x, W, b)
+    for n_res in range(N + 1):
+        m = N - n_res
+        for g in range(m + 1):
+            alpha = g / m if m else 0.0
+            y = _linear(ctx_g1, x, W, b, 2, n_res, alpha)
+            assert np.array_equal(y.astype(np.float64), ref), (n_res, g)
+
+
+def test_nondefault_stream_and_reuse(ctx):
+    s = torch.cuda.Stream()
+    x, W, b = gen.linear_inputs(11, 0, "fc1", 1, 2048, 1024)
+    ref = oracle.linear(x, W, b)
+    for _ in range(3):
+        y = _linear(ctx, x, W, b, 1, 512, 0.4, stream=s)
+        assert oracle.within_tol(y, ref)[0]
+
+
+def test_errors(ctx):
+    x, W, b = gen.linear_inputs(12, 0, "o", 1, 256, 64)
+    xd, Wd, bd = dev(x), dev(W), dev_f32(b)
+    y = torch.zeros(1, 256, device="cuda")
+    pageable = torch.from_numpy(W.view(np.int16).copy())
+    with pytest.raises(hg.HgError) as e:
+        ctx.hg_linear(xd, 1, 256, 64, None, 0, pageable, 0.5, bd, y)
+    assert e.value.status == hg.HG_ENOTPINNED
+    with pytest.raises(hg.HgError) as e:
+        ctx.hg_linear(xd, 1, 256, 64, None, 0, pinned(W), 1.5, bd, y)
+    assert e.value.status == hg.HG_EINVAL
+    with pytest.raises(hg.HgError) as e:
+        ctx.hg_linear(xd.data_ptr() + 2, 1, 256, 64, None, 0, pinned(W), 0.5, bd, y)
+    assert e.value.status == hg.HG_EALIGN
+    with pytest.raises(hg.HgError) as e:
+        ctx.hg_linear(torch.from_numpy(x.view(np.int16)), 1, 256, 64, None, 0, pinned(W), 0.5, bd, y)
+    assert e.value.status == hg.HG_ENOTDEVICE
+    with pytest.raises(hg.HgError) as e:
+        ctx.hg_linear(xd, 1, 200, 64, None, 0, pinned(W[:200]), 0.5, bd, y)  # N % G
+    assert e.value.status == hg.HG_EINVAL
+    # the context is still usable after argument errors
+    ok, _ = oracle.within_tol(_linear(ctx, x, W, b, 1, 128, 0.5), oracle.linear(x, W, b))
+    assert ok
+
+
+def test_stats_lane_breakdown():
+    with hg.Context(0, chunk_bytes=2 << 20, ring_bytes=64 << 20, collect_stats=1) as c:
+        x, W, b = gen.linear_inputs(13, 0, "fc1", 1, 4096, 4096)
+        _linear(c, x, W, b, 1, 1024, 0.5)
+        s = c.hg_stats()
+        assert s.n_linears == 1 and s.bytes_res == 1024 * 4096 * 2
+        assert s.bytes_str == 1536 * 4096 * 2 and s.bytes_cpu == 1536 * 4096 * 2
+        assert s.n_chunks == 3 and s.link_busy_s > 0 and s.gpu_busy_s > 0 and s.cpu_busy_s > 0
+        assert s.wall_s > 0 and s.gpu_launches >= 5
