@@ -156,7 +156,7 @@ def main_arm(args):
     threads = args.threads or per
     ctx = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
                      chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
-                     max_k=F, max_n=3 * H, wrap_prefetch=1, collect_stats=0)
+                     max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0)
     if world > 1:
         uid = hg.hg_dist_unique_id() if rank == 0 else None
         obj = [uid]
@@ -264,7 +264,7 @@ def main_arm(args):
     sctx_stats = None
     ctx_stats = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
                            chunk_bytes=args.chunk_mb << 20, ring_bytes=min(args.ring_mb, 4096) << 20,
-                           max_k=F, max_n=3 * H, wrap_prefetch=1, collect_stats=1) if args.breakdown else None
+                           max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1) if args.breakdown else None
     if ctx_stats is not None:
         if world > 1:
             ctx_stats.close()

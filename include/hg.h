@@ -132,6 +132,8 @@ typedef struct {
     int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
     double timeout_s;    /* bound on every host wait (default 60 s)                      */
+    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 5; 0 = never) */
+    int32_t _reserved;
 } hg_config;
 
 /* Lane breakdown of the last hg_linear / hg_layer / hg_stack call (Table 2

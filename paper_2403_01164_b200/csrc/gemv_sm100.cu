@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "hg_internal.h"
 
@@ -196,7 +197,18 @@ __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float 
 
 }  // namespace
 
+// Batches >= the calling context's gemv_tc_min_batch run the tcgen05 kernel
+// (gemv_tc_sm100.cu); 0 disables it.  Set per API call by the runtime (one
+// context per host thread), so it is thread-local.
+static thread_local int g_tc_min_batch = 5;
+static bool g_tc_ok = true;  // false when the TMA encoder / tcgen05 setup is unavailable
+
+void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }
+
+static bool use_tc(int batch) { return g_tc_ok && g_tc_min_batch > 0 && batch >= g_tc_min_batch; }
+
 GemvGeom gemv_geom(int64_t K, int batch) {
+    if (use_tc(batch)) return gemv_tc_geom(K);
     GemvGeom g;
     const int64_t s0 = (K + kSliceMax - 1) / kSliceMax;
     int64_t ks = (K + s0 - 1) / s0;
@@ -220,6 +232,7 @@ int64_t gemv_counters(int64_t n, int64_t K, int batch) {
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
                 float *y, int64_t ldy, float *ws, int *counters, void *stream) {
     if (n <= 0) return 0;
+    if (use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
     cudaStream_t st = (cudaStream_t)stream;
     switch (batch) {
         case 1: return launch_b<1>(x, K, W, n, bias, y, ldy, ws, counters, st);
@@ -241,6 +254,7 @@ int prepare_b() {
 }
 
 int gemv_prepare() {
+    if (gemv_tc_prepare() != 0) g_tc_ok = false;  // no TMA encoder: SIMT only
     int e = 0;
     e |= prepare_b<1>(); e |= prepare_b<2>(); e |= prepare_b<3>(); e |= prepare_b<4>();
     e |= prepare_b<5>(); e |= prepare_b<6>(); e |= prepare_b<7>(); e |= prepare_b<8>();

@@ -1,0 +1,382 @@
+// gemv_tc_sm100.cu -- tcgen05 tensor-core GEMV for batch 5..8.
+//
+// Same contract as gemv_sm100.cu: y[b, j] = sum_k x[b,k] W[j,k] (+bias[j]) with
+// fp32 accumulation.  At batch >= 5 the SIMT kernel spends ~B FMAs per weight
+// and the FMA pipe, not HBM, becomes the limit, so here the contraction runs on
+// the 5th-generation tensor cores while the kernel stays an HBM stream:
+//
+//   D[128 rows of W, 16] (TMEM, fp32) += A[128 x 16] (W tile, smem) . B[16 x 16] (x^T, smem)
+//
+// * one elected thread of warp 0 issues TMA (cp.async.bulk.tensor.2d) for a
+//   [128 rows x 64 k] W tile (16 KB, 128-byte swizzle) and the [16 x 64] x tile
+//   (rows >= B are out of bounds and zero-filled by TMA) into a ring of smem
+//   stages guarded by full/empty mbarriers;
+// * one elected thread of warp 1 issues tcgen05.mma.cta_group::1.kind::f16
+//   (M=128, N=16, K=16; four per stage) into a TMEM accumulator and frees each
+//   stage with tcgen05.commit;
+// * warps 2-5 drain the accumulator with tcgen05.ld (32x32b.x16) and write
+//   y (+bias), or the split-K partial.  Two accumulators (TMEM columns 0-15,
+//   16-31) let the epilogue of one work unit overlap the MMAs of the next.
+// * persistent CTAs walk work units (row tile, k-slice); the k-slices and the
+//   deterministic last-arriver reduction are the same scheme as the SIMT kernel
+//   (slice geometry depends on K only, so every launch reduces identically).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+
+#include "hg_internal.h"
+
+namespace hg {
+namespace {
+
+constexpr int kTileM = 128;        // W rows per tile (UMMA M)
+constexpr int kTileK = 64;         // k per stage (one 128-byte swizzle atom of bf16)
+constexpr int kUmmaN = 16;         // batch padded to N = 16
+constexpr int kUmmaK = 16;         // k per tcgen05.mma (bf16)
+constexpr int kStages = 6;
+constexpr int kWBytes = kTileM * kTileK * 2;  // 16 KB
+constexpr int kXBytes = kUmmaN * kTileK * 2;  // 2 KB
+constexpr int kThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 epilogue
+constexpr int64_t kSliceMaxTc = 1024;  // short slices: many work units per SM (tail balance)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar,
+                                            int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"((uint64_t)map), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+
+// K-major, 128-byte swizzled operand: 8-row core groups 1024 B apart (SBO), LBO
+// unused (1), descriptor version 1 (sm_100), layout type 2 = SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;            // LBO (16 B units), unused for swizzled K-major
+    d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+    d |= (uint64_t)1 << 46;            // version
+    d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+    return d;
+}
+
+// kind::f16 instruction descriptor: D fp32, A/B bf16, both K-major, N=16, M=128.
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kUmmaN >> 3) << 17) |
+                            ((uint32_t)(kTileM >> 4) << 24);
+
+__device__ __forceinline__ void umma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t accum) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(kIdesc), "r"(accum)
+        : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+struct Units {
+    int64_t n_tiles;
+    int S;
+    int64_t ks;  // multiple of kTileK
+};
+
+template <int B>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
+                   int64_t K, int64_t n, const float *__restrict__ bias, float *__restrict__ y,
+                   int64_t ldy, Units U, float *__restrict__ ws, int *__restrict__ counters) {
+    extern __shared__ uint8_t smem_raw[];
+    // 1024-byte alignment for the swizzle atoms
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t sW = base;                              // kStages * 16 KB
+    const uint32_t sX = base + kStages * kWBytes;          // kStages * 2 KB
+    const uint32_t bars = sX + kStages * kXBytes;          // full[k], empty[k], tfull[2], tempty[2]
+    uint32_t *tmem_slot = (uint32_t *)(gbase + (bars - base) + 8 * (2 * kStages + 4));
+    int *last_flag = (int *)(tmem_slot + 1);
+    auto full = [&](int s) { return bars + 8 * s; };
+    auto empty = [&](int s) { return bars + 8 * (kStages + s); };
+    auto tfull = [&](int a) { return bars + 8 * (2 * kStages + a); };
+    auto tempty = [&](int a) { return bars + 8 * (2 * kStages + 2 + a); };
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(full(s), 1);
+            mbar_init(empty(s), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull(a), 1);
+            mbar_init(tempty(a), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_w) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_x) : "memory");
+    }
+    if (warp == 1) {  // TMEM: 32 columns (two 16-column accumulators)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int64_t n_units = U.n_tiles * U.S;
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int64_t tile = u % U.n_tiles;
+                const int s = (int)(u / U.n_tiles);
+                const int64_t k0 = (int64_t)s * U.ks;
+                const int64_t k1 = k0 + U.ks < K ? k0 + U.ks : K;
+                for (int64_t k = k0; k < k1; k += kTileK) {
+                    mbar_wait(empty(stage), phase ^ 1);
+                    mbar_expect_tx(full(stage), kWBytes + kXBytes);
+                    tma_load_2d(sW + stage * kWBytes, &map_w, full(stage), (int32_t)k,
+                                (int32_t)(tile * kTileM));
+                    tma_load_2d(sX + stage * kXBytes, &map_x, full(stage), (int32_t)k, 0);
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+                mbar_wait(tempty(acc), aphase ^ 1);
+                tc_fence_after();
+                const int s = (int)(u / U.n_tiles);
+                const int64_t k0 = (int64_t)s * U.ks;
+                const int64_t k1 = k0 + U.ks < K ? k0 + U.ks : K;
+                const uint32_t d = tmem + (uint32_t)(acc * kUmmaN);
+                uint32_t accum = 0;
+                for (int64_t k = k0; k < k1; k += kTileK) {
+                    mbar_wait(full(stage), phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kTileK / kUmmaK; ++kk) {
+                        const uint64_t da = sw128_desc(sW + stage * kWBytes + kk * kUmmaK * 2);
+                        const uint64_t db = sw128_desc(sX + stage * kXBytes + kk * kUmmaK * 2);
+                        umma(d, da, db, accum);
+                        accum = 1;
+                    }
+                    umma_commit(empty(stage));
+                    if (++stage == kStages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(tfull(acc));
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..5
+        const int quarter = warp & 3;  // TMEM lanes this warp may access
+        const int et = (warp - 2) * 32 + lane;
+        int it = 0;
+        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+            const int64_t tile = u % U.n_tiles;
+            const int s = (int)(u / U.n_tiles);
+            mbar_wait(tfull(acc), aphase);
+            tc_fence_after();
+            uint32_t r[16];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kUmmaN);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                "%14,%15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                  "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+                  "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            mbar_arrive(tempty(acc));
+            const int64_t row = tile * kTileM + quarter * 32 + lane;
+            if (U.S == 1) {
+                if (row < n) {
+                    const float bb = bias ? bias[row] : 0.f;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) y[b * ldy + row] = __uint_as_float(r[b]) + bb;
+                }
+                continue;
+            }
+            if (row < n) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) ws[((int64_t)s * B + b) * n + row] = __uint_as_float(r[b]);
+            }
+            __threadfence();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (et == 0) *last_flag = (atomicAdd(&counters[tile], 1) == U.S - 1);
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (*last_flag) {
+                __threadfence();
+                if (row < n) {
+                    const float bb = bias ? bias[row] : 0.f;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        float sum = 0.f;
+                        for (int q = 0; q < U.S; ++q) sum += __ldcg(&ws[((int64_t)q * B + b) * n + row]);
+                        y[b * ldy + row] = sum + bb;
+                    }
+                }
+                if (et == 0) counters[tile] = 0;
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+}
+
+constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kStages + 4) + 16;
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+
+encode_fn_t encode_fn() {
+    static encode_fn_t fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (encode_fn_t)p;
+    });
+    return fn;
+}
+
+bool make_map(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, uint32_t box_inner,
+              uint32_t box_outer) {
+    encode_fn_t enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)inner * 2};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int g_num_sms = 0;
+
+template <int B>
+int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
+                int64_t ldy, float *ws, int *counters, cudaStream_t st) {
+    CUtensorMap mw, mx;
+    if (!make_map(&mw, W, K, n, kTileK, kTileM) || !make_map(&mx, x, K, B, kTileK, kUmmaN))
+        return (int)cudaErrorInvalidValue;
+    const GemvGeom g = gemv_tc_geom(K);
+    Units U{(n + kTileM - 1) / kTileM, g.s, g.ks};
+    const int64_t units = U.n_tiles * U.S;
+    int grid = g_num_sms > 0 ? g_num_sms : 148;
+    if (units < grid) grid = (int)units;
+    gemv_tc_kernel<B><<<grid, kThreads, kSmemBytes, st>>>(mw, mx, K, n, bias, y, ldy, U, ws, counters);
+    return (int)cudaGetLastError();
+}
+
+template <int B>
+int prepare_tc_b() {
+    return (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kSmemBytes);
+}
+
+}  // namespace
+
+GemvGeom gemv_tc_geom(int64_t K) {
+    GemvGeom g;
+    const int64_t s0 = (K + kSliceMaxTc - 1) / kSliceMaxTc;
+    int64_t ks = (K + s0 - 1) / s0;
+    ks = (ks + kTileK - 1) / kTileK * kTileK;
+    g.ks = ks;
+    g.s = (int)((K + ks - 1) / ks);
+    g.rows_per_cta = kTileM;
+    return g;
+}
+
+int gemv_tc_prepare() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    int e = 0;
+    e |= prepare_tc_b<5>();
+    e |= prepare_tc_b<6>();
+    e |= prepare_tc_b<7>();
+    e |= prepare_tc_b<8>();
+    if (!encode_fn()) e |= 1;
+    return e;
+}
+
+int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
+                   float *y, int64_t ldy, float *ws, int *counters, void *stream) {
+    if (n <= 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (batch) {
+        case 5: return launch_tc_b<5>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 6: return launch_tc_b<6>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 7: return launch_tc_b<7>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 8: return launch_tc_b<8>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        default: return (int)cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace hg

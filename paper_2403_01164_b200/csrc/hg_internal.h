@@ -85,4 +85,10 @@ hg_status dist_allgather(Dist *d, const float *send, float *recv, size_t count_p
                          void *stream);
 // gemv kernel attributes (dynamic smem) for the current device
 int gemv_prepare();
+void gemv_set_tc_min_batch(int b);
+// gemv_tc_sm100.cu: tcgen05 path (batch 5..8)
+GemvGeom gemv_tc_geom(int64_t K);
+int gemv_tc_prepare();
+int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
+                   float *y, int64_t ldy, float *ws, int *counters, void *stream);
 }  // namespace hg

@@ -18,6 +18,7 @@
 #include <immintrin.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -448,6 +449,7 @@ hg_status begin_call(hg_ctx *c, cudaStream_t s) {
     if (c->error) return set_error(HG_ESTATE, "context is in an error state");
     if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
     HG_CK(c, cudaSetDevice(c->device));
+    gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     if (c->cfg.collect_stats) {
         // reuse the timing events of the previous call: wait for it to finish
         if (c->have_last) HG_CK(c, cudaEventSynchronize(c->ev_done));
@@ -591,6 +593,8 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     cfg->collect_stats = 0;
     cfg->wrap_prefetch = 0;
     cfg->timeout_s = 60.0;
+    cfg->gemv_tc_min_batch = 5;
+    if (const char *v = getenv("HG_GEMV_TC_MIN_BATCH")) cfg->gemv_tc_min_batch = atoi(v);
     return HG_OK;
 }
 
@@ -659,7 +663,11 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     CREATE_CK(cudaEventCreate(&c->ev_call0));
     CREATE_CK(cudaEventCreate(&c->ev_call1));
+    gemv_set_tc_min_batch(1);  // workspace for the larger of the two geometries
     c->ws_floats = gemv_ws_floats(cfg.max_n, cfg.max_k, HG_MAX_BATCH);
+    gemv_set_tc_min_batch(0);
+    c->ws_floats = std::max(c->ws_floats, gemv_ws_floats(cfg.max_n, cfg.max_k, HG_MAX_BATCH));
+    gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
     if (c->ws_floats < 1) c->ws_floats = 1;
     CREATE_CK(cudaMalloc((void **)&c->ws, (size_t)c->ws_floats * 4));
     c->n_counters = gemv_counters(cfg.max_n, 8, 1) + 1;  // worst case: smallest rows-per-CTA
@@ -792,6 +800,7 @@ HG_API hg_status hg_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t
     if (bias) HG_TRY(check_ptr(c, bias, true, "bias"));
     if (!aligned(x, 16) || !aligned(W, 16)) return set_error(HG_EALIGN, "x/W not 16-byte aligned");
     cudaStream_t s = (cudaStream_t)stream;
+    gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     HG_TRY(stream_guard(c, s));
     HG_TRY(gemv(c, x, batch, K, W, n, bias, y, ldy, s));
     HG_CK(c, cudaEventRecord(c->ev_done, s));
@@ -880,6 +889,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
         N > c->cfg.max_n)
         return set_error(HG_EINVAL, "hg_measure: bad shape");
     HG_CK(c, cudaSetDevice(c->device));
+    gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     HG_TRY(check_ptr(c, W_host, false, "W_host"));
     HG_CK(c, cudaDeviceSynchronize());
     c->inflight.clear();  // the ring is reused below; any prefetch state is dropped
@@ -922,19 +932,24 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
 
     // GPU: GEMV over the rows now in the ring (>= L2 size when the weight allows)
     const int64_t rows = std::min<int64_t>(N, big / (2 * K));
-    HG_CK(c, cudaMemset(c->ycpu_dev, 0, (size_t)batch * K * 2));  // x = 0 (values irrelevant)
+    void *px = nullptr, *py = nullptr;
+    HG_CK(c, cudaMalloc(&px, (size_t)batch * K * 2));
+    HG_CK(c, cudaMalloc(&py, (size_t)batch * rows * 4));
+    HG_CK(c, cudaMemset(px, 0, (size_t)batch * K * 2));  // x = 0 (values irrelevant to timing)
     float best = 1e30f;
     for (int it = 0; it < 5; ++it) {
         HG_CK(c, cudaEventRecord(e0, c->copy));
-        HG_TRY(kerr(c, launch_gemv(c->ycpu_dev, batch, K, c->ring, rows, nullptr,
-                                   c->ycpu_dev + (size_t)batch * K, rows, c->ws, c->counters,
-                                   c->copy), "gemv probe"));
+        HG_TRY(kerr(c, launch_gemv(px, batch, K, c->ring, rows, nullptr, (float *)py, rows, c->ws,
+                                   c->counters, c->copy), "gemv probe"));
         HG_CK(c, cudaEventRecord(e1, c->copy));
         HG_CK(c, cudaEventSynchronize(e1));
         HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
         best = std::min(best, ms);
     }
     out->v_gpu = (double)rows * K * 2 / (best * 1e-3);
+    HG_CK(c, cudaStreamSynchronize(c->copy));
+    cudaFree(px);
+    cudaFree(py);
     best = 1e30f;
     for (int it = 0; it < 5; ++it) {
         HG_CK(c, cudaEventRecord(e0, c->copy));

@@ -65,7 +65,8 @@ class Config(ctypes.Structure):
     _fields_ = [("granule", ctypes.c_int64), ("chunk_bytes", ctypes.c_int64), ("ring_bytes", ctypes.c_int64),
                 ("max_k", ctypes.c_int64), ("max_n", ctypes.c_int64), ("cpu_threads", ctypes.c_int32),
                 ("cpu_first", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
-                ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double)]
+                ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double),
+                ("gemv_tc_min_batch", ctypes.c_int32), ("_reserved", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

@@ -48,6 +48,33 @@ def test_gemv_parity(ctx, B, N, K):
     assert ok, worst
 
 
+@pytest.fixture(scope="module")
+def ctx_simt():
+    """Same kernels with the tcgen05 path disabled (B >= 5 on the SIMT kernel)."""
+    c = hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=65536, max_n=65536,
+                   gemv_tc_min_batch=0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("B", range(5, 9))
+@pytest.mark.parametrize("N,K", [(1, 8), (128, 64), (300, 4104), (129, 7168), (1000, 28672)])
+def test_gemv_simt_path_for_large_batch(ctx_simt, B, N, K):
+    x, W, b = gen.linear_inputs(17, 0, "fc2", B, N, K)
+    y = _gemv(ctx_simt, x, W, b, B)
+    ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+    assert ok, worst
+
+
+@pytest.mark.parametrize("B", [5, 8])
+@pytest.mark.parametrize("N,K", [(128, 64), (256, 1024), (4096, 7168), (3, 200)])
+def test_gemv_tcgen05_small_integer_exact(ctx, B, N, K):
+    """tcgen05 path: fp32 accumulation of small integers is exact -> bit-equal to the oracle."""
+    x, W, b = gen.linear_inputs(18, 0, "fc1", B, N, K, integer=2 if K > 256 else 8)
+    y = _gemv(ctx, x, W, b, B)
+    assert np.array_equal(y.astype(np.float64), oracle.linear(x, W, b))
+
+
 @pytest.mark.parametrize("B", [1, 3, 8])
 @pytest.mark.parametrize("K", [256, 8192])
 def test_gemv_small_integer_exact(ctx, B, K):
@@ -190,5 +217,5 @@ def test_stats_lane_breakdown():
         s = c.hg_stats()
         assert s.n_linears == 1 and s.bytes_res == 1024 * 4096 * 2
         assert s.bytes_str == 1536 * 4096 * 2 and s.bytes_cpu == 1536 * 4096 * 2
-        assert s.n_chunks == 3 and s.link_busy_s > 0 and s.gpu_busy_s > 0 and s.cpu_busy_s > 0
+        assert s.n_chunks == 6 and s.link_busy_s > 0 and s.gpu_busy_s > 0 and s.cpu_busy_s > 0
         assert s.wall_s > 0 and s.gpu_launches >= 5

@@ -62,6 +62,7 @@ PRODUCT_SOURCES = [
     ("host_gemv_avx2.cpp", "cxx_avx2"),
     ("threadpool.cpp", "cxx"),
     ("gemv_sm100.cu", "cu"),
+    ("gemv_tc_sm100.cu", "cu"),
     ("glue_sm100.cu", "cu"),
     ("runtime.cu", "cu"),
     ("dist.cpp", "cxx"),
@@ -104,7 +105,7 @@ def build_product(force=False, verbose=False):
     if force or changed or not os.path.exists(out):
         # static cudart (nvcc default) so the library does not depend on torch's runtime copy;
         # NCCL is dlopen'ed on demand by dist.cpp (no link-time dependency).
-        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lpthread", "-ldl", "-lcuda"])
+        _run([NVCC, *ARCH, "-shared", "-o", out, *objs, "-lpthread", "-ldl"])
     return out
 
 
