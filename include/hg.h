@@ -136,9 +136,11 @@ typedef struct {
     int32_t _reserved;
 } hg_config;
 
-/* Lane breakdown of the last hg_linear / hg_layer / hg_stack call (Table 2
- * analogue).  Busy times from CUDA events (link, gpu) and host
- * clocks (cpu); fractions are busy / wall. */
+/* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last
+ * hg_reset_stats (or context creation) -- the Table 2 analogue.
+ * Busy times from CUDA events (link, gpu; collect_stats = 1) and host clocks
+ * (cpu); wall_s spans the first call's start to the last call's end on the GPU;
+ * fractions are busy / wall.  Collecting never synchronises between calls. */
 typedef struct {
     double wall_s;          /* host wall time of the call (enqueue to GPU completion)   */
     double cpu_busy_s;      /* host GEMV time (sum over linears)                        */
@@ -220,6 +222,45 @@ HG_API hg_status hg_plan(const hg_rates *rates, int64_t N, int64_t K, int batch,
  * of the pool threads), b_hbm (device read rate); v_pin = +inf. */
 HG_API hg_status hg_measure(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch,
                             int flags, hg_rates *out);
+
+/* ---------------------------------------------------------------- alpha benchmark (Sec. 4.4) */
+/* The refinement of P:252-266: lane times measured at alphas in a window around
+ * the closed-form alpha are fitted with least-squares polynomials F_CPU, F_COM
+ * (F_COM = max(F_PIN, F_TRANS) pointwise; t_pin may be NULL = no pin lane since
+ * weights are pre-pinned, reading R7) and F_CPU(a) = F_COM(a) is solved by
+ * bisection on [lo, hi] (tolerance 1e-12).  If the difference has no sign change
+ * in the window the endpoint with the smaller |difference| is returned and
+ * *clamped = 1; identical curves return `seed`.  Pure function, no device work.
+ * Errors: HG_EINVAL for n < degree + 1, degree outside [1, 6], lo > hi, NULL
+ * arrays, non-finite samples. */
+HG_API hg_status hg_alpha_solve(const double *alphas, const double *t_cpu, const double *t_com,
+                                const double *t_pin, int n, int degree, double lo, double hi,
+                                double seed, double *alpha_out, int *clamped);
+
+typedef struct {
+    double gamma;    /* half-width of the window around the seed (default 0.06)            */
+    double lambda;   /* step of the alpha grid (default 0.02)                                */
+    int32_t degree;  /* polynomial degree (default 2)                                        */
+    int32_t reps;    /* measured steps per alpha after one warm-up step (default 1)           */
+} hg_abench_cfg;
+
+#define HG_ABENCH_MAX 64
+typedef struct {
+    double alpha_seed, alpha_bar;
+    int32_t n, clamped;
+    double alpha[HG_ABENCH_MAX];   /* sampled alphas                                         */
+    double t_cpu[HG_ABENCH_MAX];   /* CPU-lane busy seconds per step (host clock)             */
+    double t_com[HG_ABENCH_MAX];   /* link busy seconds per step (CUDA events on copies)      */
+    double t_step[HG_ABENCH_MAX];  /* wall seconds per step (CUDA events)                     */
+} hg_abench_result;
+
+/* Measure the lane times of hg_stack(layers) at every alpha of the window around
+ * alpha_seed (every linear re-planned with HG_ALPHA_FIXED at that alpha, same
+ * n_res, granule and chunk size), then hg_alpha_solve.  The layers' own plans are
+ * not modified; re-plan with alpha_bar to use it.  h_dev is overwritten. */
+HG_API hg_status hg_alpha_bench(hg_ctx *ctx, const hg_opt_layer *layers, int n_layers, void *h_dev,
+                                int batch, double alpha_seed, const hg_abench_cfg *cfg,
+                                hg_abench_result *out, void *stream);
 
 /* ---------------------------------------------------------------- a2-a6: one linear */
 /* y[:, 0:N) = x . W^T (+ bias) with the rows of W split by `alpha`:

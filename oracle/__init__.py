@@ -306,6 +306,70 @@ def plan(rates: dict, N: int, K: int, batch: int, n_res: int, mode: int, alpha_f
 
 
 # ----------------------------------------------------------------------------
+# c2.7 Alpha benchmark refinement (Sec. 4.4; readings R9, R10)
+#   "we adjust its value within a small range of [alpha - gamma, alpha + gamma] in
+#   steps of lambda ... testing the times T'_CPU and max(T'_PIN, T'_TRANS) ... We then
+#   utilize polynomial formulas to model their speeds ... calculation of the alpha
+#   value at which both speeds are equal: F_CPU(alpha_bar) = F_COM(alpha_bar)".
+# ----------------------------------------------------------------------------
+def alpha_window(seed: float, gamma: float, lam: float):
+    """Sample points of [seed - gamma, seed + gamma] clipped to [0, 1], step lambda (R9)."""
+    lo, hi = max(0.0, seed - gamma), min(1.0, seed + gamma)
+    n = int(math.floor((hi - lo) / lam + 1e-9)) + 1
+    pts = [lo + i * lam for i in range(n)]
+    if hi - pts[-1] > 1e-12:
+        pts.append(hi)
+    return pts
+
+
+def fit_poly(alphas, times, degree: int):
+    """Least-squares polynomial (numpy.polyfit, highest power first)."""
+    return np.polyfit(np.asarray(alphas, dtype=np.float64), np.asarray(times, dtype=np.float64), degree)
+
+
+def alpha_bench_solve(alphas, t_cpu, t_com, degree: int, lo: float, hi: float, seed: float,
+                      tol: float = 1e-12, t_pin=None):
+    """Solve F_CPU(a) = F_COM(a) on [lo, hi]; F_COM = max(F_PIN, F_TRANS) pointwise.
+
+    Returns (alpha_bar, clamped).  Bisection on D(a) = F_CPU(a) - F_COM(a); if D has no
+    sign change on the window, the endpoint with the smaller |D| is returned and
+    clamped=True (SPEC's "return the clamped endpoint plus a warning"); if D == 0
+    everywhere (identical curves) the seed is returned.
+    """
+    fc = fit_poly(alphas, t_cpu, degree)
+    ft = fit_poly(alphas, t_com, degree)
+    fp = fit_poly(alphas, t_pin, degree) if t_pin is not None else None
+
+    def D(a):
+        com = np.polyval(ft, a)
+        if fp is not None:
+            com = max(com, np.polyval(fp, a))
+        return float(np.polyval(fc, a) - com)
+
+    dl, dh = D(lo), D(hi)
+    scale = max(1e-300, max(abs(float(np.polyval(fc, lo))), abs(float(np.polyval(fc, hi)))))
+    if abs(dl) <= 1e-12 * scale and abs(dh) <= 1e-12 * scale:
+        return seed, False
+    if dl == 0.0:
+        return lo, False
+    if dh == 0.0:
+        return hi, False
+    if (dl > 0) == (dh > 0):
+        return (lo if abs(dl) < abs(dh) else hi), True
+    a, b = lo, hi
+    for _ in range(200):
+        m = 0.5 * (a + b)
+        dm = D(m)
+        if dm == 0.0 or (b - a) <= tol:
+            return m, False
+        if (dm > 0) == (dl > 0):
+            a, dl = m, dm
+        else:
+            b = m
+    return 0.5 * (a + b), False
+
+
+# ----------------------------------------------------------------------------
 # c2.6 One OPT pre-LN decoder layer at decode position 0 (DESIGN.md reading R22)
 #   All non-linear modules stay on the GPU (P:223); the four linears are the
 #   heterogeneous modules.  bf16 storage points mirror the GPU path.

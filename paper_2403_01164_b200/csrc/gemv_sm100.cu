@@ -5,15 +5,20 @@
 // results once the communication process is completed"), run over HBM-resident
 // rows and over each streamed chunk as it lands in the device ring.  At batch
 // 1-8 the arithmetic intensity is B flop/byte, >= 30x below the B200 ridge, so
-// the kernel is an HBM stream: 128-bit non-allocating loads of W along K, x
-// staged once per CTA in shared memory, fp32 FMAs, warp-shuffle reductions.
+// the kernel is an HBM stream: 128-bit non-allocating loads of W along K with up
+// to 16 loads in flight per lane, x read through L1, fp32 FMAs, warp shuffles.
 //
-// Deterministic split-K: the K axis is cut into S slices whose length depends
-// on K only (gemv_geom).  Every output element is the same sequence of fp32
-// operations whichever launch computes it (resident GEMV, any chunk, any n),
-// so all GPU partitions are bit-identical (SURVEY 8(c) c4 "split invariance").
-// The S partials of a row tile are summed in slice order by the last CTA to
-// finish that tile (counter + threadfence), in the same kernel.
+// Reduction order (fixed by K alone, so every launch -- the resident GEMV, any
+// streamed chunk, any n -- produces bit-identical outputs):
+//   * K is cut into P = ceil(K/8192) parts of equal length (multiple of 8);
+//   * within a part one warp owns the row: lane l accumulates 16-byte vectors
+//     l, l+32, l+64, ... in ascending order (8 FMAs each, in k order), then a
+//     butterfly shuffle sums the 32 lanes (lane 0's value is used);
+//   * the P part sums are added in part order (through shared memory) and the
+//     bias is added last.
+// How many rows a warp carries (R) and how many loads are in flight (U) only
+// change which thread does the work, not the order, so they are picked per
+// launch to fill the 148 SMs.  No global workspace, atomics or fences.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -27,18 +32,19 @@ namespace {
 
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
-constexpr int64_t kSliceMax = 4096;  // elements of K per slice (8 KB of one W row)
-
-template <int B>
-struct Tile {
-    static constexpr int RT = B <= 4 ? 4 : 2;  // W rows per warp (share each x load)
-    static constexpr int U = B <= 4 ? 2 : 2;   // 16-byte W loads in flight per row per lane
-    static constexpr int ROWS = kWarps * RT;   // rows per CTA
-};
+constexpr int64_t kPartMax = 8192;  // elements of K one warp reduces (16 KB of a W row)
 
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
     uint4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
+__device__ __forceinline__ uint4 ldg_cached(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                  : "l"(p));
     return r;
@@ -64,72 +70,67 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// grid = (ceil(n / ROWS), S); block = 256; dynamic smem = B * ks * 2 bytes.
-template <int B>
-__global__ void __launch_bounds__(kThreads)
-    gemv_bf16_kernel(const uint4 *__restrict__ x, int64_t K, const uint4 *__restrict__ W, int64_t n,
-                     const float *__restrict__ bias, float *__restrict__ y, int64_t ldy, int64_t ks,
-                     int S, float *__restrict__ ws, int *__restrict__ counters) {
-    using T = Tile<B>;
-    extern __shared__ uint4 xs[];  // [B][kv]
-    __shared__ int s_last;
-
-    const int s = blockIdx.y;
-    const int64_t k0 = (int64_t)s * ks;
-    const int64_t klen = (K - k0) < ks ? (K - k0) : ks;
-    const int kv = (int)(klen >> 3);  // uint4 per row in this slice
+// grid = ceil(n / rows_per_cta); block = 32*NW.  Warp w: row group w / P, K-part w % P.
+template <int B, int R, int U, int NW>
+__global__ void __launch_bounds__(NW * 32)
+    gemv_rows_kernel(const uint4 *__restrict__ x, int64_t K, const uint4 *__restrict__ W, int64_t n,
+                     const float *__restrict__ bias, float *__restrict__ y, int64_t ldy, int P,
+                     int64_t part_len) {
+    __shared__ float red[NW][R][B];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int groups = NW / P;
+    const int g = warp / P, p = warp - g * P;
+    const bool active = g < groups;
+    const int64_t row0 = ((int64_t)blockIdx.x * groups + g) * R;
     const int64_t Kv = K >> 3;
 
-    for (int i = threadIdx.x; i < B * kv; i += kThreads) {
-        const int b = i / kv, j = i - b * kv;
-        xs[i] = x[b * Kv + (k0 >> 3) + j];
-    }
-    __syncthreads();
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t row0 = (int64_t)blockIdx.x * T::ROWS + warp * T::RT;
-    const uint4 *wp[T::RT];
+    float acc[R][B];
 #pragma unroll
-    for (int r = 0; r < T::RT; ++r) {
-        int64_t rr = row0 + r < n ? row0 + r : n - 1;
-        wp[r] = W + rr * Kv + (k0 >> 3);
-    }
-    float acc[T::RT][B];
-#pragma unroll
-    for (int r = 0; r < T::RT; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int b = 0; b < B; ++b) acc[r][b] = 0.f;
 
-    for (int j = lane; j < kv; j += 32 * T::U) {
-        uint4 wv[T::U][T::RT];
+    if (active) {
+        const int64_t k0 = (int64_t)p * part_len;
+        const int64_t klen = (K - k0) < part_len ? (K - k0) : part_len;
+        const int kv = (int)(klen >> 3);
+        const uint4 *wp[R];
 #pragma unroll
-        for (int u = 0; u < T::U; ++u)
+        for (int r = 0; r < R; ++r) {
+            const int64_t rr = row0 + r < n ? row0 + r : n - 1;
+            wp[r] = W + rr * Kv + (k0 >> 3);
+        }
+        const uint4 *xp = x + (k0 >> 3);
+        for (int j = lane; j < kv; j += 32 * U) {
+            uint4 wv[U][R];
 #pragma unroll
-            for (int r = 0; r < T::RT; ++r)
-                if (j + 32 * u < kv) wv[u][r] = ldg_stream(wp[r] + j + 32 * u);
+            for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int u = 0; u < T::U; ++u) {
-            if (j + 32 * u < kv) {
+                for (int r = 0; r < R; ++r)
+                    if (j + 32 * u < kv) wv[u][r] = ldg_stream(wp[r] + j + 32 * u);
 #pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const uint4 xv = xs[b * kv + j + 32 * u];
-                    const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
-                                         lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+            for (int u = 0; u < U; ++u) {
+                if (j + 32 * u < kv) {
 #pragma unroll
-                    for (int r = 0; r < T::RT; ++r) fma8(acc[r][b], wv[u][r], xf);
+                    for (int b = 0; b < B; ++b) {
+                        const uint4 xv = ldg_cached(xp + b * Kv + j + 32 * u);
+                        const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
+                                             lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+#pragma unroll
+                        for (int r = 0; r < R; ++r) fma8(acc[r][b], wv[u][r], xf);
+                    }
                 }
             }
         }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int b = 0; b < B; ++b) acc[r][b] = warp_sum(acc[r][b]);
     }
+    if (P == 1) {
+        if (active && lane == 0) {
 #pragma unroll
-    for (int r = 0; r < T::RT; ++r)
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc[r][b] = warp_sum(acc[r][b]);
-
-    if (S == 1) {
-        if (lane == 0) {
-#pragma unroll
-            for (int r = 0; r < T::RT; ++r) {
+            for (int r = 0; r < R; ++r) {
                 const int64_t row = row0 + r;
                 if (row < n) {
                     const float bb = bias ? bias[row] : 0.f;
@@ -140,48 +141,56 @@ __global__ void __launch_bounds__(kThreads)
         }
         return;
     }
-    // split-K: partial of slice s -> ws[(s*B + b)*n + row]
-    if (lane == 0) {
+    if (active && lane == 0) {
 #pragma unroll
-        for (int r = 0; r < T::RT; ++r) {
-            const int64_t row = row0 + r;
-            if (row < n) {
+        for (int r = 0; r < R; ++r)
 #pragma unroll
-                for (int b = 0; b < B; ++b) ws[((int64_t)s * B + b) * n + row] = acc[r][b];
-            }
-        }
-        __threadfence();
+            for (int b = 0; b < B; ++b) red[warp][r][b] = acc[r][b];
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        const int prev = atomicAdd(&counters[blockIdx.x], 1);
-        s_last = (prev == S - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    for (int i = threadIdx.x; i < B * T::ROWS; i += kThreads) {
-        const int b = i / T::ROWS;
-        const int64_t row = (int64_t)blockIdx.x * T::ROWS + (i - b * T::ROWS);
+    for (int t = threadIdx.x; t < groups * R * B; t += NW * 32) {
+        const int gg = t / (R * B), rb = t - gg * (R * B), r = rb / B, b = rb - r * B;
+        const int64_t row = ((int64_t)blockIdx.x * groups + gg) * R + r;
         if (row < n) {
-            float sum = 0.f;
-            for (int q = 0; q < S; ++q) sum += __ldcg(&ws[((int64_t)q * B + b) * n + row]);
-            y[b * ldy + row] = sum + (bias ? bias[row] : 0.f);
+            float s = 0.f;
+            for (int q = 0; q < P; ++q) s += red[gg * P + q][r][b];
+            y[b * ldy + row] = s + (bias ? bias[row] : 0.f);
         }
     }
-    if (threadIdx.x == 0) counters[blockIdx.x] = 0;  // ready for the next launch on this stream
 }
 
+int g_sms = 148;
+
+// 4-warp CTAs (short CTAs: small tail at the end of a launch) unless a row needs
+// more than 4 K-parts (K > 32768).  Neither NW nor R changes the numerics.
+template <int B, int R, int U>
+int launch_rows(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
+                int64_t ldy, int P, int64_t part_len, cudaStream_t st) {
+    if (P <= 4) {
+        const int rows_per_cta = (4 / P) * R;
+        const unsigned grid = (unsigned)((n + rows_per_cta - 1) / rows_per_cta);
+        gemv_rows_kernel<B, R, U, 4><<<grid, 128, 0, st>>>((const uint4 *)x, K, (const uint4 *)W, n, bias,
+                                                           y, ldy, P, part_len);
+    } else {
+        const int rows_per_cta = (kWarps / P) * R;
+        const unsigned grid = (unsigned)((n + rows_per_cta - 1) / rows_per_cta);
+        gemv_rows_kernel<B, R, U, kWarps><<<grid, kThreads, 0, st>>>((const uint4 *)x, K, (const uint4 *)W, n,
+                                                                     bias, y, ldy, P, part_len);
+    }
+    return (int)cudaGetLastError();
+}
+
+// R (rows per warp) trades per-warp reuse of x against the number of warps; it
+// does not change numerics, so choose it per launch from n.
 template <int B>
 int launch_b(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
-             int64_t ldy, float *ws, int *counters, cudaStream_t st) {
-    const GemvGeom g = gemv_geom(K, B);
-    const size_t smem = (size_t)B * (size_t)g.ks * 2;
-    dim3 grid((unsigned)((n + Tile<B>::ROWS - 1) / Tile<B>::ROWS), (unsigned)g.s);
-    gemv_bf16_kernel<B><<<grid, kThreads, smem, st>>>(
-        (const uint4 *)x, K, (const uint4 *)W, n, bias, y, ldy, g.ks, g.s, ws, counters);
-    return (int)cudaGetLastError();
+             int64_t ldy, int P, int64_t part_len, cudaStream_t st) {
+    if constexpr (B <= 4) {
+        const int64_t ctas_r2 = (n + (kWarps / P) * 2 - 1) / ((kWarps / P) * 2);
+        if (ctas_r2 >= 4 * g_sms)
+            return launch_rows<B, 2, (B <= 2 ? 8 : 4)>(x, K, W, n, bias, y, ldy, P, part_len, st);
+    }
+    return launch_rows<B, 1, (B <= 2 ? 16 : 8)>(x, K, W, n, bias, y, ldy, P, part_len, st);
 }
 
 // ---------------------------------------------------------------- read-BW probe
@@ -210,22 +219,24 @@ static bool use_tc(int batch) { return g_tc_ok && g_tc_min_batch > 0 && batch >=
 GemvGeom gemv_geom(int64_t K, int batch) {
     if (use_tc(batch)) return gemv_tc_geom(K);
     GemvGeom g;
-    const int64_t s0 = (K + kSliceMax - 1) / kSliceMax;
-    int64_t ks = (K + s0 - 1) / s0;
-    ks = (ks + 7) / 8 * 8;
-    g.ks = ks;
-    g.s = (int)((K + ks - 1) / ks);
-    g.rows_per_cta = kWarps * (batch <= 4 ? 4 : 2);
+    const int64_t P = (K + kPartMax - 1) / kPartMax;
+    int64_t len = (K + P - 1) / P;
+    len = (len + 7) / 8 * 8;
+    g.ks = len;
+    g.s = (int)((K + len - 1) / len);
+    g.rows_per_cta = kWarps / g.s;  // with R = 1
     return g;
 }
 
 int64_t gemv_ws_floats(int64_t n, int64_t K, int batch) {
-    const GemvGeom g = gemv_geom(K, batch);
+    if (!use_tc(batch)) return 0;  // SIMT kernel reduces inside the CTA
+    const GemvGeom g = gemv_tc_geom(K);
     return g.s > 1 ? (int64_t)g.s * batch * n : 0;
 }
 
 int64_t gemv_counters(int64_t n, int64_t K, int batch) {
-    const GemvGeom g = gemv_geom(K, batch);
+    if (!use_tc(batch)) return 0;
+    const GemvGeom g = gemv_tc_geom(K);
     return (n + g.rows_per_cta - 1) / g.rows_per_cta;
 }
 
@@ -233,32 +244,28 @@ int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, c
                 float *y, int64_t ldy, float *ws, int *counters, void *stream) {
     if (n <= 0) return 0;
     if (use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
+    const GemvGeom g = gemv_geom(K, batch);
+    if (g.s > kWarps) return (int)cudaErrorInvalidValue;  // K > 8 * 8192
     cudaStream_t st = (cudaStream_t)stream;
     switch (batch) {
-        case 1: return launch_b<1>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 2: return launch_b<2>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 3: return launch_b<3>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 4: return launch_b<4>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 5: return launch_b<5>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 6: return launch_b<6>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 7: return launch_b<7>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 8: return launch_b<8>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 1: return launch_b<1>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 2: return launch_b<2>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 3: return launch_b<3>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 4: return launch_b<4>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 5: return launch_b<5>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 6: return launch_b<6>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 7: return launch_b<7>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
+        case 8: return launch_b<8>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
         default: return (int)cudaErrorInvalidValue;
     }
 }
 
-template <int B>
-int prepare_b() {
-    return (int)cudaFuncSetAttribute(gemv_bf16_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)(B * kSliceMax * 2));
-}
-
 int gemv_prepare() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     if (gemv_tc_prepare() != 0) g_tc_ok = false;  // no TMA encoder: SIMT only
-    int e = 0;
-    e |= prepare_b<1>(); e |= prepare_b<2>(); e |= prepare_b<3>(); e |= prepare_b<4>();
-    e |= prepare_b<5>(); e |= prepare_b<6>(); e |= prepare_b<7>(); e |= prepare_b<8>();
-    return e;
+    return 0;
 }
 
 int launch_read_bw(const void *p, int64_t bytes, float *sink, void *stream) {

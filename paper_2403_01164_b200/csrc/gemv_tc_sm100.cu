@@ -41,7 +41,8 @@ constexpr int kStages = 6;
 constexpr int kWBytes = kTileM * kTileK * 2;  // 16 KB
 constexpr int kXBytes = kUmmaN * kTileK * 2;  // 2 KB
 constexpr int kThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 epilogue
-constexpr int64_t kSliceMaxTc = 1024;  // short slices: many work units per SM (tail balance)
+constexpr int64_t kSliceMaxTc = 2048;  // k per work unit: enough units per SM for tail balance,
+                                       // long enough to amortise the epilogue
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -119,7 +120,7 @@ struct Units {
 };
 
 template <int B>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
                    int64_t K, int64_t n, const float *__restrict__ bias, float *__restrict__ y,
                    int64_t ldy, Units U, float *__restrict__ ws, int *__restrict__ counters) {
@@ -267,7 +268,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
                         float sum = 0.f;
-                        for (int q = 0; q < U.S; ++q) sum += __ldcg(&ws[((int64_t)q * B + b) * n + row]);
+                        for (int q0 = 0; q0 < U.S; q0 += 8) {  // 8 loads in flight, summed in order
+                            float part[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q0 + q < U.S) part[q] = __ldcg(&ws[((int64_t)(q0 + q) * B + b) * n + row]);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q0 + q < U.S) sum += part[q];
+                        }
                         y[b * ldy + row] = sum + bb;
                     }
                 }
@@ -328,7 +337,8 @@ int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float 
     const GemvGeom g = gemv_tc_geom(K);
     Units U{(n + kTileM - 1) / kTileM, g.s, g.ks};
     const int64_t units = U.n_tiles * U.S;
-    int grid = g_num_sms > 0 ? g_num_sms : 148;
+    // two CTAs per SM (2 x 112 KB smem): one streams while the other drains its epilogue
+    int grid = 2 * (g_num_sms > 0 ? g_num_sms : 148);
     if (units < grid) grid = (int)units;
     gemv_tc_kernel<B><<<grid, kThreads, kSmemBytes, st>>>(mw, mx, K, n, bias, y, ldy, U, ws, counters);
     return (int)cudaGetLastError();

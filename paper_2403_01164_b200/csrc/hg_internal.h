@@ -70,6 +70,9 @@ void pool_destroy(ThreadPool *p);
 int pool_size(const ThreadPool *p);
 // Run fn(arg, worker_index) on every worker (the caller is worker 0); returns when all finished.
 void pool_run(ThreadPool *p, void (*fn)(void *, int), void *arg);
+// Asynchronous form: post() starts workers 1..n-1; join() runs worker 0 on the caller and waits.
+void pool_post(ThreadPool *p, void (*fn)(void *, int), void *arg);
+void pool_join(ThreadPool *p);
 
 }  // namespace hg
 

@@ -52,9 +52,115 @@ int64_t chunk_rows_for(int64_t K, int64_t G, int64_t chunk_bytes) {
     return G * (g < 1 ? 1 : g);
 }
 
+// Least-squares polynomial fit (ascending coefficients) by Householder QR of the
+// Vandermonde matrix; n <= 64 samples, degree <= 6.
+static bool lsq_poly(const double *x, const double *y, int n, int deg, double *coef) {
+    const int m = deg + 1;
+    double A[64][7], b[64];
+    for (int i = 0; i < n; ++i) {
+        double p = 1.0;
+        for (int j = 0; j < m; ++j) {
+            A[i][j] = p;
+            p *= x[i];
+        }
+        b[i] = y[i];
+    }
+    for (int j = 0; j < m; ++j) {
+        double nrm = 0.0;
+        for (int i = j; i < n; ++i) nrm += A[i][j] * A[i][j];
+        nrm = std::sqrt(nrm);
+        if (nrm == 0.0) return false;
+        const double alpha = A[j][j] > 0 ? -nrm : nrm;
+        double v[64];
+        for (int i = 0; i < n; ++i) v[i] = i < j ? 0.0 : A[i][j];
+        v[j] -= alpha;
+        double vn = 0.0;
+        for (int i = j; i < n; ++i) vn += v[i] * v[i];
+        if (vn == 0.0) continue;
+        for (int c = j; c < m; ++c) {
+            double d = 0.0;
+            for (int i = j; i < n; ++i) d += v[i] * A[i][c];
+            d = 2.0 * d / vn;
+            for (int i = j; i < n; ++i) A[i][c] -= d * v[i];
+        }
+        double d = 0.0;
+        for (int i = j; i < n; ++i) d += v[i] * b[i];
+        d = 2.0 * d / vn;
+        for (int i = j; i < n; ++i) b[i] -= d * v[i];
+    }
+    for (int j = m - 1; j >= 0; --j) {  // back substitution R c = Q^T b
+        double s = b[j];
+        for (int c = j + 1; c < m; ++c) s -= A[j][c] * coef[c];
+        if (A[j][j] == 0.0) return false;
+        coef[j] = s / A[j][j];
+    }
+    return true;
+}
+
+static double poly_at(const double *c, int deg, double x) {
+    double r = 0.0;
+    for (int j = deg; j >= 0; --j) r = r * x + c[j];
+    return r;
+}
+
 }  // namespace hg
 
 using namespace hg;
+
+extern "C" HG_API hg_status hg_alpha_solve(const double *alphas, const double *t_cpu, const double *t_com,
+                                           const double *t_pin, int n, int degree, double lo, double hi,
+                                           double seed, double *alpha_out, int *clamped) {
+    if (!alphas || !t_cpu || !t_com || !alpha_out || !clamped)
+        return set_error(HG_EINVAL, "hg_alpha_solve: NULL argument");
+    if (degree < 1 || degree > 6 || n < degree + 1 || n > HG_ABENCH_MAX || !(lo <= hi))
+        return set_error(HG_EINVAL, "hg_alpha_solve: need 1 <= degree <= 6, degree < n <= %d, lo <= hi",
+                         HG_ABENCH_MAX);
+    for (int i = 0; i < n; ++i)
+        if (!std::isfinite(alphas[i]) || !std::isfinite(t_cpu[i]) || !std::isfinite(t_com[i]) ||
+            (t_pin && !std::isfinite(t_pin[i])))
+            return set_error(HG_EINVAL, "hg_alpha_solve: non-finite sample %d", i);
+    double fc[7] = {0}, ft[7] = {0}, fp[7] = {0};
+    if (!lsq_poly(alphas, t_cpu, n, degree, fc) || !lsq_poly(alphas, t_com, n, degree, ft) ||
+        (t_pin && !lsq_poly(alphas, t_pin, n, degree, fp)))
+        return set_error(HG_EINVAL, "hg_alpha_solve: singular fit (repeated alphas?)");
+    auto D = [&](double a) {
+        double com = poly_at(ft, degree, a);
+        if (t_pin) com = std::fmax(com, poly_at(fp, degree, a));
+        return poly_at(fc, degree, a) - com;
+    };
+    double dl = D(lo), dh = D(hi);
+    const double scale = std::fmax(1e-300, std::fmax(std::fabs(poly_at(fc, degree, lo)),
+                                                     std::fabs(poly_at(fc, degree, hi))));
+    *clamped = 0;
+    if (std::fabs(dl) <= 1e-12 * scale && std::fabs(dh) <= 1e-12 * scale) {
+        *alpha_out = seed;  // identical curves: every alpha balances
+        return HG_OK;
+    }
+    if (dl == 0.0) { *alpha_out = lo; return HG_OK; }
+    if (dh == 0.0) { *alpha_out = hi; return HG_OK; }
+    if ((dl > 0) == (dh > 0)) {
+        *alpha_out = std::fabs(dl) < std::fabs(dh) ? lo : hi;
+        *clamped = 1;
+        return HG_OK;
+    }
+    double a = lo, b = hi;
+    for (int it = 0; it < 200; ++it) {
+        const double m = 0.5 * (a + b);
+        const double dm = D(m);
+        if (dm == 0.0 || (b - a) <= 1e-12) {
+            *alpha_out = m;
+            return HG_OK;
+        }
+        if ((dm > 0) == (dl > 0)) {
+            a = m;
+            dl = dm;
+        } else {
+            b = m;
+        }
+    }
+    *alpha_out = 0.5 * (a + b);
+    return HG_OK;
+}
 
 extern "C" HG_API hg_status hg_plan(const hg_rates *r, int64_t N, int64_t K, int batch,
                                     int64_t n_res, int mode, double alpha_fixed, int64_t granule,

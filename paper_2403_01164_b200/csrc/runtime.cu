@@ -154,6 +154,7 @@ struct hg_ctx {
     std::vector<std::pair<size_t, size_t>> copy_ev, gemv_ev;
     cudaEvent_t ev_call0 = nullptr, ev_call1 = nullptr;
     bool call_timed = false;
+    bool stats_open = false;  // ev_call0 recorded since the last reset
 };
 
 namespace {
@@ -349,15 +350,11 @@ hg_status stream_guard(hg_ctx *c, cudaStream_t s) {
     return HG_OK;
 }
 
-hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
+// GPU lanes of one linear: a3 resident GEMV, a4 streamed chunk GEMVs.
+hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const hg_plan_t &p = L.plan;
     const int B = (int)p.batch;
     const int64_t K = p.K;
-    HG_TRY(pump(c));
-    if (p.n_cpu > 0) {  // a2: activation to the host first, so the CPU lane starts early
-        HG_CK(c, cudaMemcpyAsync(c->x_host, L.x, (size_t)B * K * 2, cudaMemcpyDeviceToHost, s));
-        HG_CK(c, cudaEventRecord(c->ev_x, s));
-    }
     if (p.n_res > 0) {  // a3
         HG_TRY(gemv(c, L.x, B, K, L.W_dev, p.n_res, L.bias, L.y, L.ldy, s));
         c->st.bytes_res += 2 * K * p.n_res;
@@ -378,7 +375,28 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         c->st.bytes_str += 2 * K * p.n_str;
         c->st.n_chunks += p.n_chunks;
     }
-    if (p.n_cpu > 0) {  // a5 + a6
+    return HG_OK;
+}
+
+hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
+    const hg_plan_t &p = L.plan;
+    const int B = (int)p.batch;
+    const int64_t K = p.K;
+    HG_TRY(pump(c));
+    if (p.n_cpu == 0) {
+        HG_TRY(enqueue_gpu_lanes(c, L, s));
+        c->st.n_linears++;
+        return HG_OK;
+    }
+    // a2: activation to the host first; the CPU lane is the long pole
+    HG_CK(c, cudaMemcpyAsync(c->x_host, L.x, (size_t)B * K * 2, cudaMemcpyDeviceToHost, s));
+    HG_CK(c, cudaEventRecord(c->ev_x, s));
+    {  // a5 + a3/a4: workers start on the CPU rows the moment x lands, while this thread
+       // enqueues the GPU lanes behind the D2H and then joins the CPU rows itself
+       // (HG_ASYNC_POST=0: enqueue the GPU lanes first, then compute -- A/B switch).
+        static const bool async_post = !getenv("HG_ASYNC_POST") || atoi(getenv("HG_ASYNC_POST")) != 0;
+        hg_status gst = HG_OK;
+        if (!async_post) HG_TRY(enqueue_gpu_lanes(c, L, s));
         HG_TRY(wait_event(c, c->ev_x, &c->st.x_wait_s));
         HG_TRY(wait_event(c, c->ev_ycpu, nullptr));  // bounce buffer free (previous H2D done)
         const auto t0 = clk::now();
@@ -394,7 +412,14 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         job.ldy = p.n_cpu;
         job.block = 16;
         job.next.store(0);
-        pool_run(c->pool, host_job_run, &job);
+        if (async_post) {
+            pool_post(c->pool, host_job_run, &job);
+            gst = enqueue_gpu_lanes(c, L, s);
+            pool_join(c->pool);  // always: workers reference `job`
+        } else {
+            pool_run(c->pool, host_job_run, &job);
+        }
+        if (gst != HG_OK) return gst;
         c->st.cpu_busy_s += secs(t0, clk::now());
         c->st.bytes_cpu += 2 * K * p.n_cpu;
         HG_CK(c, cudaMemcpyAsync(c->ycpu_dev, c->ycpu_host, (size_t)B * p.n_cpu * 4,
@@ -407,6 +432,7 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
     c->st.n_linears++;
     return HG_OK;
 }
+
 
 hg_status validate_plan(hg_ctx *c, const hg_plan_t &p) {
     if (p.batch < 1 || p.batch > HG_MAX_BATCH) return set_error(HG_EINVAL, "batch %lld", (long long)p.batch);
@@ -450,19 +476,13 @@ hg_status begin_call(hg_ctx *c, cudaStream_t s) {
     if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
     HG_CK(c, cudaSetDevice(c->device));
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
-    if (c->cfg.collect_stats) {
-        // reuse the timing events of the previous call: wait for it to finish
-        if (c->have_last) HG_CK(c, cudaEventSynchronize(c->ev_done));
-        c->tev_used = 0;
-        c->copy_ev.clear();
-        c->gemv_ev.clear();
-    }
-    const int64_t launches = c->st.gpu_launches;
-    std::memset(&c->st, 0, sizeof c->st);
-    c->st.gpu_launches = launches;  // cumulative (hg_reset_stats zeroes it)
     HG_TRY(stream_guard(c, s));
-    HG_CK(c, cudaEventRecord(c->ev_call0, s));
-    c->st.wall_s = -1;
+    // Stats accumulate over all calls since hg_reset_stats (no per-call sync, so the
+    // copy stream keeps running ahead across calls while statistics are collected).
+    if (!c->stats_open) {
+        HG_CK(c, cudaEventRecord(c->ev_call0, s));
+        c->stats_open = true;
+    }
     return HG_OK;
 }
 
@@ -670,7 +690,9 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
     if (c->ws_floats < 1) c->ws_floats = 1;
     CREATE_CK(cudaMalloc((void **)&c->ws, (size_t)c->ws_floats * 4));
-    c->n_counters = gemv_counters(cfg.max_n, 8, 1) + 1;  // worst case: smallest rows-per-CTA
+    gemv_set_tc_min_batch(1);  // split-K counters are used by the tcgen05 path only
+    c->n_counters = gemv_counters(cfg.max_n, cfg.max_k, HG_MAX_BATCH) + 1;
+    gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
     CREATE_CK(cudaMalloc((void **)&c->counters, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
@@ -875,8 +897,71 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
 
 HG_API hg_status hg_reset_stats(hg_ctx *c) {
     if (!c) return set_error(HG_EINVAL, "NULL ctx");
+    if (c->device >= 0 && c->have_last) {  // pending timing events belong to the old window
+        HG_CK(c, cudaSetDevice(c->device));
+        HG_CK(c, cudaEventSynchronize(c->ev_done));
+        HG_CK(c, cudaStreamSynchronize(c->copy));
+    }
+    c->tev_used = 0;
+    c->copy_ev.clear();
+    c->gemv_ev.clear();
+    c->stats_open = false;
+    c->call_timed = false;
     std::memset(&c->st, 0, sizeof c->st);
     return HG_OK;
+}
+
+// ---------------------------------------------------------------- alpha benchmark
+HG_API hg_status hg_alpha_bench(hg_ctx *c, const hg_opt_layer *layers, int n_layers, void *h, int batch,
+                                double alpha_seed, const hg_abench_cfg *cfg_in, hg_abench_result *out,
+                                void *stream) {
+    if (!c || !layers || n_layers < 1 || !h || !out) return set_error(HG_EINVAL, "NULL argument");
+    if (!(alpha_seed >= 0.0 && alpha_seed <= 1.0)) return set_error(HG_EINVAL, "alpha_seed outside [0,1]");
+    hg_abench_cfg cfg = {0.06, 0.02, 2, 1};
+    if (cfg_in) cfg = *cfg_in;
+    if (!(cfg.gamma > 0) || !(cfg.lambda > 0) || cfg.reps < 1 || cfg.degree < 1)
+        return set_error(HG_EINVAL, "bad alpha-bench config");
+    // window [seed - gamma, seed + gamma] ∩ [0, 1] in steps of lambda (reading R9)
+    const double lo = std::max(0.0, alpha_seed - cfg.gamma), hi = std::min(1.0, alpha_seed + cfg.gamma);
+    std::vector<double> pts;
+    const int npts = (int)std::floor((hi - lo) / cfg.lambda + 1e-9) + 1;
+    for (int i = 0; i < npts && (int)pts.size() < HG_ABENCH_MAX; ++i) pts.push_back(lo + i * cfg.lambda);
+    if (hi - pts.back() > 1e-12 && (int)pts.size() < HG_ABENCH_MAX) pts.push_back(hi);
+    if ((int)pts.size() < cfg.degree + 1) return set_error(HG_EINVAL, "window has too few alphas");
+
+    std::vector<hg_opt_layer> work(layers, layers + n_layers);
+    const int saved_stats = c->cfg.collect_stats;
+    c->cfg.collect_stats = 1;
+    std::memset(out, 0, sizeof *out);
+    out->alpha_seed = alpha_seed;
+    hg_rates unit = {1, 1, 1, 1, 1, 1, 1};
+    hg_status st = HG_OK;
+    for (size_t i = 0; i < pts.size() && st == HG_OK; ++i) {
+        for (auto &L : work)
+            for (int j = 0; j < 4 && st == HG_OK; ++j) {
+                const hg_plan_t &p = L.lin[j].plan;
+                st = hg_plan(&unit, p.N, p.K, batch, p.n_res, HG_ALPHA_FIXED, pts[i], p.granule,
+                             c->cfg.chunk_bytes, &L.lin[j].plan);
+            }
+        if (st != HG_OK) break;
+        st = hg_stack(c, work.data(), n_layers, h, batch, stream);  // warm the pipeline at this alpha
+        if (st == HG_OK) st = hg_reset_stats(c);
+        for (int r = 0; r < cfg.reps && st == HG_OK; ++r) st = hg_stack(c, work.data(), n_layers, h, batch, stream);
+        hg_stats_t s;
+        if (st == HG_OK) st = hg_stats(c, &s);
+        if (st == HG_OK) {
+            out->alpha[i] = pts[i];
+            out->t_cpu[i] = s.cpu_busy_s / cfg.reps;
+            out->t_com[i] = s.link_busy_s / cfg.reps;
+            out->t_step[i] = s.wall_s / cfg.reps;
+        }
+    }
+    c->cfg.collect_stats = saved_stats;
+    hg_reset_stats(c);
+    if (st != HG_OK) return st;
+    out->n = (int)pts.size();
+    return hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, nullptr, out->n, cfg.degree, pts.front(),
+                          pts.back(), alpha_seed, &out->alpha_bar, &out->clamped);
 }
 
 // ---------------------------------------------------------------- measurement

@@ -39,14 +39,22 @@ class ThreadPool {
     }
     int size() const { return n_; }
 
-    void run(void (*fn)(void *, int), void *arg) {
+    // Start fn(arg, i) on workers 1..n-1 and return at once (the caller may enqueue GPU
+    // work meanwhile); join() then runs fn(arg, 0) on the caller and waits for all.
+    void post(void (*fn)(void *, int), void *arg) {
         fn_ = fn;
         arg_ = arg;
         done_.store(0, std::memory_order_relaxed);
         gen_.fetch_add(1, std::memory_order_acq_rel);
         if (sleepers_.load(std::memory_order_acquire) > 0) futex_wake();
-        fn(arg, 0);
+    }
+    void join() {
+        fn_(arg_, 0);
         while (done_.load(std::memory_order_acquire) != n_ - 1) _mm_pause();
+    }
+    void run(void (*fn)(void *, int), void *arg) {
+        post(fn, arg);
+        join();
     }
 
    private:
@@ -106,5 +114,7 @@ ThreadPool *pool_create(int nthreads, int first_core) { return new ThreadPool(nt
 void pool_destroy(ThreadPool *p) { delete p; }
 int pool_size(const ThreadPool *p) { return p->size(); }
 void pool_run(ThreadPool *p, void (*fn)(void *, int), void *arg) { p->run(fn, arg); }
+void pool_post(ThreadPool *p, void (*fn)(void *, int), void *arg) { p->post(fn, arg); }
+void pool_join(ThreadPool *p) { p->join(); }
 
 }  // namespace hg

@@ -93,6 +93,26 @@ class LayerTrace(ctypes.Structure):
     _fields_ = [(n, ctypes.c_void_p) for n in ("a", "y_qkv", "v", "y_o", "h1", "a2", "y_fc1", "u", "y_fc2")]
 
 
+HG_ABENCH_MAX = 64
+
+
+class AbenchCfg(ctypes.Structure):
+    _fields_ = [("gamma", ctypes.c_double), ("lambda_", ctypes.c_double), ("degree", ctypes.c_int32),
+                ("reps", ctypes.c_int32)]
+
+
+class AbenchResult(ctypes.Structure):
+    _fields_ = [("alpha_seed", ctypes.c_double), ("alpha_bar", ctypes.c_double), ("n", ctypes.c_int32),
+                ("clamped", ctypes.c_int32)] + [(f, ctypes.c_double * HG_ABENCH_MAX)
+                                                for f in ("alpha", "t_cpu", "t_com", "t_step")]
+
+    def as_dict(self):
+        n = self.n
+        return {"alpha_seed": self.alpha_seed, "alpha_bar": self.alpha_bar, "clamped": bool(self.clamped),
+                "alpha": list(self.alpha[:n]), "t_cpu": list(self.t_cpu[:n]), "t_com": list(self.t_com[:n]),
+                "t_step": list(self.t_step[:n])}
+
+
 _vp, _i32, _i64, _dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _P = ctypes.POINTER
 _sig = {
@@ -113,6 +133,9 @@ _sig = {
     "hg_dist_unique_id": (_i32, [_vp]),
     "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
     "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hg_alpha_solve": (_i32, [_P(_dbl), _P(_dbl), _P(_dbl), _P(_dbl), _i32, _i32, _dbl, _dbl, _dbl,
+                              _P(_dbl), _P(_i32)]),
+    "hg_alpha_bench": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _dbl, _P(AbenchCfg), _P(AbenchResult), _vp]),
     "hg_stats": (_i32, [_vp, _P(Stats)]),
     "hg_reset_stats": (_i32, [_vp]),
 }
@@ -170,6 +193,16 @@ def hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed=0.0, granule=128, chunk
     _check(_lib.hg_plan(ctypes.byref(rates), N, K, batch, n_res, mode, float(alpha_fixed), granule,
                         chunk_bytes, ctypes.byref(p)))
     return p
+
+
+def hg_alpha_solve(alphas, t_cpu, t_com, degree, lo, hi, seed, t_pin=None):
+    """Returns (alpha_bar, clamped)."""
+    n = len(alphas)
+    arr = lambda v: (_dbl * n)(*[float(t) for t in v])
+    out, cl = _dbl(), _i32()
+    _check(_lib.hg_alpha_solve(arr(alphas), arr(t_cpu), arr(t_com), None if t_pin is None else arr(t_pin), n,
+                               degree, float(lo), float(hi), float(seed), ctypes.byref(out), ctypes.byref(cl)))
+    return out.value, bool(cl.value)
 
 
 def hg_dist_unique_id() -> bytes:
@@ -246,6 +279,15 @@ class Context:
         r = Rates()
         _check(_lib.hg_measure(self._h, _ptr(W_host), N, K, batch, 1 if under_load else 0, ctypes.byref(r)))
         return r
+
+    def hg_alpha_bench(self, layers, h, batch, alpha_seed, gamma=0.06, lam=0.02, degree=2, reps=1,
+                       stream=None) -> AbenchResult:
+        arr = (OptLayer * len(layers))(*layers)
+        cfg = AbenchCfg(gamma, lam, degree, reps)
+        res = AbenchResult()
+        _check(_lib.hg_alpha_bench(self._h, arr, len(layers), _ptr(h), batch, float(alpha_seed), ctypes.byref(cfg),
+                                   ctypes.byref(res), _stream(stream)))
+        return res
 
     def hg_dist_init(self, nranks, rank, uid: bytes):
         buf = ctypes.create_string_buffer(uid, 128)

@@ -109,3 +109,34 @@ def test_gpu_calls_on_host_only_context_fail_cleanly():
         with pytest.raises(hg.HgError) as e:
             ctx.hg_gemv(0, 1, 1, 8, 0, None, 0)
         assert e.value.status == hg.HG_ESTATE
+
+
+# ---------------------------------------------------------------- alpha benchmark solver (pure host)
+def test_hg_alpha_solve_matches_oracle():
+    rng = np.random.default_rng(21)
+    for it in range(300):
+        seed = float(rng.uniform(0.1, 0.9))
+        a = oracle.alpha_window(seed, float(rng.choice([0.05, 0.1, 0.2])), float(rng.choice([0.01, 0.02])))
+        c, k = rng.uniform(0.5, 5.0, 2)
+        q1, q2 = rng.uniform(-0.5, 0.5, 2)
+        tc = [(1 - x) * c + q1 * x * x + 0.001 * rng.standard_normal() for x in a]
+        tm = [x * k + q2 * x * x + 0.001 * rng.standard_normal() for x in a]
+        deg = int(rng.integers(1, 4))
+        use_pin = rng.random() < 0.3
+        tp = [x * k * 1.3 for x in a] if use_pin else None
+        got = hg.hg_alpha_solve(a, tc, tm, deg, a[0], a[-1], seed, t_pin=tp)
+        ref = oracle.alpha_bench_solve(a, tc, tm, deg, a[0], a[-1], seed, t_pin=tp)
+        assert got[1] == ref[1]
+        assert abs(got[0] - ref[0]) < 1e-9, (it, got, ref)
+
+
+def test_hg_alpha_solve_closed_forms_and_errors():
+    a = oracle.alpha_window(0.7, 0.2, 0.02)
+    got, cl = hg.hg_alpha_solve(a, [(1 - x) * 3 for x in a], list(a), 1, a[0], a[-1], 0.7)
+    assert not cl and abs(got - 0.75) < 1e-12
+    t = [1 + x for x in a]
+    assert hg.hg_alpha_solve(a, t, t, 2, a[0], a[-1], 0.7) == (0.7, False)
+    with pytest.raises(hg.HgError):
+        hg.hg_alpha_solve([0.1, 0.2], [1, 2], [2, 1], 2, 0.1, 0.2, 0.1)   # n < degree + 1
+    with pytest.raises(hg.HgError):
+        hg.hg_alpha_solve([0.1, 0.1, 0.1], [1, 2, 3], [2, 1, 0], 1, 0.1, 0.1, 0.1)  # singular fit
