@@ -133,7 +133,11 @@ typedef struct {
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
     double timeout_s;    /* bound on every host wait (default 60 s)                      */
     int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 5; 0 = never) */
-    int32_t _reserved;
+    int32_t handshake;   /* streamed-chunk synchronisation: 1 = device tags (default): the copy
+                            stream writes an arrival tag per chunk (cuStreamWriteValue32) and waits
+                            on the slot's consumed tag (cuStreamWaitValue32), one persistent GEMV
+                            launch per linear consumes chunks as they land; 0 = host events, one
+                            GEMV launch per chunk (A/B reference)                                 */
 } hg_config;
 
 /* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last

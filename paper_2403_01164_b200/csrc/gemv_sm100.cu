@@ -1,24 +1,36 @@
-// gemv_sm100.cu -- device GEMV for the resident and streamed slices
-// (SURVEY 8(a) a3/a4): y[b, j] = sum_k x[b,k] * W[j,k] (+ bias[j]), B = 1..8.
+// gemv_sm100.cu -- the GPU lanes of a heterogeneous linear:
+//   y[b, j] = sum_k x[b,k] * W[j,k] (+ bias[j]),   B = 1..8 (SIMT; tcgen05 for B >= 5 lives in
+//   gemv_tc_sm100.cu).
 //
-// The GPU share of a heterogeneous linear ("The GPU, in turn, generates
-// results once the communication process is completed"), run over HBM-resident
-// rows and over each streamed chunk as it lands in the device ring.  At batch
-// 1-8 the arithmetic intensity is B flop/byte, >= 30x below the B200 ridge, so
-// the kernel is an HBM stream: 128-bit non-allocating loads of W along K with up
-// to 16 loads in flight per lane, x read through L1, fp32 FMAs, warp shuffles.
+// One persistent launch per linear covers BOTH GPU lanes: the HBM-resident rows
+// [0, n_res) and every streamed chunk of rows [n_res, n_res+n_str) as it lands in
+// the device ring ("The GPU, in turn, generates results once the
+// communication process is completed"; the overlap of Fig. 5c).  At batch
+// 1-8 the arithmetic intensity is B flop/byte, >= 30x below the B200 ridge, so the
+// kernel is an HBM stream and is built like one:
 //
-// Reduction order (fixed by K alone, so every launch -- the resident GEMV, any
-// streamed chunk, any n -- produces bit-identical outputs):
-//   * K is cut into P = ceil(K/8192) parts of equal length (multiple of 8);
-//   * within a part one warp owns the row: lane l accumulates 16-byte vectors
-//     l, l+32, l+64, ... in ascending order (8 FMAs each, in k order), then a
-//     butterfly shuffle sums the 32 lanes (lane 0's value is used);
-//   * the P part sums are added in part order (through shared memory) and the
-//     bias is added last.
-// How many rows a warp carries (R) and how many loads are in flight (U) only
-// change which thread does the work, not the order, so they are picked per
-// launch to fill the 148 SMs.  No global workspace, atomics or fences.
+//   * the last warp, one lane (producer): walks this CTA's work in order; for a streamed
+//     chunk it first spins on the chunk's arrival tag (written by the copy stream
+//     with cuStreamWriteValue32 right after the chunk's cudaMemcpyAsync), then
+//     moves W row segments into a ring of shared-memory stages with 1-D TMA bulk
+//     copies (cp.async.bulk ... mbarrier::complete_tx, L2 evict-first) -- tens of
+//     KB in flight per SM with one thread issuing;
+//   * warps 0..W-1 (consumers): take stages round-robin, FMA the bf16 W segment
+//     against x (staged once per launch in shared memory) in fp32, butterfly
+//     reduce, release the stage;
+//   * when every CTA has drained a chunk's stages, the last one writes the slot's
+//     `consumed` tag, which the copy stream waits on (cuStreamWaitValue32) before
+//     it overwrites the slot with a later chunk.  No host round trip per chunk.
+//
+// Work split (depends on K and B only, never on the partition, so every row -- resident or
+// streamed, any alpha, any chunking -- is reduced identically; SURVEY 8(c) c4 split invariance):
+//   * K is cut into P parts of equal length len (multiple of 8, <= 8192 elements for B = 1,
+//     <= 4096 for B >= 3); CTA (p, j) handles part p of rows [j*R/gp, (j+1)*R/gp) of every
+//     source (resident block, then chunk 0, 1, ...), gp = #CTAs per part;
+//   * a part sum: lane l accumulates 16-byte vectors l, l+32, l+64, ... in ascending order
+//     (8 fmaf each, k ascending), then a butterfly over the 32 lanes;
+//   * y = (((S_0 + S_1) + ...) + S_{P-1}) + bias: for P > 1 the part sums go through a
+//     global workspace and the last of a row's P arrivals adds them in part order.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,24 +42,130 @@
 namespace hg {
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
-constexpr int64_t kPartMax = 8192;  // elements of K one warp reduces (16 KB of a W row)
+// Per-batch configuration: rows per stage R (x reuse across rows), stages S, consumer warps W,
+// max part length.  S must be a multiple of W: consumer warp w takes the groups it = w (mod W),
+// so it only ever waits for the phase right after the one it consumed itself from the same
+// stage (an mbarrier parity wait two phases ahead would pass at once).
+template <int B> struct Cfg;
+template <> struct Cfg<1> { static constexpr int R = 1, S = 8, W = 8, PART = 8192; };
+template <> struct Cfg<2> { static constexpr int R = 2, S = 10, W = 10, PART = 4096; };
+template <> struct Cfg<3> { static constexpr int R = 2, S = 10, W = 10, PART = 4096; };
+template <> struct Cfg<4> { static constexpr int R = 2, S = 10, W = 10, PART = 4096; };
+template <> struct Cfg<5> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
+template <> struct Cfg<6> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
+template <> struct Cfg<7> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
+template <> struct Cfg<8> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
+template <int B> constexpr int threads_for() { return (Cfg<B>::W + 1) * 32; }
 
-__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
+inline int part_max(int B) { return B <= 1 ? 8192 : 4096; }
+
+struct SArgs {
+    const uint16_t *x;
+    int64_t K, len;  // part length (elements)
+    int P, gp;
+    const uint8_t *W_res;
+    int64_t n_res;
+    const uint8_t *ring;
+    int64_t slot_bytes;
+    int64_t nslots;
+    int64_t seq0;
+    int64_t n_chunks, chunk_rows, n_str;
+    const uint32_t *arrived;  // null: chunks already present, no tags
+    uint32_t *consumed;
+    uint32_t *slot_cnt;
+    const float *bias;
+    float *y;
+    int64_t ldy;
+    float *ws;
+    uint32_t *row_cnt;
+    uint32_t *err;
+    unsigned long long timeout_ns;
+};
+
+struct Src {
+    const uint8_t *base;
+    int64_t rows, g0;
+    int64_t slot;
+    uint32_t tag;
+    bool flagged;
+};
+
+__device__ __forceinline__ Src source(const SArgs &a, int64_t s) {  // s = -1: resident block
+    Src r;
+    if (s < 0) {
+        r.base = a.W_res;
+        r.rows = a.n_res;
+        r.g0 = 0;
+        r.slot = -1;
+        r.tag = 0;
+        r.flagged = false;
+    } else {
+        const int64_t seq = a.seq0 + s;
+        r.slot = seq % a.nslots;
+        r.base = a.ring + r.slot * a.slot_bytes;
+        const int64_t r0 = s * a.chunk_rows;
+        r.rows = a.chunk_rows < a.n_str - r0 ? a.chunk_rows : a.n_str - r0;
+        r.g0 = a.n_res + r0;
+        r.tag = (uint32_t)(seq + 1);
+        r.flagged = a.arrived != nullptr;
+    }
     return r;
 }
 
-__device__ __forceinline__ uint4 ldg_cached(const uint4 *p) {
-    uint4 r;
-    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ float lo_f(uint32_t v) { return __uint_as_float(v << 16); }
@@ -70,130 +188,221 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// grid = ceil(n / rows_per_cta); block = 32*NW.  Warp w: row group w / P, K-part w % P.
-template <int B, int R, int U, int NW>
-__global__ void __launch_bounds__(NW * 32)
-    gemv_rows_kernel(const uint4 *__restrict__ x, int64_t K, const uint4 *__restrict__ W, int64_t n,
-                     const float *__restrict__ bias, float *__restrict__ y, int64_t ldy, int P,
-                     int64_t part_len) {
-    __shared__ float red[NW][R][B];
+__device__ void signal_consumed(const SArgs &a, int64_t slot, uint32_t tag) {
+    __threadfence();
+    const uint32_t old = atomicAdd(&a.slot_cnt[slot], 1u);
+    if (old == gridDim.x - 1) {
+        atomicExch(&a.slot_cnt[slot], 0u);
+        __threadfence();
+        st_release_sys(&a.consumed[slot], tag);
+    }
+}
+
+template <int B>
+__global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const __grid_constant__ SArgs a) {
+    constexpr int R = Cfg<B>::R, S = Cfg<B>::S, kConsumerWarps = Cfg<B>::W;
+    static_assert(S % kConsumerWarps == 0, "stage count must be a multiple of the consumer warps");
+    extern __shared__ __align__(128) uint8_t smem[];
+    const int64_t kvmax = a.len >> 3;            // vectors per (full) part
+    const int64_t unit_bytes = a.len * 2;        // stage slot per row
+    uint64_t *bars = (uint64_t *)smem;           // full[S], empty[S]
+    uint8_t *stages = smem + 128;                // S * R * unit_bytes
+    uint4 *xs = (uint4 *)(stages + (int64_t)S * R * unit_bytes);  // [B][kvmax]
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
+    const uint32_t stage0 = smem_u32(stages);
+
+    const int p = blockIdx.x / a.gp, j = blockIdx.x - p * a.gp;
+    const int64_t k0 = (int64_t)p * a.len;
+    const int64_t klen = a.K - k0 < a.len ? a.K - k0 : a.len;
+    const int kv = (int)(klen >> 3);
+    const uint32_t bytes_p = (uint32_t)(klen * 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int groups = NW / P;
-    const int g = warp / P, p = warp - g * P;
-    const bool active = g < groups;
-    const int64_t row0 = ((int64_t)blockIdx.x * groups + g) * R;
-    const int64_t Kv = K >> 3;
 
-    float acc[R][B];
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int b = 0; b < B; ++b) acc[r][b] = 0.f;
-
-    if (active) {
-        const int64_t k0 = (int64_t)p * part_len;
-        const int64_t klen = (K - k0) < part_len ? (K - k0) : part_len;
-        const int kv = (int)(klen >> 3);
-        const uint4 *wp[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int64_t rr = row0 + r < n ? row0 + r : n - 1;
-            wp[r] = W + rr * Kv + (k0 >> 3);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(full0 + 8 * s, 1);
+            mbar_init(empty0 + 8 * s, 1);
         }
-        const uint4 *xp = x + (k0 >> 3);
-        for (int j = lane; j < kv; j += 32 * U) {
-            uint4 wv[U][R];
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // x part p -> shared memory, once per launch (every source has the same x)
+    {
+        const uint4 *xg = (const uint4 *)a.x;
+        const int64_t Kv = a.K >> 3;
+        for (int64_t i = threadIdx.x; i < (int64_t)B * kv; i += blockDim.x) {
+            const int64_t b = i / kv, v = i - b * kv;
+            xs[b * kvmax + v] = xg[b * Kv + (k0 >> 3) + v];
+        }
+    }
+    __syncthreads();
+
+    const int64_t s_begin = a.n_res > 0 ? -1 : 0;
+    if (warp == kConsumerWarps) {
+        // ------------------------------------------------------------ producer
+        if (lane != 0) return;
+        uint64_t policy;
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+        int64_t issued = 0, done = 0;  // groups issued / known consumed (all < done)
+        constexpr int QMAX = 32;
+        int64_t q_slot[QMAX], q_last[QMAX];
+        uint32_t q_tag[QMAX];
+        int qh = 0, qn = 0;
+        auto consume_upto = [&](int64_t g) {
+            while (done <= g) {
+                mbar_wait(empty0 + 8 * (int)(done % S), (uint32_t)((done / S) & 1));
+                ++done;
+            }
+        };
+        auto flush = [&]() {
+            while (qn > 0 && q_last[qh] < done) {
+                signal_consumed(a, q_slot[qh], q_tag[qh]);
+                qh = (qh + 1) % QMAX;
+                --qn;
+            }
+        };
+        // Wait for a chunk's arrival tag while releasing whatever the consumers have drained:
+        // the copy stream may need one of those slots before it can deliver this chunk.
+        auto wait_arrival = [&](const Src &src) {
+            const unsigned long long t0 = globaltimer();
+            for (;;) {
+                if ((int32_t)(ld_acquire(a.arrived + src.slot) - src.tag) >= 0) return;
+                while (done < issued && mbar_test(empty0 + 8 * (int)(done % S), (uint32_t)((done / S) & 1))) ++done;
+                flush();
+                __nanosleep(64);
+                if (globaltimer() - t0 > a.timeout_ns) {
+                    atomicOr(a.err, 1u);
+                    return;
+                }
+            }
+        };
+        for (int64_t s = s_begin; s < a.n_chunks; ++s) {
+            const Src src = source(a, s);
+            if (src.flagged) wait_arrival(src);
+            const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
+            for (int64_t r = ra; r < rb; r += R) {
+                const int st = (int)(issued % S);
+                if (issued >= S) {
+                    consume_upto(issued - S);
+                    flush();
+                }
+                const int nrows = rb - r < R ? (int)(rb - r) : R;
+                const uint32_t fb = full0 + 8 * st;
+                mbar_expect_tx(fb, (uint32_t)nrows * bytes_p);
+                const uint8_t *g = src.base + (r * a.K + k0) * 2;
+#pragma unroll 1
+                for (int q = 0; q < nrows; ++q)
+                    bulk_g2s(stage0 + (uint32_t)((st * R + q) * unit_bytes), g + q * a.K * 2, bytes_p, fb, policy);
+                ++issued;
+            }
+            if (src.flagged) {
+                if (qn == QMAX) {
+                    consume_upto(q_last[qh]);
+                    flush();
+                }
+                const int qt = (qh + qn) % QMAX;
+                q_slot[qt] = src.slot;
+                q_tag[qt] = src.tag;
+                q_last[qt] = issued - 1;
+                ++qn;
+                flush();
+            }
+        }
+        consume_upto(issued - 1);
+        flush();
+        return;
+    }
+
+    // ---------------------------------------------------------------- consumers
+    int64_t it = 0;
+    for (int64_t s = s_begin; s < a.n_chunks; ++s) {
+        const Src src = source(a, s);
+        const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
+        for (int64_t r = ra; r < rb; r += R, ++it) {
+            if ((int)(it % kConsumerWarps) != warp) continue;
+            const int st = (int)(it % S);
+            const int nrows = rb - r < R ? (int)(rb - r) : R;
+            mbar_wait(full0 + 8 * st, (uint32_t)((it / S) & 1));
+            const uint4 *sw = (const uint4 *)(stages + (int64_t)st * R * unit_bytes);
+            float acc[R][B];
 #pragma unroll
-            for (int u = 0; u < U; ++u)
+            for (int q = 0; q < R; ++q)
 #pragma unroll
-                for (int r = 0; r < R; ++r)
-                    if (j + 32 * u < kv) wv[u][r] = ldg_stream(wp[r] + j + 32 * u);
+                for (int b = 0; b < B; ++b) acc[q][b] = 0.f;
+            for (int v = lane; v < kv; v += 32) {
+                float xf[B][8];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                if (j + 32 * u < kv) {
+                for (int b = 0; b < B; ++b) {
+                    const uint4 xv = xs[b * kvmax + v];
+                    xf[b][0] = lo_f(xv.x);
+                    xf[b][1] = hi_f(xv.x);
+                    xf[b][2] = lo_f(xv.y);
+                    xf[b][3] = hi_f(xv.y);
+                    xf[b][4] = lo_f(xv.z);
+                    xf[b][5] = hi_f(xv.z);
+                    xf[b][6] = lo_f(xv.w);
+                    xf[b][7] = hi_f(xv.w);
+                }
 #pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        const uint4 xv = ldg_cached(xp + b * Kv + j + 32 * u);
-                        const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
-                                             lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+                for (int q = 0; q < R; ++q) {
+                    if (q < nrows) {
+                        const uint4 wv = sw[q * kvmax + v];
 #pragma unroll
-                        for (int r = 0; r < R; ++r) fma8(acc[r][b], wv[u][r], xf);
+                        for (int b = 0; b < B; ++b) fma8(acc[q][b], wv, xf[b]);
                     }
                 }
             }
-        }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty0 + 8 * st);
+            // butterfly; lane q*B + b then owns part sum (q, b) (static indices: acc stays in registers)
+            float mine = 0.f;
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+            for (int q = 0; q < R; ++q)
 #pragma unroll
-            for (int b = 0; b < B; ++b) acc[r][b] = warp_sum(acc[r][b]);
-    }
-    if (P == 1) {
-        if (active && lane == 0) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int64_t row = row0 + r;
-                if (row < n) {
-                    const float bb = bias ? bias[row] : 0.f;
-#pragma unroll
-                    for (int b = 0; b < B; ++b) y[b * ldy + row] = acc[r][b] + bb;
+                for (int b = 0; b < B; ++b) {
+                    const float t = warp_sum(acc[q][b]);
+                    if (lane == q * B + b) mine = t;
                 }
+            const int myq = lane / B, myb = lane - myq * B;
+            const bool act = lane < R * B && myq < nrows;
+            const int64_t g = src.g0 + r + myq;
+            if (a.P == 1) {
+                if (act) a.y[myb * a.ldy + g] = mine + (a.bias ? a.bias[g] : 0.f);
+                continue;
             }
-        }
-        return;
-    }
-    if (active && lane == 0) {
-#pragma unroll
-        for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int b = 0; b < B; ++b) red[warp][r][b] = acc[r][b];
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < groups * R * B; t += NW * 32) {
-        const int gg = t / (R * B), rb = t - gg * (R * B), r = rb / B, b = rb - r * B;
-        const int64_t row = ((int64_t)blockIdx.x * groups + gg) * R + r;
-        if (row < n) {
-            float s = 0.f;
-            for (int q = 0; q < P; ++q) s += red[gg * P + q][r][b];
-            y[b * ldy + row] = s + (bias ? bias[row] : 0.f);
+            float *wsr = a.ws + g * (int64_t)a.P * B;
+            if (act) {
+                wsr[p * B + myb] = mine;
+                __threadfence();
+            }
+            __syncwarp();
+            bool last = false;
+            if (lane < nrows) last = atomicAdd(&a.row_cnt[src.g0 + r + lane], 1u) == (uint32_t)(a.P - 1);
+            const unsigned lastmask = __ballot_sync(0xffffffffu, last);
+            if (act && ((lastmask >> myq) & 1u)) {
+                __threadfence();
+                float sum = 0.f;
+                for (int pp = 0; pp < a.P; ++pp) sum += __ldcg(&wsr[pp * B + myb]);
+                a.y[myb * a.ldy + g] = sum + (a.bias ? a.bias[g] : 0.f);
+            }
+            if (last) a.row_cnt[src.g0 + r + lane] = 0;
         }
     }
 }
 
-int g_sms = 148;
-
-// 4-warp CTAs (short CTAs: small tail at the end of a launch) unless a row needs
-// more than 4 K-parts (K > 32768).  Neither NW nor R changes the numerics.
-template <int B, int R, int U>
-int launch_rows(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
-                int64_t ldy, int P, int64_t part_len, cudaStream_t st) {
-    if (P <= 4) {
-        const int rows_per_cta = (4 / P) * R;
-        const unsigned grid = (unsigned)((n + rows_per_cta - 1) / rows_per_cta);
-        gemv_rows_kernel<B, R, U, 4><<<grid, 128, 0, st>>>((const uint4 *)x, K, (const uint4 *)W, n, bias,
-                                                           y, ldy, P, part_len);
-    } else {
-        const int rows_per_cta = (kWarps / P) * R;
-        const unsigned grid = (unsigned)((n + rows_per_cta - 1) / rows_per_cta);
-        gemv_rows_kernel<B, R, U, kWarps><<<grid, kThreads, 0, st>>>((const uint4 *)x, K, (const uint4 *)W, n,
-                                                                     bias, y, ldy, P, part_len);
-    }
-    return (int)cudaGetLastError();
-}
-
-// R (rows per warp) trades per-warp reuse of x against the number of warps; it
-// does not change numerics, so choose it per launch from n.
 template <int B>
-int launch_b(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
-             int64_t ldy, int P, int64_t part_len, cudaStream_t st) {
-    if constexpr (B <= 4) {
-        const int64_t ctas_r2 = (n + (kWarps / P) * 2 - 1) / ((kWarps / P) * 2);
-        if (ctas_r2 >= 4 * g_sms)
-            return launch_rows<B, 2, (B <= 2 ? 8 : 4)>(x, K, W, n, bias, y, ldy, P, part_len, st);
-    }
-    return launch_rows<B, 1, (B <= 2 ? 16 : 8)>(x, K, W, n, bias, y, ldy, P, part_len, st);
+constexpr size_t smem_bytes_for(int64_t len) {
+    return 128 + (size_t)Cfg<B>::S * Cfg<B>::R * len * 2 + (size_t)B * len * 2;
 }
 
 // ---------------------------------------------------------------- read-BW probe
+__device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
+    return r;
+}
+
 __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float *sink) {
     uint32_t acc = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec;
@@ -202,6 +411,33 @@ __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float 
         acc ^= v.x ^ v.y ^ v.z ^ v.w;
     }
     if (acc == 0x9e3779b9u) sink[0] = (float)acc;  // practically never; keeps loads live
+}
+
+int g_sms = 148;
+
+template <int B>
+int launch_b(const SArgs &a, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.P * a.gp));
+    cfg.blockDim = dim3(threads_for<B>());
+    cfg.dynamicSmemBytes = smem_bytes_for<B>(a.len);
+    cfg.stream = st;
+    // With tags every CTA must be resident at once: a chunk's slot is only refilled after all
+    // CTAs drained its previous occupant (one CTA per SM; cooperative launch guarantees it).
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.arrived ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B>, a);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
+template <int B>
+int prepare_b() {
+    return (int)cudaFuncSetAttribute(gemv_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_bytes_for<B>(Cfg<B>::PART));
 }
 
 }  // namespace
@@ -214,58 +450,116 @@ static bool g_tc_ok = true;  // false when the TMA encoder / tcgen05 setup is un
 
 void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }
 
-static bool use_tc(int batch) { return g_tc_ok && g_tc_min_batch > 0 && batch >= g_tc_min_batch; }
+bool gemv_use_tc(int batch) { return g_tc_ok && g_tc_min_batch > 0 && batch >= g_tc_min_batch; }
 
 GemvGeom gemv_geom(int64_t K, int batch) {
-    if (use_tc(batch)) return gemv_tc_geom(K);
+    if (gemv_use_tc(batch)) return gemv_tc_geom(K);
     GemvGeom g;
-    const int64_t P = (K + kPartMax - 1) / kPartMax;
+    const int64_t pm = part_max(batch);
+    const int64_t P = (K + pm - 1) / pm;
     int64_t len = (K + P - 1) / P;
     len = (len + 7) / 8 * 8;
     g.ks = len;
     g.s = (int)((K + len - 1) / len);
-    g.rows_per_cta = kWarps / g.s;  // with R = 1
+    g.rows_per_cta = 0;
     return g;
 }
 
 int64_t gemv_ws_floats(int64_t n, int64_t K, int batch) {
-    if (!use_tc(batch)) return 0;  // SIMT kernel reduces inside the CTA
-    const GemvGeom g = gemv_tc_geom(K);
+    if (gemv_use_tc(batch)) {
+        const GemvGeom g = gemv_tc_geom(K);
+        return g.s > 1 ? (int64_t)g.s * batch * n : 0;
+    }
+    const GemvGeom g = gemv_geom(K, batch);
     return g.s > 1 ? (int64_t)g.s * batch * n : 0;
 }
 
 int64_t gemv_counters(int64_t n, int64_t K, int batch) {
-    if (!use_tc(batch)) return 0;
-    const GemvGeom g = gemv_tc_geom(K);
-    return (n + g.rows_per_cta - 1) / g.rows_per_cta;
+    if (gemv_use_tc(batch)) {
+        const GemvGeom g = gemv_tc_geom(K);
+        return (n + g.rows_per_cta - 1) / g.rows_per_cta;
+    }
+    return gemv_geom(K, batch).s > 1 ? n : 0;  // one arrival counter per row
+}
+
+int launch_gemv_stream(const StreamLaunch &L, void *stream) {
+    if (L.n_res + L.n_str <= 0) return 0;
+    if (L.batch < 1 || L.batch > HG_MAX_BATCH) return (int)cudaErrorInvalidValue;
+    const GemvGeom g = gemv_geom(L.K, L.batch);
+    SArgs a;
+    a.x = (const uint16_t *)L.x;
+    a.K = L.K;
+    a.len = g.ks;
+    a.P = g.s;
+    a.gp = g_sms / a.P;
+    if (a.gp < 1) return (int)cudaErrorInvalidValue;
+    a.W_res = (const uint8_t *)L.W_res;
+    a.n_res = L.n_res;
+    a.ring = L.ring;
+    a.slot_bytes = L.slot_bytes;
+    a.nslots = L.nslots > 0 ? L.nslots : 1;
+    a.seq0 = L.seq0;
+    a.n_chunks = L.n_str > 0 ? L.n_chunks : 0;
+    a.chunk_rows = L.chunk_rows;
+    a.n_str = L.n_str;
+    a.arrived = L.arrived;
+    a.consumed = L.consumed;
+    a.slot_cnt = L.slot_cnt;
+    a.bias = L.bias;
+    a.y = L.y;
+    a.ldy = L.ldy;
+    a.ws = L.ws;
+    a.row_cnt = L.row_cnt;
+    a.err = L.err;
+    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
+    if (a.P > 1 && (!a.ws || !a.row_cnt)) return (int)cudaErrorInvalidValue;
+    if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (L.batch) {
+        case 1: return launch_b<1>(a, st);
+        case 2: return launch_b<2>(a, st);
+        case 3: return launch_b<3>(a, st);
+        case 4: return launch_b<4>(a, st);
+        case 5: return launch_b<5>(a, st);
+        case 6: return launch_b<6>(a, st);
+        case 7: return launch_b<7>(a, st);
+        default: return launch_b<8>(a, st);
+    }
 }
 
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
                 float *y, int64_t ldy, float *ws, int *counters, void *stream) {
     if (n <= 0) return 0;
-    if (use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
-    const GemvGeom g = gemv_geom(K, batch);
-    if (g.s > kWarps) return (int)cudaErrorInvalidValue;  // K > 8 * 8192
-    cudaStream_t st = (cudaStream_t)stream;
-    switch (batch) {
-        case 1: return launch_b<1>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 2: return launch_b<2>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 3: return launch_b<3>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 4: return launch_b<4>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 5: return launch_b<5>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 6: return launch_b<6>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 7: return launch_b<7>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        case 8: return launch_b<8>(x, K, W, n, bias, y, ldy, g.s, g.ks, st);
-        default: return (int)cudaErrorInvalidValue;
-    }
+    if (gemv_use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
+    StreamLaunch L{};
+    L.x = x;
+    L.batch = batch;
+    L.K = K;
+    L.W_res = W;
+    L.n_res = n;
+    L.bias = bias;
+    L.y = y;
+    L.ldy = ldy;
+    L.ws = ws;
+    L.row_cnt = (uint32_t *)counters;
+    return launch_gemv_stream(L, stream);
 }
 
 int gemv_prepare() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    int e = 0;
+    e |= prepare_b<1>();
+    e |= prepare_b<2>();
+    e |= prepare_b<3>();
+    e |= prepare_b<4>();
+    e |= prepare_b<5>();
+    e |= prepare_b<6>();
+    e |= prepare_b<7>();
+    e |= prepare_b<8>();
     if (gemv_tc_prepare() != 0) g_tc_ok = false;  // no TMA encoder: SIMT only
-    return 0;
+    return e;
 }
 
 int launch_read_bw(const void *p, int64_t bytes, float *sink, void *stream) {

@@ -33,6 +33,34 @@ int64_t gemv_counters(int64_t n, int64_t K, int batch);
 // Launch: y[b*ldy + j] = sum_k x[b,k] W[j,k] (+bias[j]), j < n.  Returns a CUDA error code (int).
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
                 float *y, int64_t ldy, float *ws, int *counters, void *stream);
+bool gemv_use_tc(int batch);
+
+// One persistent SIMT launch over the GPU lanes of a linear: resident rows [0, n_res) of W_res,
+// then streamed chunk c (rows [n_res + c*chunk_rows, ...)) in ring slot (seq0 + c) % nslots.
+// With `arrived` set the kernel waits for arrived[slot] >= seq+1 (copy stream's
+// cuStreamWriteValue32) before reading a chunk and, once every CTA has drained it, writes
+// consumed[slot] = seq+1 (the copy stream's cuStreamWaitValue32 before reusing the slot).
+// With arrived == NULL the chunks are taken as present (no tags).  Rows of y are global.
+struct StreamLaunch {
+    const void *x;
+    int batch;
+    int64_t K;
+    const void *W_res;
+    int64_t n_res;
+    const uint8_t *ring;
+    int64_t slot_bytes, nslots;
+    int64_t seq0, n_chunks, chunk_rows, n_str;
+    const uint32_t *arrived;
+    uint32_t *consumed, *slot_cnt;
+    const float *bias;
+    float *y;
+    int64_t ldy;
+    float *ws;
+    uint32_t *row_cnt;
+    uint32_t *err;
+    double timeout_s;
+};
+int launch_gemv_stream(const StreamLaunch &L, void *stream);
 
 // ---------------------------------------------------------------- glue_sm100.cu
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,

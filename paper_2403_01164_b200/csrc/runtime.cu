@@ -60,7 +60,33 @@ struct ChunkReq {
 struct Inflight {
     ChunkReq req;
     int slot;
+    int64_t seq;
 };
+
+// cuStreamWaitValue32 / cuStreamWriteValue32 (driver entry points; stream memory operations)
+typedef int (*memop_fn_t)(void *stream, unsigned long long addr, uint32_t value, unsigned int flags);
+constexpr unsigned kWaitGeq = 0x0;      // CU_STREAM_WAIT_VALUE_GEQ: (int32)(*addr - value) >= 0
+constexpr unsigned kWriteDefault = 0x0; // CU_STREAM_WRITE_VALUE_DEFAULT: fence before the write
+memop_fn_t g_wait_value = nullptr, g_write_value = nullptr;
+
+bool load_memops() {
+    static int state = -1;
+    if (state >= 0) return state == 1;
+    void *w = nullptr, *v = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &v, cudaEnableDefault, &q2) == cudaSuccess &&
+        q2 == cudaDriverEntryPointSuccess) {
+        g_wait_value = (memop_fn_t)w;
+        g_write_value = (memop_fn_t)v;
+        state = 1;
+    } else {
+        cudaGetLastError();
+        state = 0;
+    }
+    return state == 1;
+}
 
 struct HostJob {
     host_rows_fn fn;
@@ -119,6 +145,10 @@ struct hg_ctx {
     std::vector<char> slot_used;
     std::deque<Inflight> inflight;
     int64_t next_seq = 0;
+    int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
+    bool tags = false;      // cfg.handshake == 1 and stream memory operations available
+    uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4]
+    uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr;
     std::vector<ChunkReq> future;
     size_t fpos = 0;
     bool fwrap = false;
@@ -205,6 +235,18 @@ hg_status kerr(hg_ctx *c, int e, const char *what) {
     return HG_OK;
 }
 
+// A tag wait inside a kernel that timed out leaves err != 0 (read at synchronising calls).
+hg_status check_device_error(hg_ctx *c) {
+    if (!c->err) return HG_OK;
+    uint32_t e = 0;
+    HG_CK(c, cudaMemcpy(&e, c->err, 4, cudaMemcpyDeviceToHost));
+    if (e) {
+        c->error = true;
+        return set_error(HG_ETIMEOUT, "a GEMV waited longer than %.1f s for a streamed chunk", c->cfg.timeout_s);
+    }
+    return HG_OK;
+}
+
 hg_status wait_event(hg_ctx *c, cudaEvent_t ev, double *waited) {
     const auto t0 = clk::now();
     for (int spin = 0;; ++spin) {
@@ -236,9 +278,27 @@ cudaEvent_t tev_get(hg_ctx *c, size_t *idx) {
 }
 
 // ---------------------------------------------------------------- chunk ring
-hg_status issue_copy(hg_ctx *c, const ChunkReq &r) {
-    const int slot = (int)(c->next_seq % c->nslots);
-    if (c->slot_used[slot]) HG_CK(c, cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
+hg_status memop(hg_ctx *c, memop_fn_t fn, cudaStream_t s, const uint32_t *addr, uint32_t v, unsigned flags) {
+    const int e = fn((void *)s, (unsigned long long)(uintptr_t)addr, v, flags);
+    if (e != 0) {
+        c->error = true;
+        return set_error(HG_ECUDA, "stream memory operation failed (CUresult %d)", e);
+    }
+    return HG_OK;
+}
+
+// Enqueue chunk `r` into the next ring slot on the copy stream.  `bound`: a GEMV that consumes
+// it is already enqueued (tags mode), so it is not tracked as in flight.
+hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
+    const int64_t seq = c->next_seq;
+    const int slot = (int)(seq % c->nslots);
+    if (c->tags) {
+        // the slot's previous occupant (seq - nslots) must have been drained by its GEMV
+        if (seq >= c->nslots)
+            HG_TRY(memop(c, g_wait_value, c->copy, c->consumed + slot, (uint32_t)(seq - c->nslots + 1), kWaitGeq));
+    } else if (c->slot_used[slot]) {
+        HG_CK(c, cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
+    }
     size_t i0 = 0, i1 = 0;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (c->cfg.collect_stats) {
@@ -247,7 +307,8 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r) {
     }
     HG_CK(c, cudaMemcpyAsync(c->ring + (int64_t)slot * c->slot_bytes, r.src, (size_t)r.bytes,
                              cudaMemcpyHostToDevice, c->copy));
-    HG_CK(c, cudaEventRecord(c->ev_arrived[slot], c->copy));
+    if (c->tags) HG_TRY(memop(c, g_write_value, c->copy, c->arrived + slot, (uint32_t)(seq + 1), kWriteDefault));
+    else HG_CK(c, cudaEventRecord(c->ev_arrived[slot], c->copy));
     if (c->cfg.collect_stats && e0) {
         e1 = tev_get(c, &i1);
         if (e1) {
@@ -256,8 +317,22 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r) {
         }
     }
     c->slot_used[slot] = 1;
-    c->inflight.push_back({r, slot});
+    if (!bound) c->inflight.push_back({r, slot, seq});
     ++c->next_seq;
+    return HG_OK;
+}
+
+// Give up prefetched chunks nobody will consume (the call sequence changed): release their slots.
+hg_status drop_front(hg_ctx *c) {
+    const Inflight &f = c->inflight.front();
+    if (c->tags) HG_TRY(memop(c, g_write_value, c->copy, c->consumed + f.slot, (uint32_t)(f.seq + 1), kWriteDefault));
+    else HG_CK(c, cudaEventRecord(c->ev_free[f.slot], c->copy));
+    c->inflight.pop_front();
+    return HG_OK;
+}
+
+hg_status drop_inflight(hg_ctx *c) {
+    while (!c->inflight.empty()) HG_TRY(drop_front(c));
     return HG_OK;
 }
 
@@ -273,17 +348,51 @@ bool future_next(hg_ctx *c, ChunkReq *out) {
 
 hg_status pump(hg_ctx *c) {
     ChunkReq r;
+    while (c->prebound > 0) {  // chunks an enqueued GEMV waits for: issue unconditionally
+        if (!future_next(c, &r)) return set_error(HG_ESTATE, "bound chunk missing from the schedule");
+        HG_TRY(issue_copy(c, r, true));
+        --c->prebound;
+    }
     while ((int)c->inflight.size() < c->nslots && future_next(c, &r)) HG_TRY(issue_copy(c, r));
+    return HG_OK;
+}
+
+// Tags mode: bind the chunks of one linear to the GEMV about to be enqueued.  They must occupy
+// consecutive sequence numbers (the kernel derives slot = (seq0 + c) % nslots): the in-flight
+// prefix followed by the next entries of the schedule.  Anything else is dropped and the
+// schedule restarts with this linear.
+hg_status bind_chunks(hg_ctx *c, const std::vector<ChunkReq> &mine, int64_t *seq0) {
+    const size_t n = mine.size();
+    size_t m = std::min(n, c->inflight.size());
+    bool ok = true;
+    for (size_t i = 0; i < m && ok; ++i) ok = c->inflight[i].req == mine[i];
+    if (ok && m < n) {  // the rest must be next in the schedule
+        size_t pos = c->fpos;
+        for (size_t i = m; i < n && ok; ++i) {
+            if (pos >= c->future.size()) {
+                if (!c->fwrap || c->future.empty()) { ok = false; break; }
+                pos = 0;
+            }
+            ok = c->future[pos++] == mine[i];
+        }
+    }
+    if (!ok) {
+        HG_TRY(drop_inflight(c));
+        c->future = mine;
+        c->fpos = 0;
+        c->fwrap = false;
+        m = 0;
+    }
+    *seq0 = m > 0 ? c->inflight.front().seq : c->next_seq;
+    for (size_t i = 0; i < m; ++i) c->inflight.pop_front();
+    c->prebound += (int64_t)(n - m);
     return HG_OK;
 }
 
 // The slot holding `r`, with `stream` ordered after its arrival.
 hg_status acquire(hg_ctx *c, const ChunkReq &r, cudaStream_t stream, int *slot) {
-    while (!c->inflight.empty() && !(c->inflight.front().req == r)) {
-        // a prefetched chunk nobody will consume (the call sequence changed): free its slot
-        HG_CK(c, cudaEventRecord(c->ev_free[c->inflight.front().slot], c->copy));
-        c->inflight.pop_front();
-    }
+    while (!c->inflight.empty() && !(c->inflight.front().req == r)) HG_TRY(drop_front(c));
+    int64_t seq = 0;
     if (c->inflight.empty()) {
         // not prefetched: the planned sequence diverged -> restart it here
         c->future.clear();
@@ -291,12 +400,17 @@ hg_status acquire(hg_ctx *c, const ChunkReq &r, cudaStream_t stream, int *slot) 
         HG_TRY(issue_copy(c, r));
     }
     *slot = c->inflight.front().slot;
-    HG_CK(c, cudaStreamWaitEvent(stream, c->ev_arrived[*slot], 0));
+    seq = c->inflight.front().seq;
+    if (c->tags) HG_TRY(memop(c, g_wait_value, stream, c->arrived + *slot, (uint32_t)(seq + 1), kWaitGeq));
+    else HG_CK(c, cudaStreamWaitEvent(stream, c->ev_arrived[*slot], 0));
     return HG_OK;
 }
 
 hg_status release(hg_ctx *c, int slot, cudaStream_t stream) {
-    HG_CK(c, cudaEventRecord(c->ev_free[slot], stream));
+    if (c->tags)
+        HG_TRY(memop(c, g_write_value, stream, c->consumed + slot, (uint32_t)(c->inflight.front().seq + 1),
+                     kWriteDefault));
+    else HG_CK(c, cudaEventRecord(c->ev_free[slot], stream));
     c->inflight.pop_front();
     return HG_OK;
 }
@@ -355,6 +469,58 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const hg_plan_t &p = L.plan;
     const int B = (int)p.batch;
     const int64_t K = p.K;
+    if (c->tags && !gemv_use_tc(B)) {
+        // a3 + a4 in ONE persistent launch: resident rows, then each chunk as its arrival tag lands
+        std::vector<ChunkReq> mine;
+        push_chunks(mine, p, L.W_host);
+        int64_t seq0 = 0;
+        if (p.n_str > 0) HG_TRY(bind_chunks(c, mine, &seq0));
+        const int64_t n = p.n_res + p.n_str;
+        if (gemv_ws_floats(n, K, B) > c->ws_floats || gemv_counters(n, K, B) > c->n_counters)
+            return set_error(HG_EINVAL, "GEMV of %lld rows x K=%lld exceeds the context workspace", (long long)n,
+                             (long long)K);
+        StreamLaunch S{};
+        S.x = L.x;
+        S.batch = B;
+        S.K = K;
+        S.W_res = L.W_dev;
+        S.n_res = p.n_res;
+        S.ring = c->ring;
+        S.slot_bytes = c->slot_bytes;
+        S.nslots = c->nslots;
+        S.seq0 = seq0;
+        S.n_chunks = p.n_str > 0 ? p.n_chunks : 0;
+        S.chunk_rows = p.chunk_rows;
+        S.n_str = p.n_str;
+        S.arrived = c->arrived;
+        S.consumed = c->consumed;
+        S.slot_cnt = c->slot_cnt;
+        S.bias = L.bias;
+        S.y = L.y;
+        S.ldy = L.ldy;
+        S.ws = c->ws;
+        S.row_cnt = (uint32_t *)c->counters;
+        S.err = c->err;
+        S.timeout_s = c->cfg.timeout_s;
+        if (n > 0) {
+            size_t i0 = 0, i1 = 0;
+            cudaEvent_t e0 = nullptr;
+            if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
+            HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv stream launch"));
+            c->st.gpu_launches++;
+            if (e0) {
+                cudaEvent_t e1 = tev_get(c, &i1);
+                if (e1) {
+                    HG_CK(c, cudaEventRecord(e1, s));
+                    c->gemv_ev.push_back({i0, i1});
+                }
+            }
+        }
+        c->st.bytes_res += 2 * K * p.n_res;
+        c->st.bytes_str += 2 * K * p.n_str;
+        if (p.n_str > 0) c->st.n_chunks += p.n_chunks;
+        return pump(c);
+    }
     if (p.n_res > 0) {  // a3
         HG_TRY(gemv(c, L.x, B, K, L.W_dev, p.n_res, L.bias, L.y, L.ldy, s));
         c->st.bytes_res += 2 * K * p.n_res;
@@ -615,6 +781,8 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     cfg->timeout_s = 60.0;
     cfg->gemv_tc_min_batch = 5;
     if (const char *v = getenv("HG_GEMV_TC_MIN_BATCH")) cfg->gemv_tc_min_batch = atoi(v);
+    cfg->handshake = 1;
+    if (const char *v = getenv("HG_HANDSHAKE")) cfg->handshake = atoi(v);
     return HG_OK;
 }
 
@@ -683,19 +851,27 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     CREATE_CK(cudaEventCreate(&c->ev_call0));
     CREATE_CK(cudaEventCreate(&c->ev_call1));
-    gemv_set_tc_min_batch(1);  // workspace for the larger of the two geometries
-    c->ws_floats = gemv_ws_floats(cfg.max_n, cfg.max_k, HG_MAX_BATCH);
-    gemv_set_tc_min_batch(0);
-    c->ws_floats = std::max(c->ws_floats, gemv_ws_floats(cfg.max_n, cfg.max_k, HG_MAX_BATCH));
+    // workspace / counters: the largest any batch needs on either GEMV (SIMT stream, tcgen05)
+    c->ws_floats = 1;
+    c->n_counters = 1;
+    for (int tcmin : {1, 0})
+        for (int b = 1; b <= HG_MAX_BATCH; ++b) {
+            gemv_set_tc_min_batch(tcmin);
+            c->ws_floats = std::max(c->ws_floats, gemv_ws_floats(cfg.max_n, cfg.max_k, b));
+            c->n_counters = std::max(c->n_counters, gemv_counters(cfg.max_n, cfg.max_k, b) + 1);
+        }
     gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
-    if (c->ws_floats < 1) c->ws_floats = 1;
     CREATE_CK(cudaMalloc((void **)&c->ws, (size_t)c->ws_floats * 4));
-    gemv_set_tc_min_batch(1);  // split-K counters are used by the tcgen05 path only
-    c->n_counters = gemv_counters(cfg.max_n, cfg.max_k, HG_MAX_BATCH) + 1;
-    gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
     CREATE_CK(cudaMalloc((void **)&c->counters, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
+    c->tags = cfg.handshake != 0 && load_memops();
+    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 4) * 4));
+    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 4) * 4));
+    c->arrived = c->tagmem;
+    c->consumed = c->tagmem + c->nslots;
+    c->slot_cnt = c->tagmem + 2 * c->nslots;
+    c->err = c->tagmem + 3 * c->nslots;
     CREATE_CK(cudaDeviceSynchronize());
 #undef CREATE_CK
     *out = c;
@@ -716,7 +892,7 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
         if (c->copy) cudaStreamDestroy(c->copy);
         for (void *p : {(void *)c->ring, (void *)c->ycpu_dev, (void *)c->ws, (void *)c->counters,
                         (void *)c->sink, c->act, (void *)c->yscr, c->h1, (void *)c->ylocal,
-                        (void *)c->gbuf})
+                        (void *)c->gbuf, (void *)c->tagmem})
             if (p) cudaFree(p);
         if (c->x_host) cudaFreeHost(c->x_host);
         if (c->ycpu_host) cudaFreeHost(c->ycpu_host);
@@ -872,6 +1048,7 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
     if (c->device >= 0 && c->call_timed) {
         HG_CK(c, cudaSetDevice(c->device));
         HG_CK(c, cudaEventSynchronize(c->ev_done));
+        HG_TRY(check_device_error(c));
         float ms = 0;
         HG_CK(c, cudaEventElapsedTime(&ms, c->ev_call0, c->ev_call1));
         c->st.wall_s = ms * 1e-3;
@@ -976,10 +1153,13 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     HG_CK(c, cudaSetDevice(c->device));
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     HG_TRY(check_ptr(c, W_host, false, "W_host"));
-    HG_CK(c, cudaDeviceSynchronize());
-    c->inflight.clear();  // the ring is reused below; any prefetch state is dropped
+    // the ring is reused below: release every prefetched chunk, then wait for the device
+    HG_TRY(pump(c));
+    HG_TRY(drop_inflight(c));
     c->future.clear();
     c->fpos = 0;
+    HG_CK(c, cudaDeviceSynchronize());
+    HG_TRY(check_device_error(c));
     std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
 
     const int64_t wbytes = 2 * N * K;

@@ -66,7 +66,7 @@ class Config(ctypes.Structure):
                 ("max_k", ctypes.c_int64), ("max_n", ctypes.c_int64), ("cpu_threads", ctypes.c_int32),
                 ("cpu_first", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
                 ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double),
-                ("gemv_tc_min_batch", ctypes.c_int32), ("_reserved", ctypes.c_int32)]
+                ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

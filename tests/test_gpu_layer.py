@@ -104,3 +104,25 @@ def test_stack_wrap_prefetch_repeatable():
             torch.cuda.synchronize()
             outs.append(bits(h))
         assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[0], outs[2])
+
+
+def test_stack_wrap_then_other_calls():
+    """wrap_prefetch streams the next token's first chunks; a different call in between drops them
+    (their slots are released) and later stacks still match layer-by-layer results."""
+    H, F, B = 256, 1024, 1
+    with hg.Context(0, chunk_bytes=256 << 10, ring_bytes=2 << 20, max_k=4096, max_n=8192,
+                    wrap_prefetch=1) as c:
+        keep = []
+        layers = [make_layer(c, H, F, B, layer=l, alpha=0.8, keep=keep)[0] for l in range(2)]
+        h0 = gen.uniform_bf16(8, 996, B * H, 1.0).reshape(B, H)
+        ref = dev(h0)
+        for L in layers:
+            c.hg_layer(L, ref, B)
+        for _ in range(2):
+            h = dev(h0)
+            c.hg_stack(layers, h, B)
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(h), bits(ref))
+            h2 = dev(h0)
+            c.hg_layer(layers[1], h2, B)  # diverges from the wrapped schedule
+            torch.cuda.synchronize()

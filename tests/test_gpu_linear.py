@@ -218,4 +218,42 @@ def test_stats_lane_breakdown():
         assert s.n_linears == 1 and s.bytes_res == 1024 * 4096 * 2
         assert s.bytes_str == 1536 * 4096 * 2 and s.bytes_cpu == 1536 * 4096 * 2
         assert s.n_chunks == 6 and s.link_busy_s > 0 and s.gpu_busy_s > 0 and s.cpu_busy_s > 0
-        assert s.wall_s > 0 and s.gpu_launches >= 5
+        assert s.wall_s > 0 and s.gpu_launches >= 2
+
+
+@pytest.mark.parametrize("B", [1, 3, 6])
+def test_tags_ring_smaller_than_linear(B):
+    """Device-tag pipeline with 2 ring slots and 32 chunks per linear: the copy stream refills a
+    slot only after every CTA of the (cooperative) GEMV drained it; results match the oracle."""
+    with hg.Context(0, chunk_bytes=64 << 10, ring_bytes=128 << 10, max_k=256, max_n=8192) as c:
+        assert c.config.handshake == 1
+        x, W, b = gen.linear_inputs(31, 0, "fc1", B, 4096, 256)
+        for n_res, alpha in ((0, 1.0), (512, 1.0), (0, 0.6)):
+            y = _linear(c, x, W, b, B, n_res, alpha)
+            ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+            assert ok, (n_res, alpha, worst)
+
+
+@pytest.mark.parametrize("B", [1, 2, 4, 8])
+def test_event_path_equals_tag_path(ctx, B):
+    """handshake=0 (host events, one GEMV per chunk) and the default device-tag pipeline compute
+    identical bits: same kernel arithmetic, only the synchronisation differs."""
+    x, W, b = gen.linear_inputs(32, 0, "fc2", B, 2048, 7168)
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=8192, max_n=4096, handshake=0) as ce:
+        y_ev = _linear(ce, x, W, b, B, 256, 0.7)
+    y_tag = _linear(ctx, x, W, b, B, 256, 0.7)
+    assert np.array_equal(y_ev, y_tag)
+    assert oracle.within_tol(y_tag, oracle.linear(x, W, b))[0]
+
+
+def test_schedule_divergence_drops_prefetch():
+    """Chunks prefetched for a call that never comes are released (tags written) and the
+    next, different linear restarts the schedule without stalling the copy stream."""
+    with hg.Context(0, chunk_bytes=64 << 10, ring_bytes=512 << 10, max_k=1024, max_n=8192) as c:
+        x1, W1, b1 = gen.linear_inputs(33, 0, "fc1", 1, 2048, 1024)
+        x2, W2, b2 = gen.linear_inputs(34, 0, "fc2", 1, 1024, 1024)
+        for it in range(3):
+            y1 = _linear(c, x1, W1, b1, 1, 0, 0.9)
+            y2 = _linear(c, x2, W2, b2, 1, 128, 0.5)
+            assert oracle.within_tol(y1, oracle.linear(x1, W1, b1))[0], it
+            assert oracle.within_tol(y2, oracle.linear(x2, W2, b2))[0], it

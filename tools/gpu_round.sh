@@ -1,0 +1,37 @@
+#!/bin/bash
+# One GPU call: parity tests, the bench line, the ncu launch list of the bench
+# command and one `--set full` capture of the top kernel.  Outputs in gpurun_out/<tag>/.
+#   bash tools/gpu_round.sh <tag> [what...]    what: tests bench launches full micro (default: all)
+tag=${1:-run}; shift
+what=${*:-tests bench launches full}
+out=gpurun_out/$tag
+mkdir -p $out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,pcie.link.gen.current,pcie.link.width.current --format=csv > $out/smi.txt 2>&1
+has() { [[ " $what " == *" $1 "* ]]; }
+if has tests; then
+  timeout 1500 python -m pytest tests -m gpu -x -q > $out/pytest_gpu.txt 2>&1; echo "pytest rc=$?" >> $out/pytest_gpu.txt
+  tail -3 $out/pytest_gpu.txt
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $out/smoke.txt 2>&1; echo "smoke rc=$?" >> $out/smoke.txt
+fi
+if has bench; then
+  timeout 900 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench rc=$?"
+  tail -c 3000 $out/bench.json
+fi
+if has micro; then
+  timeout 600 python tools/microbench.py > $out/micro.txt 2>&1; tail -30 $out/micro.txt
+fi
+if has launches; then
+  # launch list of the bench command (serialised, cold-cache: compare shares)
+  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+    python bench.py --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline > $out/launches_bench.json 2>&1
+  echo "launches rc=$?"
+  python tools/ncu_summary.py launches $out/launches.csv > $out/launches_summary.md 2>&1; head -20 $out/launches_summary.md
+fi
+if has full; then
+  # the top kernel (streamed-chunk GEMV) inside the step
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemv -s 300 -c 4 \
+    -o $out/prof_gemv python bench.py --layers 4 --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline \
+    > $out/full_bench.log 2>&1
+  echo "full rc=$?"
+  python tools/ncu_summary.py full $out/prof_gemv.ncu-rep > $out/full_summary.md 2>&1; head -60 $out/full_summary.md
+fi
