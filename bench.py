@@ -138,49 +138,57 @@ def run_reference(args):
     return 0
 
 
-def chunk_gemv_roofline(ctx, plans, layers, B, torch, pk, iters=40):
-    """Average device time of the step's streamed-chunk GEMV launches (same kernel, shapes and
-    launch configuration as in the step), each launch reading a different 1 GiB-buffer window so
-    the weights come from HBM, timed with CUDA events on the launching stream.
+def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20):
+    """Average device time of the step's GEMV launches -- one persistent launch per linear over
+    its resident rows and all its streamed chunks (hg_gemv_replay: same kernel, grid and
+    per-chunk work split as in the step, chunks read from ring slots 0..n_chunks-1 with the
+    arrival tags skipped) -- timed with CUDA events on the launching stream, L2 flushed (a
+    256 MiB write) between launches so W comes from HBM.
 
-    Algorithmic bytes per launch = 2*K*rows (the chunk of W; x/bias/y are < 0.1%).
+    Algorithmic bytes per launch = 2*K*(n_res + n_str) (the W rows the GPU lanes must read;
+    x, bias and y are < 0.1%).  Returns None when the GEMV runs on the tcgen05 path.
     """
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    buf = torch.empty(1 << 29, dtype=torch.int16, device="cuda").random_(-3000, 3000)  # 1 GiB
     s = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     tot_bytes, tot_time, detail = 0.0, 0.0, {}
     for name, p in plans.items():
-        if p.n_str <= 0:
+        n_gpu = p.n_res + p.n_str
+        if n_gpu <= 0:
             continue
-        rows, K = min(p.chunk_rows, p.n_str), p.K
-        cbytes = 2 * K * rows
-        nwin = (buf.numel() * 2) // cbytes
-        x = torch.empty((B, K), dtype=torch.int16, device="cuda").random_(-3000, 3000)
-        y = torch.empty((B, rows), device="cuda")
-        for i in range(3):
-            ctx.hg_gemv(x, B, rows, K, buf.data_ptr() + (i % nwin) * cbytes, None, y, stream=s)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for i in range(iters):
-            ctx.hg_gemv(x, B, rows, K, buf.data_ptr() + ((i * 7) % nwin) * cbytes, None, y, stream=s)
-        e1.record(s)
-        torch.cuda.synchronize()
-        t = e0.elapsed_time(e1) * 1e-3 / iters
-        n_launch = p.n_chunks * layers
-        tot_bytes += cbytes * n_launch
-        tot_time += t * n_launch
-        detail[name] = {"rows": rows, "K": K, "us": round(t * 1e6, 2), "GBps": round(cbytes / t / 1e9, 1)}
-    del buf
+        x = torch.empty((B, p.K), dtype=torch.int16, device="cuda").random_(-3000, 3000)
+        y = torch.empty((B, p.N), device="cuda")
+        try:
+            for _ in range(3):
+                ctx.hg_gemv_replay(p, x, None, None, y, stream=s)
+        except Exception as e:  # tcgen05 batches: no replay entry point
+            return {"unavailable": str(e)}
+        ts = []
+        for _ in range(iters):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            ctx.hg_gemv_replay(p, x, None, None, y, stream=s)
+            e1.record(s)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        t = statistics.mean(ts)
+        nbytes = 2 * p.K * n_gpu
+        tot_bytes += nbytes * layers
+        tot_time += t * layers
+        detail[name] = {"rows": n_gpu, "chunks": p.n_chunks, "K": p.K, "us": round(t * 1e6, 2),
+                        "GBps": round(nbytes / t / 1e9, 1)}
+    del flush
     if tot_time <= 0:
         return None
     gbps = tot_bytes / tot_time / 1e9
-    return {"bound": "hbm", "kernel": "gemv_rows_kernel (streamed-chunk GEMV)" if B < 5 else
-            "gemv_tc_kernel (streamed-chunk GEMV, tcgen05)", "achieved": round(gbps, 1), "peak": hbm_peak,
-            "unit": "GB/s", "frac": round(gbps / hbm_peak, 4), "traffic": None,
+    return {"bound": "hbm", "kernel": "gemv_stream_kernel (persistent per-linear GEMV, TMA bulk staged)",
+            "achieved": round(gbps, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4),
+            "traffic": None,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy BW)" if "hbm_gbs" in pk else "fallback 6650 GB/s",
             "per_linear": detail,
-            "note": "CUDA-event replay of the step's chunk-GEMV launches on HBM-resident (cold) chunks; in the "
-                    "step the chunk was just written by the copy engine and may hit L2"}
+            "note": "bytes = 2*K*(n_res+n_str) per launch; CUDA events around each hg_gemv_replay launch (the "
+                    "step's launch configuration, arrival tags skipped), L2 flushed between launches; mean"}
 
 
 # ---------------------------------------------------------------- our arm
@@ -321,7 +329,7 @@ def main_arm(args):
     # ---- dominant kernel: the streamed-chunk GEMV, replayed with CUDA events on cold data ----
     roof = None
     if rank == 0:
-        roof = chunk_gemv_roofline(ctx, plans, args.layers, B, torch, pk)
+        roof = gemv_roofline(ctx, plans, args.layers, B, torch, pk)
 
     times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
     if world > 1:

@@ -303,6 +303,16 @@ HG_API hg_status hg_gemv(hg_ctx *ctx, const void *x_dev, int batch, int64_t n, i
                          const void *W_dev, const float *bias_dev, float *y_dev, int64_t ldy,
                          void *stream);
 
+/* Measurement entry point: the persistent GEMV launch hg_linear_planned would enqueue for
+ * `plan` (resident rows from W_dev, then the plan's n_chunks streamed chunks read from ring
+ * slots 0..n_chunks-1), with the chunks taken as already present -- no arrival tags, nothing
+ * released -- so its CUDA-event time is the kernel's own duration in the step's launch
+ * configuration.  Streamed outputs are computed from whatever the ring holds (timing only);
+ * resident outputs are exact.  y [batch, N] fp32 device.  Batches on the tcgen05 path and
+ * plans with more chunks than ring slots return HG_EUNSUPPORTED / HG_EINVAL. */
+HG_API hg_status hg_gemv_replay(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
+                                const void *W_dev, const float *bias_dev, float *y_dev, void *stream);
+
 /* CPU lane alone: y_host[b*n + j] = x_host[b,:] . W_host[j,:] (+ bias_host[j]) on
  * the context's thread pool.  All host pointers (need not be pinned).  Works on
  * host-only contexts. */

@@ -29,8 +29,9 @@
 //     source (resident block, then chunk 0, 1, ...), gp = #CTAs per part;
 //   * a part sum: lane l accumulates 16-byte vectors l, l+32, l+64, ... in ascending order
 //     (8 fmaf each, k ascending), then a butterfly over the 32 lanes;
-//   * y = (((S_0 + S_1) + ...) + S_{P-1}) + bias: for P > 1 the part sums go through a
-//     global workspace and the last of a row's P arrivals adds them in part order.
+//   * y = (((S_0 + S_1) + ...) + S_{P-1}) + bias: for P > 1 the part sums are stored to a
+//     global workspace; after one grid-wide barrier at the end of the (cooperative) launch each
+//     CTA adds the parts of its share of the rows in part order.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -77,7 +78,7 @@ struct SArgs {
     float *y;
     int64_t ldy;
     float *ws;
-    uint32_t *row_cnt;
+    uint32_t *gbar;  // [2]: arrival count, generation (grid barrier for P > 1)
     uint32_t *err;
     unsigned long long timeout_ns;
 };
@@ -186,6 +187,28 @@ __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     return v;
+}
+
+// All CTAs of the launch meet here (one thread per CTA; co-residency from the cooperative launch).
+__device__ void grid_barrier(const SArgs &a) {
+    volatile uint32_t *gen = a.gbar + 1;
+    const uint32_t g0 = *gen;
+    __threadfence();
+    if (atomicAdd(a.gbar, 1u) == gridDim.x - 1) {
+        atomicExch(a.gbar, 0u);
+        __threadfence();
+        atomicAdd(a.gbar + 1, 1u);
+    } else {
+        const unsigned long long t0 = globaltimer();
+        while (*gen == g0) {
+            __nanosleep(32);
+            if (globaltimer() - t0 > a.timeout_ns) {
+                atomicOr(a.err, 2u);
+                break;
+            }
+        }
+    }
+    __threadfence();
 }
 
 __device__ void signal_consumed(const SArgs &a, int64_t slot, uint32_t tag) {
@@ -353,39 +376,46 @@ __global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const 
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
-            // butterfly; lane q*B + b then owns part sum (q, b) (static indices: acc stays in registers)
-            float mine = 0.f;
+            // butterfly: every lane then holds every part sum (static indices keep acc in registers)
 #pragma unroll
             for (int q = 0; q < R; ++q)
 #pragma unroll
-                for (int b = 0; b < B; ++b) {
-                    const float t = warp_sum(acc[q][b]);
-                    if (lane == q * B + b) mine = t;
-                }
-            const int myq = lane / B, myb = lane - myq * B;
-            const bool act = lane < R * B && myq < nrows;
-            const int64_t g = src.g0 + r + myq;
+                for (int b = 0; b < B; ++b) acc[q][b] = warp_sum(acc[q][b]);
             if (a.P == 1) {
-                if (act) a.y[myb * a.ldy + g] = mine + (a.bias ? a.bias[g] : 0.f);
+#pragma unroll
+                for (int q = 0; q < R; ++q)
+#pragma unroll
+                    for (int b = 0; b < B; ++b)
+                        if (lane == q * B + b && q < nrows) {
+                            const int64_t g = src.g0 + r + q;
+                            a.y[b * a.ldy + g] = acc[q][b] + (a.bias ? a.bias[g] : 0.f);
+                        }
                 continue;
             }
-            float *wsr = a.ws + g * (int64_t)a.P * B;
-            if (act) {
-                wsr[p * B + myb] = mine;
-                __threadfence();
-            }
-            __syncwarp();
-            bool last = false;
-            if (lane < nrows) last = atomicAdd(&a.row_cnt[src.g0 + r + lane], 1u) == (uint32_t)(a.P - 1);
-            const unsigned lastmask = __ballot_sync(0xffffffffu, last);
-            if (act && ((lastmask >> myq) & 1u)) {
-                __threadfence();
-                float sum = 0.f;
-                for (int pp = 0; pp < a.P; ++pp) sum += __ldcg(&wsr[pp * B + myb]);
-                a.y[myb * a.ldy + g] = sum + (a.bias ? a.bias[g] : 0.f);
-            }
-            if (last) a.row_cnt[src.g0 + r + lane] = 0;
+            // P > 1: publish the part sum (q, b) to the workspace; summed after the grid barrier
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int b = 0; b < B; ++b)
+                    if (lane == q * B + b && q < nrows)
+                        a.ws[((src.g0 + r + q) * a.P + p) * B + b] = acc[q][b];
         }
+    }
+    if (a.P == 1) return;
+    // ---------------------------------------------------------------- P > 1: parts -> y
+    constexpr int kConsumerThreads = kConsumerWarps * 32;
+    asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
+    if (threadIdx.x == 0) grid_barrier(a);
+    asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
+    const int64_t n = a.n_res + a.n_str;
+    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
+    for (int64_t i = threadIdx.x; i < (r1 - r0) * B; i += kConsumerThreads) {
+        const int64_t g = r0 + i / B;
+        const int b = (int)(i % B);
+        const float *w = a.ws + g * a.P * B + b;
+        float sum = 0.f;
+        for (int pp = 0; pp < a.P; ++pp) sum += __ldcg(w + pp * B);
+        a.y[b * a.ldy + g] = sum + (a.bias ? a.bias[g] : 0.f);
     }
 }
 
@@ -428,7 +458,7 @@ int launch_b(const SArgs &a, cudaStream_t st) {
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = a.arrived ? 1 : 0;
+    cfg.numAttrs = (a.arrived || a.P > 1) ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B>, a);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
@@ -479,7 +509,7 @@ int64_t gemv_counters(int64_t n, int64_t K, int batch) {
         const GemvGeom g = gemv_tc_geom(K);
         return (n + g.rows_per_cta - 1) / g.rows_per_cta;
     }
-    return gemv_geom(K, batch).s > 1 ? n : 0;  // one arrival counter per row
+    return 0;  // SIMT: grid barrier words live in the context's tag memory
 }
 
 int launch_gemv_stream(const StreamLaunch &L, void *stream) {
@@ -509,10 +539,10 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.y = L.y;
     a.ldy = L.ldy;
     a.ws = L.ws;
-    a.row_cnt = L.row_cnt;
+    a.gbar = L.gbar;
     a.err = L.err;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
-    if (a.P > 1 && (!a.ws || !a.row_cnt)) return (int)cudaErrorInvalidValue;
+    if (a.P > 1 && (!a.ws || !a.gbar || !a.err)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
     switch (L.batch) {
@@ -528,7 +558,8 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
 }
 
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
-                float *y, int64_t ldy, float *ws, int *counters, void *stream) {
+                float *y, int64_t ldy, float *ws, int *counters, uint32_t *gbar, uint32_t *err,
+                void *stream) {
     if (n <= 0) return 0;
     if (gemv_use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
     StreamLaunch L{};
@@ -541,7 +572,9 @@ int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, c
     L.y = y;
     L.ldy = ldy;
     L.ws = ws;
-    L.row_cnt = (uint32_t *)counters;
+    L.gbar = gbar;
+    L.err = err;
+    L.timeout_s = 60.0;
     return launch_gemv_stream(L, stream);
 }
 

@@ -31,8 +31,11 @@ GemvGeom gemv_geom(int64_t K, int batch);
 int64_t gemv_ws_floats(int64_t n, int64_t K, int batch);
 int64_t gemv_counters(int64_t n, int64_t K, int batch);
 // Launch: y[b*ldy + j] = sum_k x[b,k] W[j,k] (+bias[j]), j < n.  Returns a CUDA error code (int).
+// ws/counters: split-K workspace (tcgen05) or part sums (SIMT, P > 1); gbar: 2 zeroed words
+// for the SIMT grid barrier; err: device error word (timeouts).
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
-                float *y, int64_t ldy, float *ws, int *counters, void *stream);
+                float *y, int64_t ldy, float *ws, int *counters, uint32_t *gbar, uint32_t *err,
+                void *stream);
 bool gemv_use_tc(int batch);
 
 // One persistent SIMT launch over the GPU lanes of a linear: resident rows [0, n_res) of W_res,
@@ -56,7 +59,7 @@ struct StreamLaunch {
     float *y;
     int64_t ldy;
     float *ws;
-    uint32_t *row_cnt;
+    uint32_t *gbar;
     uint32_t *err;
     double timeout_s;
 };

@@ -147,8 +147,8 @@ struct hg_ctx {
     int64_t next_seq = 0;
     int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
     bool tags = false;      // cfg.handshake == 1 and stream memory operations available
-    uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4]
-    uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr;
+    uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4]
+    uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr, *gbar = nullptr;
     std::vector<ChunkReq> future;
     size_t fpos = 0;
     bool fwrap = false;
@@ -444,7 +444,7 @@ hg_status gemv(hg_ctx *c, const void *x, int B, int64_t K, const void *W, int64_
     size_t i0 = 0, i1 = 0;
     cudaEvent_t e0 = nullptr;
     if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
-    HG_TRY(kerr(c, launch_gemv(x, B, K, W, n, bias, y, ldy, c->ws, c->counters, s), "gemv launch"));
+    HG_TRY(kerr(c, launch_gemv(x, B, K, W, n, bias, y, ldy, c->ws, c->counters, c->gbar, c->err, s), "gemv launch"));
     c->st.gpu_launches++;
     if (e0) {
         cudaEvent_t e1 = tev_get(c, &i1);
@@ -499,7 +499,7 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         S.y = L.y;
         S.ldy = L.ldy;
         S.ws = c->ws;
-        S.row_cnt = (uint32_t *)c->counters;
+        S.gbar = c->gbar;
         S.err = c->err;
         S.timeout_s = c->cfg.timeout_s;
         if (n > 0) {
@@ -866,12 +866,13 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
     c->tags = cfg.handshake != 0 && load_memops();
-    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 4) * 4));
-    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 4) * 4));
+    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8) * 4));
+    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8) * 4));
     c->arrived = c->tagmem;
     c->consumed = c->tagmem + c->nslots;
     c->slot_cnt = c->tagmem + 2 * c->nslots;
     c->err = c->tagmem + 3 * c->nslots;
+    c->gbar = c->err + 4;
     CREATE_CK(cudaDeviceSynchronize());
 #undef CREATE_CK
     *out = c;
@@ -1001,6 +1002,52 @@ HG_API hg_status hg_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     HG_TRY(stream_guard(c, s));
     HG_TRY(gemv(c, x, batch, K, W, n, bias, y, ldy, s));
+    HG_CK(c, cudaEventRecord(c->ev_done, s));
+    return HG_OK;
+}
+
+HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, const void *W_dev,
+                                const float *bias, float *y, void *stream) {
+    if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(validate_plan(c, *p));
+    HG_TRY(check_ptr(c, x, true, "x"));
+    HG_TRY(check_ptr(c, y, true, "y"));
+    if (p->n_res > 0) HG_TRY(check_ptr(c, W_dev, true, "W_dev"));
+    if (bias) HG_TRY(check_ptr(c, bias, true, "bias"));
+    const int B = (int)p->batch;
+    gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
+    if (gemv_use_tc(B)) return set_error(HG_EUNSUPPORTED, "replay covers the SIMT streaming GEMV (batch < %d)",
+                                         c->cfg.gemv_tc_min_batch);
+    if (p->n_chunks > c->nslots) return set_error(HG_EINVAL, "plan has more chunks than ring slots");
+    const int64_t n = p->n_res + p->n_str;
+    if (gemv_ws_floats(n, p->K, B) > c->ws_floats) return set_error(HG_EINVAL, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(stream_guard(c, s));
+    StreamLaunch S{};
+    S.x = x;
+    S.batch = B;
+    S.K = p->K;
+    S.W_res = W_dev;
+    S.n_res = p->n_res;
+    S.ring = c->ring;
+    S.slot_bytes = c->slot_bytes;
+    S.nslots = c->nslots;
+    S.seq0 = 0;
+    S.n_chunks = p->n_str > 0 ? p->n_chunks : 0;
+    S.chunk_rows = p->chunk_rows;
+    S.n_str = p->n_str;
+    S.arrived = nullptr;  // chunks taken as present: no tags, nothing signalled
+    S.bias = bias;
+    S.y = y;
+    S.ldy = p->N;
+    S.ws = c->ws;
+    S.gbar = c->gbar;
+    S.err = c->err;
+    S.timeout_s = c->cfg.timeout_s;
+    HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));
     HG_CK(c, cudaEventRecord(c->ev_done, s));
     return HG_OK;
 }
@@ -1205,7 +1252,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     for (int it = 0; it < 5; ++it) {
         HG_CK(c, cudaEventRecord(e0, c->copy));
         HG_TRY(kerr(c, launch_gemv(px, batch, K, c->ring, rows, nullptr, (float *)py, rows, c->ws,
-                                   c->counters, c->copy), "gemv probe"));
+                                   c->counters, c->gbar, c->err, c->copy), "gemv probe"));
         HG_CK(c, cudaEventRecord(e1, c->copy));
         HG_CK(c, cudaEventSynchronize(e1));
         HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));

@@ -128,6 +128,7 @@ _sig = {
     "hg_layer": (_i32, [_vp, _P(OptLayer), _vp, _i32, _P(LayerTrace), _vp]),
     "hg_stack": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _vp]),
     "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
+    "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp]),
     "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "hg_host_isa": (ctypes.c_char_p, []),
     "hg_dist_unique_id": (_i32, [_vp]),
@@ -267,6 +268,10 @@ class Context:
     def hg_stack(self, layers, h, batch, stream=None):
         arr = (OptLayer * len(layers))(*layers)
         _check(_lib.hg_stack(self._h, arr, len(layers), _ptr(h), batch, _stream(stream)))
+
+    def hg_gemv_replay(self, plan, x, W_dev, bias, y, stream=None):
+        _check(_lib.hg_gemv_replay(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(bias), _ptr(y),
+                                   _stream(stream)))
 
     def hg_gemv(self, x, batch, n, K, W, bias, y, ldy=None, stream=None):
         _check(_lib.hg_gemv(self._h, _ptr(x), batch, n, K, _ptr(W), _ptr(bias), _ptr(y),

@@ -29,7 +29,7 @@ if has launches; then
 fi
 if has full; then
   # the top kernel (streamed-chunk GEMV) inside the step
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemv -s 300 -c 4 \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemv_stream -s 8 -c 4 \
     -o $out/prof_gemv python bench.py --layers 4 --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline \
     > $out/full_bench.log 2>&1
   echo "full rc=$?"
