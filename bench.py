@@ -264,6 +264,29 @@ def main_arm(args):
     h_out = torch.empty_like(h_host, pin_memory=True)
     s = torch.cuda.Stream()
 
+    # ---- a1 refinement: the alpha benchmark (Sec. 4.4) around the Eq. (5) alpha: lane
+    # times measured in this pipeline under real interference, fitted and solved F_CPU = F_COM ----
+    abench = None
+    alpha_seed = plans["fc1"].alpha_req
+    if args.alpha is None and args.abench:
+        if world > 1:  # every rank must sample the same alpha grid (the stack all-gathers)
+            t = torch.tensor([alpha_seed], dtype=torch.float64, device="cuda")
+            dist.broadcast(t, 0)
+            alpha_seed = float(t.item())
+        res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_seed, gamma=args.abench_gamma, lam=0.02, degree=2,
+                                 reps=1, stream=s)
+        abench = res.as_dict()
+        layers = []
+        for l in range(args.layers):
+            descs = []
+            for name in NAMES:
+                N, K = SHAPES[name]
+                p = ctx.plan(rates, N // world, K, B, 0, hg.FIXED, res.alpha_bar)
+                plans[name] = p
+                descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name]))
+            layers.append(hg.opt_layer(H, F, descs))
+        h_dev.copy_(h_host)
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -372,8 +395,10 @@ def main_arm(args):
         "data": "synthetic (seeded counter-based generator; random-init OPT-30B-shaped weights)",
         "config": {"workload": "OPT-30B 48-layer decode linear stack (qkv,o,fc1,fc2 x48), batch %d" % B,
                    "batch": B, "hidden": H, "ffn": F, "layers": args.layers, "r_resident": 0.0,
-                   "alpha_mode": "fixed" if args.alpha is not None else "Eq5 exact (measured rates)",
-                   "alpha": plans["fc1"].alpha_eff, "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
+                   "alpha_mode": "fixed" if args.alpha is not None else (
+                       "Eq5 (measured rates) refined by the alpha benchmark (Sec. 4.4)" if abench else
+                       "Eq5 exact (measured rates)"),
+                   "alpha": plans["fc1"].alpha_eff, "alpha_seed_eq5": alpha_seed, "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
                    "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": threads,
                    "l2": "inputs larger than L2: %.1f GB of weights streamed/computed per step" % (shard_bytes / 1e9)},
         "gpu_launches": int(launches),
@@ -388,6 +413,11 @@ def main_arm(args):
                           "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3)},
         "rates_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rd.items()},
         "lanes": lanes,
+        "alpha_bench": None if abench is None else {
+            "alpha_bar": abench["alpha_bar"], "clamped": abench["clamped"],
+            "points": [[round(a, 4), round(tc * 1e3, 3), round(tl * 1e3, 3), round(ts * 1e3, 3)] for a, tc, tl, ts in
+                       zip(abench["alpha"], abench["t_cpu"], abench["t_com"], abench["t_step"])],
+            "points_cols": ["alpha", "t_cpu_ms", "t_link_ms", "t_step_ms"]},
         "clocks": ck,
         "wall_ms_per_step": round(wall / args.steps * 1e3, 3),
         "setup_s": round(t_setup, 1),
@@ -415,11 +445,13 @@ def main():
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--layers", type=int, default=LAYERS, help="(development only; the metric needs 48)")
     ap.add_argument("--alpha", type=float, default=None)
-    ap.add_argument("--chunk-mb", type=int, default=16)
+    ap.add_argument("--chunk-mb", type=int, default=32)
     ap.add_argument("--ring-mb", type=int, default=4096)
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--no-breakdown", dest="breakdown", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-abench", dest="abench", action="store_false", help="use Eq. (5) alpha unrefined")
+    ap.add_argument("--abench-gamma", type=float, default=0.06)
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -84,6 +84,7 @@ __global__ void residual_ln_kernel(const __nv_bfloat16 *__restrict__ h, const fl
     layernorm_row([&](int64_t i) { return bf(row[i]); }, H, g, b, a2 + off, red);
 }
 
+// ycpu is normally the CPU lane's mapped pinned buffer: the reads cross PCIe (zero-copy).
 __global__ void join_kernel(float *__restrict__ y, int64_t ldy, int64_t col0, int64_t ncols,
                             int batch, const float *__restrict__ ycpu, const float *__restrict__ bias) {
     const int64_t total = (int64_t)batch * ncols;

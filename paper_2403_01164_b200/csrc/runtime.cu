@@ -154,9 +154,15 @@ struct hg_ctx {
     bool fwrap = false;
 
     uint16_t *x_host = nullptr;   // pinned [max_batch, max_k]
-    float *ycpu_host = nullptr;   // pinned [max_batch, max_n]
-    float *ycpu_dev = nullptr;    // device [max_batch, max_n]
-    cudaEvent_t ev_x = nullptr, ev_ycpu = nullptr, ev_done = nullptr;
+    // CPU-lane results: two mapped pinned buffers [max_batch, max_n] used alternately; the join
+    // kernel reads them in place (zero-copy).  A cudaMemcpyAsync H2D here would queue behind every
+    // chunk copy already in the copy engine's queue (measured: 2 GiB queued -> 39 ms), draining the
+    // link's run-ahead at every linear boundary.
+    float *ycpu_host[2] = {nullptr, nullptr};
+    float *ycpu_map[2] = {nullptr, nullptr};  // device addresses of the same buffers
+    float *ycpu_dev = nullptr;    // device [max_batch, max_n] (HG_JOIN_MEMCPY=1 A/B path only)
+    int ybuf = 0;
+    cudaEvent_t ev_x = nullptr, ev_ycpu[2] = {nullptr, nullptr}, ev_done = nullptr;
     cudaStream_t last_stream = nullptr;
     bool have_last = false;
 
@@ -293,9 +299,17 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
     const int64_t seq = c->next_seq;
     const int slot = (int)(seq % c->nslots);
     if (c->tags) {
-        // the slot's previous occupant (seq - nslots) must have been drained by its GEMV
-        if (seq >= c->nslots)
-            HG_TRY(memop(c, g_wait_value, c->copy, c->consumed + slot, (uint32_t)(seq - c->nslots + 1), kWaitGeq));
+        // The slot's previous occupant (seq - nslots) must have been drained by its GEMV.  ev_free
+        // follows that GEMV (or the drop): when the host already sees it complete, the device-side
+        // wait (which costs the copy engine a few microseconds) is skipped.
+        if (seq >= c->nslots) {
+            const cudaError_t q = cudaEventQuery(c->ev_free[slot]);
+            if (q != cudaSuccess) {
+                if (q != cudaErrorNotReady) HG_CK(c, q);
+                HG_TRY(memop(c, g_wait_value, c->copy, c->consumed + slot, (uint32_t)(seq - c->nslots + 1),
+                             kWaitGeq));
+            }
+        }
     } else if (c->slot_used[slot]) {
         HG_CK(c, cudaStreamWaitEvent(c->copy, c->ev_free[slot], 0));
     }
@@ -326,7 +340,7 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
 hg_status drop_front(hg_ctx *c) {
     const Inflight &f = c->inflight.front();
     if (c->tags) HG_TRY(memop(c, g_write_value, c->copy, c->consumed + f.slot, (uint32_t)(f.seq + 1), kWriteDefault));
-    else HG_CK(c, cudaEventRecord(c->ev_free[f.slot], c->copy));
+    HG_CK(c, cudaEventRecord(c->ev_free[f.slot], c->copy));
     c->inflight.pop_front();
     return HG_OK;
 }
@@ -410,7 +424,7 @@ hg_status release(hg_ctx *c, int slot, cudaStream_t stream) {
     if (c->tags)
         HG_TRY(memop(c, g_write_value, stream, c->consumed + slot, (uint32_t)(c->inflight.front().seq + 1),
                      kWriteDefault));
-    else HG_CK(c, cudaEventRecord(c->ev_free[slot], stream));
+    HG_CK(c, cudaEventRecord(c->ev_free[slot], stream));
     c->inflight.pop_front();
     return HG_OK;
 }
@@ -508,6 +522,8 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
             if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
             HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv stream launch"));
             c->st.gpu_launches++;
+            for (int64_t i = 0; i < S.n_chunks; ++i)  // the slots are free once this GEMV is done
+                HG_CK(c, cudaEventRecord(c->ev_free[(seq0 + i) % c->nslots], s));
             if (e0) {
                 cudaEvent_t e1 = tev_get(c, &i1);
                 if (e1) {
@@ -564,7 +580,9 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         hg_status gst = HG_OK;
         if (!async_post) HG_TRY(enqueue_gpu_lanes(c, L, s));
         HG_TRY(wait_event(c, c->ev_x, &c->st.x_wait_s));
-        HG_TRY(wait_event(c, c->ev_ycpu, nullptr));  // bounce buffer free (previous H2D done)
+        const int yb = c->ybuf;
+        c->ybuf ^= 1;
+        HG_TRY(wait_event(c, c->ev_ycpu[yb], nullptr));  // this buffer's previous join has read it
         const auto t0 = clk::now();
         HostJob job;
         job.fn = c->host_fn;
@@ -574,7 +592,7 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         job.n = p.n_cpu;
         job.W = (const uint16_t *)(L.W_host + 2 * K * p.n_str);
         job.bias = nullptr;  // bias joins on the device
-        job.y = c->ycpu_host;
+        job.y = c->ycpu_host[yb];
         job.ldy = p.n_cpu;
         job.block = 16;
         job.next.store(0);
@@ -588,11 +606,16 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         if (gst != HG_OK) return gst;
         c->st.cpu_busy_s += secs(t0, clk::now());
         c->st.bytes_cpu += 2 * K * p.n_cpu;
-        HG_CK(c, cudaMemcpyAsync(c->ycpu_dev, c->ycpu_host, (size_t)B * p.n_cpu * 4,
-                                 cudaMemcpyHostToDevice, s));
-        HG_CK(c, cudaEventRecord(c->ev_ycpu, s));
+        static const bool join_memcpy = getenv("HG_JOIN_MEMCPY") && atoi(getenv("HG_JOIN_MEMCPY")) != 0;
+        const float *ysrc = c->ycpu_map[yb];
+        if (join_memcpy) {  // A/B reference: H2D copy engine (queues behind the chunk stream)
+            HG_CK(c, cudaMemcpyAsync(c->ycpu_dev, c->ycpu_host[yb], (size_t)B * p.n_cpu * 4,
+                                     cudaMemcpyHostToDevice, s));
+            ysrc = c->ycpu_dev;
+        }
         const int64_t col0 = p.n_res + p.n_str;
-        HG_TRY(kerr(c, launch_join(L.y, L.ldy, col0, p.n_cpu, B, c->ycpu_dev, L.bias, s), "join"));
+        HG_TRY(kerr(c, launch_join(L.y, L.ldy, col0, p.n_cpu, B, ysrc, L.bias, s), "join"));
+        HG_CK(c, cudaEventRecord(c->ev_ycpu[yb], s));
         c->st.gpu_launches++;
     }
     c->st.n_linears++;
@@ -844,10 +867,14 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
         CREATE_CK(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming));
     }
     CREATE_CK(cudaHostAlloc((void **)&c->x_host, (size_t)HG_MAX_BATCH * cfg.max_k * 2, cudaHostAllocDefault));
-    CREATE_CK(cudaHostAlloc((void **)&c->ycpu_host, (size_t)HG_MAX_BATCH * cfg.max_n * 4, cudaHostAllocDefault));
+    for (int i = 0; i < 2; ++i) {
+        CREATE_CK(cudaHostAlloc((void **)&c->ycpu_host[i], (size_t)HG_MAX_BATCH * cfg.max_n * 4,
+                                cudaHostAllocMapped));
+        CREATE_CK(cudaHostGetDevicePointer((void **)&c->ycpu_map[i], c->ycpu_host[i], 0));
+        CREATE_CK(cudaEventCreateWithFlags(&c->ev_ycpu[i], cudaEventDisableTiming));
+    }
     CREATE_CK(cudaMalloc((void **)&c->ycpu_dev, (size_t)HG_MAX_BATCH * cfg.max_n * 4));
     CREATE_CK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
-    CREATE_CK(cudaEventCreateWithFlags(&c->ev_ycpu, cudaEventDisableTiming));
     CREATE_CK(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
     CREATE_CK(cudaEventCreate(&c->ev_call0));
     CREATE_CK(cudaEventCreate(&c->ev_call1));
@@ -888,7 +915,7 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
         for (auto e : c->ev_arrived) if (e) cudaEventDestroy(e);
         for (auto e : c->ev_free) if (e) cudaEventDestroy(e);
         for (auto e : c->tev) cudaEventDestroy(e);
-        for (cudaEvent_t e : {c->ev_x, c->ev_ycpu, c->ev_done, c->ev_call0, c->ev_call1})
+        for (cudaEvent_t e : {c->ev_x, c->ev_ycpu[0], c->ev_ycpu[1], c->ev_done, c->ev_call0, c->ev_call1})
             if (e) cudaEventDestroy(e);
         if (c->copy) cudaStreamDestroy(c->copy);
         for (void *p : {(void *)c->ring, (void *)c->ycpu_dev, (void *)c->ws, (void *)c->counters,
@@ -896,7 +923,8 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
                         (void *)c->gbuf, (void *)c->tagmem})
             if (p) cudaFree(p);
         if (c->x_host) cudaFreeHost(c->x_host);
-        if (c->ycpu_host) cudaFreeHost(c->ycpu_host);
+        for (float *p : c->ycpu_host)
+            if (p) cudaFreeHost(p);
     }
     if (c->pool) pool_destroy(c->pool);
     delete c;
