@@ -220,9 +220,9 @@ def main_arm(args):
 
     # ---- weights: this rank's row shard of every linear, pinned host (r = 0) ----
     t_setup = time.perf_counter()
-    host, biases = [], []
+    host, biases, biases_h = [], [], []
     for l in range(args.layers):
-        hl, bl = {}, {}
+        hl, bl, bh = {}, {}, {}
         for name in NAMES:
             N, K = SHAPES[name]
             r0, r1 = rank * N // world, (rank + 1) * N // world
@@ -232,9 +232,11 @@ def main_arm(args):
             b = gen.bf16_bits_to_f32(gen.uniform_bf16(SEED, gen.tensor_id(l, name, "bias"), r1 - r0,
                                                       gen.BIAS_SCALE, offset=r0))
             hl[name] = Wt
-            bl[name] = torch.from_numpy(b).cuda()
+            bh[name] = torch.from_numpy(b)  # host copy: the CPU lane adds its rows' bias (mirrored glue)
+            bl[name] = bh[name].cuda()
         host.append(hl)
         biases.append(bl)
+        biases_h.append(bh)
     t_setup = time.perf_counter() - t_setup
 
     # ---- a1: measured rates -> alpha (Eq. 5), per-linear plans ----
@@ -254,7 +256,7 @@ def main_arm(args):
             N, K = SHAPES[name]
             p = ctx.plan(rates, N // world, K, B, 0, mode, af)
             plans[name] = p
-            descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name]))
+            descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name], biases_h[l][name]))
         layers.append(hg.opt_layer(H, F, descs))
 
     h0 = gen.uniform_bf16(SEED + 1, 999, B * H, 1.0).reshape(B, H)
@@ -283,7 +285,7 @@ def main_arm(args):
                 N, K = SHAPES[name]
                 p = ctx.plan(rates, N // world, K, B, 0, hg.FIXED, res.alpha_bar)
                 plans[name] = p
-                descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name]))
+                descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name], biases_h[l][name]))
             layers.append(hg.opt_layer(H, F, descs))
         h_dev.copy_(h_host)
 

@@ -64,7 +64,7 @@ extern "C" {
 #endif
 
 #define HG_MAX_BATCH 8
-#define HG_ABI_VERSION 1
+#define HG_ABI_VERSION 2
 
 typedef enum {
     HG_OK = 0,
@@ -138,6 +138,13 @@ typedef struct {
                             on the slot's consumed tag (cuStreamWaitValue32), one persistent GEMV
                             launch per linear consumes chunks as they land; 0 = host events, one
                             GEMV launch per chunk (A/B reference)                                 */
+    int32_t mirror_glue; /* 1 (default): in hg_layer / hg_stack on one GPU the CPU lane recomputes
+                            the glue between linears (LN, V slice, residual, ReLU) bit-exactly from
+                            the full linear output instead of waiting for the GPU's result to cross
+                            the saturated host link; needs host mirrors of non-NULL biases (for the
+                            CPU rows) and LN parameters, else the call uses the GPU-only glue      */
+    int32_t verify_mirror; /* 1: after every mirrored glue step compare the host activation with
+                            the device one (synchronising; tests) -> hg_stats.mirror_mismatch     */
 } hg_config;
 
 /* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last
@@ -151,12 +158,15 @@ typedef struct {
     double link_busy_s;     /* H2D chunk copy time (collect_stats=1)                    */
     double gpu_busy_s;      /* GEMV kernel time, resident + streamed (collect_stats=1)  */
     double x_wait_s;        /* host time waiting for activations to reach the host     */
+    double glue_s;          /* host time in the mirrored glue (critical path, per call)   */
     int64_t bytes_res;      /* W bytes read by resident GEMVs                           */
     int64_t bytes_str;      /* W bytes streamed over the link                           */
     int64_t bytes_cpu;      /* W bytes read by the CPU lane                             */
     int64_t n_chunks;       /* streamed chunks consumed                                 */
     int64_t n_linears;
     int64_t gpu_launches;   /* kernels this library launched                            */
+    int64_t mirror_linears; /* linears whose input the CPU lane computed itself          */
+    int64_t mirror_mismatch; /* verify_mirror: activation elements host != device         */
 } hg_stats_t;
 
 typedef struct hg_ctx hg_ctx;
@@ -172,6 +182,7 @@ typedef struct {
     const void *W_host;
     const float *bias;
     hg_plan_t plan;
+    const float *bias_host; /* host copy of bias [N_local] fp32 or NULL (mirror_glue, reading R24) */
 } hg_linear_desc;
 
 /* One OPT pre-LN decoder layer (reading R22).  lin[0..3] =
@@ -182,6 +193,7 @@ typedef struct {
     int64_t hidden, ffn;
     hg_linear_desc lin[4];
     const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
+    const float *ln1_g_host, *ln1_b_host, *ln2_g_host, *ln2_b_host; /* host copies (mirror_glue) */
 } hg_opt_layer;
 
 /* Optional per-step device copies of a layer's intermediates (teacher-forced

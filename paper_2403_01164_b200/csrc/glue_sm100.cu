@@ -24,7 +24,7 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162f
 // Deterministic block sum (fixed tree) for 256 threads.
 __device__ float block_sum(float v, float *red) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    for (int o = 16; o > 0; o >>= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __syncthreads();
     if (lane == 0) red[warp] = v;
@@ -33,31 +33,33 @@ __device__ float block_sum(float v, float *red) {
     if (threadIdx.x < 32) {
         t = threadIdx.x < kThreads / 32 ? red[threadIdx.x] : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        for (int o = 16; o > 0; o >>= 1) t = __fadd_rn(t, __shfl_xor_sync(0xffffffffu, t, o));
         if (threadIdx.x == 0) red[0] = t;
     }
     __syncthreads();
     return red[0];
 }
 
-// LayerNorm of one row held in `row` (fp32 values read through `get`).
+// LayerNorm of one row held in `row` (fp32 values read through `get`).  Every operation is an
+// explicit IEEE intrinsic (no contraction), and block_sum's tree is fixed, so host_glue.cpp can
+// reproduce the result bit for bit (the CPU lane's mirrored glue).
 template <typename Get>
 __device__ void layernorm_row(Get get, int64_t H, const float *g, const float *b,
                               __nv_bfloat16 *out, float *red) {
     float s = 0.f;
-    for (int64_t i = threadIdx.x; i < H; i += kThreads) s += get(i);
-    const float mean = block_sum(s, red) / (float)H;
+    for (int64_t i = threadIdx.x; i < H; i += kThreads) s = __fadd_rn(s, get(i));
+    const float mean = __fdiv_rn(block_sum(s, red), (float)H);
     float q = 0.f;
     for (int64_t i = threadIdx.x; i < H; i += kThreads) {
-        const float d = get(i) - mean;
-        q += d * d;
+        const float d = __fsub_rn(get(i), mean);
+        q = __fmaf_rn(d, d, q);
     }
-    const float var = block_sum(q, red) / (float)H;
-    const float rstd = 1.0f / sqrtf(var + kLnEps);
+    const float var = __fdiv_rn(block_sum(q, red), (float)H);
+    const float rstd = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, kLnEps)));
     for (int64_t i = threadIdx.x; i < H; i += kThreads) {
-        float v = (get(i) - mean) * rstd;
-        if (g) v *= g[i];
-        if (b) v += b[i];
+        float v = __fmul_rn(__fsub_rn(get(i), mean), rstd);
+        if (g) v = __fmul_rn(v, g[i]);
+        if (b) v = __fadd_rn(v, b[i]);
         out[i] = __float2bfloat16_rn(v);
     }
 }
@@ -78,7 +80,7 @@ __global__ void residual_ln_kernel(const __nv_bfloat16 *__restrict__ h, const fl
     __shared__ float red[32];
     const int64_t off = blockIdx.x * H;
     for (int64_t i = threadIdx.x; i < H; i += kThreads)
-        h1[off + i] = __float2bfloat16_rn(bf(h[off + i]) + y[off + i]);
+        h1[off + i] = __float2bfloat16_rn(__fadd_rn(bf(h[off + i]), y[off + i]));
     __syncthreads();
     const __nv_bfloat16 *row = h1 + off;
     layernorm_row([&](int64_t i) { return bf(row[i]); }, H, g, b, a2 + off, red);
@@ -86,12 +88,14 @@ __global__ void residual_ln_kernel(const __nv_bfloat16 *__restrict__ h, const fl
 
 // ycpu is normally the CPU lane's mapped pinned buffer: the reads cross PCIe (zero-copy).
 __global__ void join_kernel(float *__restrict__ y, int64_t ldy, int64_t col0, int64_t ncols,
-                            int batch, const float *__restrict__ ycpu, const float *__restrict__ bias) {
+                            int batch, const float *__restrict__ ycpu, int64_t ldsrc,
+                            const float *__restrict__ bias) {
     const int64_t total = (int64_t)batch * ncols;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / ncols, j = i - b * ncols;
-        y[b * ldy + col0 + j] = ycpu[i] + (bias ? bias[col0 + j] : 0.f);
+        const float v = ycpu[b * ldsrc + j];
+        y[b * ldy + col0 + j] = bias ? __fadd_rn(v, bias[col0 + j]) : v;
     }
 }
 
@@ -109,14 +113,14 @@ __global__ void relu_bf16_kernel(const float *__restrict__ y, int64_t total,
                                  __nv_bfloat16 *__restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = __float2bfloat16_rn(fmaxf(y[i], 0.f));
+        out[i] = __float2bfloat16_rn(y[i] > 0.f ? y[i] : 0.f);  // +0 for -0 and NaN (host mirror)
 }
 
 __global__ void residual_kernel(const __nv_bfloat16 *__restrict__ h1, const float *__restrict__ y,
                                 int64_t total, __nv_bfloat16 *__restrict__ out) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = __float2bfloat16_rn(bf(h1[i]) + y[i]);
+        out[i] = __float2bfloat16_rn(__fadd_rn(bf(h1[i]), y[i]));
 }
 
 // y[b, p*n_local + j] = gbuf[p][b][j]
@@ -141,10 +145,10 @@ inline unsigned grid_for(int64_t total) {
 }  // namespace
 
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,
-                const float *bias, void *stream) {
+                int64_t ldsrc, const float *bias, void *stream) {
     if (ncols <= 0) return 0;
     join_kernel<<<grid_for(batch * ncols), kThreads, 0, (cudaStream_t)stream>>>(y, ldy, col0, ncols,
-                                                                               batch, ycpu, bias);
+                                                                               batch, ycpu, ldsrc, bias);
     return (int)cudaGetLastError();
 }
 

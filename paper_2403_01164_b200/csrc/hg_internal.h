@@ -67,7 +67,7 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream);
 
 // ---------------------------------------------------------------- glue_sm100.cu
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,
-                const float *bias, void *stream);
+                int64_t ldsrc, const float *bias, void *stream);
 int launch_layernorm(const void *h, int64_t H, int batch, const float *g, const float *b, void *out,
                      void *stream);
 int launch_slice_to_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch,
@@ -93,6 +93,15 @@ void host_rows_scalar(const uint16_t *x, int batch, int64_t K, const uint16_t *W
 host_rows_fn host_rows_select(const char **name);
 // Host read-bandwidth kernel (probe): returns a checksum so the loads are not elided.
 uint64_t host_read_avx512(const void *p, int64_t bytes);
+
+// ---------------------------------------------------------------- host_glue.cpp
+// Bit-exact host mirrors of the glue_sm100.cu kernels (bf16 = uint16 bit patterns).
+void hglue_layernorm(const uint16_t *h, int64_t H, int batch, const float *g, const float *b, uint16_t *out);
+void hglue_residual_ln(const uint16_t *h, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *h1,
+                       const float *g, const float *b, uint16_t *a2);
+void hglue_residual(const uint16_t *h1, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *out);
+void hglue_slice_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, uint16_t *out);
+void hglue_relu_bf16(const float *y, int64_t ldy, int64_t n, int batch, uint16_t *out);
 
 // ---------------------------------------------------------------- threadpool.cpp
 class ThreadPool;

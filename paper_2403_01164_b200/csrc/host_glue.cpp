@@ -1,0 +1,131 @@
+// host_glue.cpp -- the CPU lane's mirror of the GPU glue between linears.
+//
+// HeteGen keeps the non-linear modules on the GPU and sends the CPU's outputs back "for
+// final processing".  On the B200 box the host link is saturated by the streamed weight
+// slice, and every small transfer at a linear boundary queues behind it (measured: a 14 KB D2H
+// takes 44 us instead of 10, a zero-copy read of the CPU rows 78 us).  Waiting for the GPU's
+// glue output before starting the next linear's CPU rows would put both on the CPU lane's
+// critical path 192 times per token.  So the CPU lane recomputes the glue itself from the full
+// linear output (its own rows + the GPU rows, copied D2H while it was computing) -- the GPU still
+// computes the same glue for its own lanes and for the layer output.
+//
+// Each function reproduces the GPU kernel in glue_sm100.cu operation for operation (IEEE fp32,
+// no contraction: this file is built with -ffp-contract=off; LayerNorm's block_sum tree of 256
+// threads and 8 warps is emulated exactly), so both lanes see bit-identical activations.
+// hg_config.verify_mirror checks that at run time.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "hg_internal.h"
+
+namespace hg {
+namespace {
+
+constexpr int kThreads = 256;  // glue_sm100.cu block size
+constexpr float kLnEps = 1e-5f;
+
+inline float bf2f(uint16_t v) {
+    uint32_t u = (uint32_t)v << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+
+// __float2bfloat16_rn: round to nearest even; NaN -> canonical 0x7FFF
+inline uint16_t f2bf(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fff;
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+// glue_sm100.cu block_sum: per-thread partials -> xor butterfly in each warp (all lanes equal) ->
+// warp 0 sums the 8 warp totals (lanes >= 8 contribute 0) with the same butterfly.
+float block_sum(const float (&part)[kThreads]) {
+    float red[kThreads / 32];
+    for (int w = 0; w < kThreads / 32; ++w) {
+        float v[32];
+        for (int l = 0; l < 32; ++l) v[l] = part[w * 32 + l];
+        for (int o = 16; o > 0; o >>= 1) {
+            float n[32];
+            for (int l = 0; l < 32; ++l) n[l] = v[l] + v[l ^ o];
+            std::memcpy(v, n, sizeof v);
+        }
+        red[w] = v[0];
+    }
+    float t[32];
+    for (int l = 0; l < 32; ++l) t[l] = l < kThreads / 32 ? red[l] : 0.f;
+    for (int o = 16; o > 0; o >>= 1) {
+        float n[32];
+        for (int l = 0; l < 32; ++l) n[l] = t[l] + t[l ^ o];
+        std::memcpy(t, n, sizeof t);
+    }
+    return t[0];
+}
+
+template <typename Get>
+void layernorm_row(Get get, int64_t H, const float *g, const float *b, uint16_t *out) {
+    float part[kThreads];
+    for (int t = 0; t < kThreads; ++t) {
+        float s = 0.f;
+        for (int64_t i = t; i < H; i += kThreads) s = s + get(i);
+        part[t] = s;
+    }
+    const float mean = block_sum(part) / (float)H;
+    for (int t = 0; t < kThreads; ++t) {
+        float q = 0.f;
+        for (int64_t i = t; i < H; i += kThreads) {
+            const float d = get(i) - mean;
+            q = std::fma(d, d, q);
+        }
+        part[t] = q;
+    }
+    const float var = block_sum(part) / (float)H;
+    const float rstd = 1.0f / std::sqrt(var + kLnEps);
+    for (int64_t i = 0; i < H; ++i) {
+        float v = (get(i) - mean) * rstd;
+        if (g) v = v * g[i];
+        if (b) v = v + b[i];
+        out[i] = f2bf(v);
+    }
+}
+
+}  // namespace
+
+void hglue_layernorm(const uint16_t *h, int64_t H, int batch, const float *g, const float *b, uint16_t *out) {
+    for (int r = 0; r < batch; ++r) {
+        const uint16_t *row = h + r * H;
+        layernorm_row([&](int64_t i) { return bf2f(row[i]); }, H, g, b, out + r * H);
+    }
+}
+
+void hglue_residual_ln(const uint16_t *h, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *h1,
+                       const float *g, const float *b, uint16_t *a2) {
+    for (int r = 0; r < batch; ++r) {
+        for (int64_t i = 0; i < H; ++i) h1[r * H + i] = f2bf(bf2f(h[r * H + i]) + y[r * ldy + i]);
+        const uint16_t *row = h1 + r * H;
+        layernorm_row([&](int64_t i) { return bf2f(row[i]); }, H, g, b, a2 + r * H);
+    }
+}
+
+void hglue_residual(const uint16_t *h1, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *out) {
+    for (int r = 0; r < batch; ++r)
+        for (int64_t i = 0; i < H; ++i) out[r * H + i] = f2bf(bf2f(h1[r * H + i]) + y[r * ldy + i]);
+}
+
+void hglue_slice_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, uint16_t *out) {
+    for (int r = 0; r < batch; ++r)
+        for (int64_t j = 0; j < ncols; ++j) out[r * ncols + j] = f2bf(y[r * ldy + col0 + j]);
+}
+
+void hglue_relu_bf16(const float *y, int64_t ldy, int64_t n, int batch, uint16_t *out) {
+    for (int r = 0; r < batch; ++r)
+        for (int64_t j = 0; j < n; ++j) {
+            const float v = y[r * ldy + j];
+            out[r * n + j] = f2bf(v > 0.f ? v : 0.f);
+        }
+}
+
+}  // namespace hg

@@ -163,6 +163,8 @@ struct hg_ctx {
     float *ycpu_dev = nullptr;    // device [max_batch, max_n] (HG_JOIN_MEMCPY=1 A/B path only)
     int ybuf = 0;
     cudaEvent_t ev_x = nullptr, ev_ycpu[2] = {nullptr, nullptr}, ev_done = nullptr;
+    cudaEvent_t ev_yg[2] = {nullptr, nullptr};  // mirrored glue: GPU rows of y reached the host
+    std::vector<uint16_t> hh, hh1, xchk;          // mirrored glue: host residual stream, check buffer
     cudaStream_t last_stream = nullptr;
     bool have_last = false;
 
@@ -614,7 +616,7 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
             ysrc = c->ycpu_dev;
         }
         const int64_t col0 = p.n_res + p.n_str;
-        HG_TRY(kerr(c, launch_join(L.y, L.ldy, col0, p.n_cpu, B, ysrc, L.bias, s), "join"));
+        HG_TRY(kerr(c, launch_join(L.y, L.ldy, col0, p.n_cpu, B, ysrc, p.n_cpu, L.bias, s), "join"));
         HG_CK(c, cudaEventRecord(c->ev_ycpu[yb], s));
         c->st.gpu_launches++;
     }
@@ -779,6 +781,135 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
     return HG_OK;
 }
 
+// ---------------------------------------------------------------- mirrored glue (reading R24)
+bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n, hg_layer_trace *tr) {
+    if (!c->cfg.mirror_glue || tr || dist_nranks(c->dist) != 1) return false;
+    for (int l = 0; l < n; ++l) {
+        const hg_opt_layer &L = layers[l];
+        if ((L.ln1_g && !L.ln1_g_host) || (L.ln1_b && !L.ln1_b_host) || (L.ln2_g && !L.ln2_g_host) ||
+            (L.ln2_b && !L.ln2_b_host))
+            return false;
+        for (int i = 0; i < 4; ++i)
+            if (L.lin[i].bias && !L.lin[i].bias_host && L.lin[i].plan.n_cpu > 0) return false;
+    }
+    return true;
+}
+
+// Compare the host activation with the device one (verify_mirror; synchronises).
+hg_status verify_act(hg_ctx *c, const uint16_t *xh, const void *xd, int64_t n, cudaStream_t s) {
+    c->xchk.resize((size_t)n);
+    HG_CK(c, cudaMemcpyAsync(c->xchk.data(), xd, (size_t)n * 2, cudaMemcpyDeviceToHost, s));
+    HG_CK(c, cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < n; ++i) c->st.mirror_mismatch += c->xchk[i] != xh[i];
+    return HG_OK;
+}
+
+// One decode step over n layers (P = 1) with the glue mirrored on the host: per linear the CPU lane
+// computes its input itself from the previous linear's full output -- its own rows plus the GPU
+// rows, copied D2H while it was busy -- so neither the D2H of x nor the zero-copy join sits on its
+// critical path.  The GPU runs exactly the kernel sequence of run_layer.
+hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *h, int B, cudaStream_t s) {
+    const int64_t H = layers[0].hidden;
+    int64_t maxF = 0;
+    for (int l = 0; l < nl; ++l) maxF = std::max(maxF, layers[l].ffn);
+    HG_TRY(ensure(c, &c->act, &c->act_elems, (int64_t)B * std::max(maxF, H) * 2));
+    HG_TRY(ensure(c, (void **)&c->yscr, &c->yscr_elems, (int64_t)B * std::max(maxF, 3 * H) * 4));
+    HG_TRY(ensure(c, &c->h1, &c->h1_elems, (int64_t)B * H * 2));
+    c->hh.resize((size_t)B * H);
+    c->hh1.resize((size_t)B * H);
+    HG_CK(c, cudaMemcpyAsync(c->hh.data(), h, (size_t)B * H * 2, cudaMemcpyDeviceToHost, s));
+    HG_CK(c, cudaStreamSynchronize(s));
+    uint16_t *xh = c->x_host;
+    const float *yprev = nullptr;  // host view of the previous linear's full output [B, N]
+    int prev_buf = -1;
+    bool prev_gpu = false;
+    for (int l = 0; l < nl; ++l) {
+        const hg_opt_layer &L = layers[l];
+        const int64_t F = L.ffn;
+        for (int i = 0; i < 4; ++i) {
+            const hg_linear_desc &d = L.lin[i];
+            const hg_plan_t &p = d.plan;
+            const int64_t N = p.N, K = p.K, n_gpu = p.n_res + p.n_str;
+            HG_TRY(pump(c));
+            // ---- the previous linear's GPU rows on the host (normally long done)
+            if (prev_gpu) HG_TRY(wait_event(c, c->ev_yg[prev_buf], &c->st.x_wait_s));
+            // ---- glue -> this linear's input, on the GPU (run_layer's kernels) and on the host
+            const auto tg = clk::now();
+            if (i == 0) {
+                if (l > 0) {  // h = h1 + y_fc2 of the previous layer
+                    hglue_residual(c->hh1.data(), yprev, H, H, B, c->hh.data());
+                }
+                HG_TRY(kerr(c, launch_layernorm(h, H, B, L.ln1_g, L.ln1_b, c->act, s), "ln1"));
+                hglue_layernorm(c->hh.data(), H, B, L.ln1_g_host, L.ln1_b_host, xh);
+            } else if (i == 1) {
+                HG_TRY(kerr(c, launch_slice_to_bf16(c->yscr, 3 * H, 2 * H, H, B, c->act, s), "v"));
+                hglue_slice_bf16(yprev, 3 * H, 2 * H, H, B, xh);
+            } else if (i == 2) {
+                HG_TRY(kerr(c, launch_residual_ln(h, c->yscr, H, B, c->h1, L.ln2_g, L.ln2_b, c->act, s), "res+ln2"));
+                hglue_residual_ln(c->hh.data(), yprev, H, H, B, c->hh1.data(), L.ln2_g_host, L.ln2_b_host, xh);
+            } else {
+                HG_TRY(kerr(c, launch_relu_bf16(c->yscr, F, B, c->act, s), "relu"));
+                hglue_relu_bf16(yprev, F, F, B, xh);
+            }
+            c->st.gpu_launches++;
+            c->st.glue_s += secs(tg, clk::now());
+            c->st.mirror_linears++;
+            if (c->cfg.verify_mirror) HG_TRY(verify_act(c, xh, c->act, (int64_t)B * K, s));
+            // ---- CPU rows: post to the pool; they land in the host buffer of this linear's y
+            const int yb = c->ybuf;
+            c->ybuf ^= 1;
+            HG_TRY(wait_event(c, c->ev_ycpu[yb], nullptr));  // the join that read this buffer is done
+            float *yfull = c->ycpu_host[yb];
+            HostJob job;
+            const auto t0 = clk::now();
+            if (p.n_cpu > 0) {
+                job.fn = c->host_fn;
+                job.x = xh;
+                job.batch = B;
+                job.K = K;
+                job.n = p.n_cpu;
+                job.W = (const uint16_t *)((const uint8_t *)d.W_host + 2 * K * p.n_str);
+                job.bias = d.bias_host ? d.bias_host + n_gpu : nullptr;
+                job.y = yfull + n_gpu;
+                job.ldy = N;
+                job.block = 16;
+                job.next.store(0);
+                pool_post(c->pool, host_job_run, &job);
+            }
+            // ---- GPU rows, then their copy to the host (for the next glue step)
+            Lin lin{p, c->act, d.W_dev, (const uint8_t *)d.W_host, d.bias, c->yscr, N};
+            hg_status gst = enqueue_gpu_lanes(c, lin, s);
+            if (gst == HG_OK && n_gpu > 0) {
+                cudaError_t e = cudaMemcpy2DAsync(yfull, (size_t)N * 4, c->yscr, (size_t)N * 4, (size_t)n_gpu * 4,
+                                                  (size_t)B, cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) e = cudaEventRecord(c->ev_yg[yb], s);
+                if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H");
+            }
+            if (p.n_cpu > 0) {
+                pool_join(c->pool);  // always: workers reference `job`
+                c->st.cpu_busy_s += secs(t0, clk::now());
+                c->st.bytes_cpu += 2 * K * p.n_cpu;
+            }
+            if (gst != HG_OK) return gst;
+            // ---- join: the CPU rows (bias already added on the host) into y on the device
+            if (p.n_cpu > 0) {
+                HG_TRY(kerr(c, launch_join(c->yscr, N, n_gpu, p.n_cpu, B, c->ycpu_map[yb] + n_gpu, N,
+                                           d.bias_host ? nullptr : d.bias, s), "join"));
+                c->st.gpu_launches++;
+            }
+            HG_CK(c, cudaEventRecord(c->ev_ycpu[yb], s));
+            c->st.n_linears++;
+            yprev = yfull;
+            prev_buf = yb;
+            prev_gpu = n_gpu > 0;
+        }
+        // h = h1 + y_fc2 on the GPU (the host does the same at the next layer's first glue step)
+        HG_TRY(kerr(c, launch_residual(c->h1, c->yscr, H, B, h, s), "residual"));
+        c->st.gpu_launches++;
+    }
+    return HG_OK;
+}
+
 }  // namespace
 
 // =====================================================================================
@@ -806,6 +937,9 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     if (const char *v = getenv("HG_GEMV_TC_MIN_BATCH")) cfg->gemv_tc_min_batch = atoi(v);
     cfg->handshake = 1;
     if (const char *v = getenv("HG_HANDSHAKE")) cfg->handshake = atoi(v);
+    cfg->mirror_glue = 1;
+    if (const char *v = getenv("HG_MIRROR_GLUE")) cfg->mirror_glue = atoi(v);
+    cfg->verify_mirror = 0;
     return HG_OK;
 }
 
@@ -872,6 +1006,7 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
                                 cudaHostAllocMapped));
         CREATE_CK(cudaHostGetDevicePointer((void **)&c->ycpu_map[i], c->ycpu_host[i], 0));
         CREATE_CK(cudaEventCreateWithFlags(&c->ev_ycpu[i], cudaEventDisableTiming));
+        CREATE_CK(cudaEventCreateWithFlags(&c->ev_yg[i], cudaEventDisableTiming));
     }
     CREATE_CK(cudaMalloc((void **)&c->ycpu_dev, (size_t)HG_MAX_BATCH * cfg.max_n * 4));
     CREATE_CK(cudaEventCreateWithFlags(&c->ev_x, cudaEventDisableTiming));
@@ -915,7 +1050,8 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
         for (auto e : c->ev_arrived) if (e) cudaEventDestroy(e);
         for (auto e : c->ev_free) if (e) cudaEventDestroy(e);
         for (auto e : c->tev) cudaEventDestroy(e);
-        for (cudaEvent_t e : {c->ev_x, c->ev_ycpu[0], c->ev_ycpu[1], c->ev_done, c->ev_call0, c->ev_call1})
+        for (cudaEvent_t e : {c->ev_x, c->ev_ycpu[0], c->ev_ycpu[1], c->ev_yg[0], c->ev_yg[1], c->ev_done,
+                              c->ev_call0, c->ev_call1})
             if (e) cudaEventDestroy(e);
         if (c->copy) cudaStreamDestroy(c->copy);
         for (void *p : {(void *)c->ring, (void *)c->ycpu_dev, (void *)c->ws, (void *)c->counters,
@@ -990,7 +1126,8 @@ HG_API hg_status hg_layer(hg_ctx *c, const hg_opt_layer *l, void *h, int batch,
     std::vector<ChunkReq> list;
     for (int i = 0; i < 4; ++i) push_chunks(list, l->lin[i].plan, l->lin[i].W_host);
     set_future(c, std::move(list), false);
-    HG_TRY(run_layer(c, *l, h, batch, trace, s));
+    if (can_mirror(c, l, 1, trace)) HG_TRY(run_stack_mirror(c, l, 1, h, batch, s));
+    else HG_TRY(run_layer(c, *l, h, batch, trace, s));
     return end_call(c, s);
 }
 
@@ -1008,7 +1145,13 @@ HG_API hg_status hg_stack(hg_ctx *c, const hg_opt_layer *layers, int n_layers, v
     for (int l = 0; l < n_layers; ++l)
         for (int i = 0; i < 4; ++i) push_chunks(list, layers[l].lin[i].plan, layers[l].lin[i].W_host);
     set_future(c, std::move(list), c->cfg.wrap_prefetch != 0);
-    for (int l = 0; l < n_layers; ++l) HG_TRY(run_layer(c, layers[l], h, batch, nullptr, s));
+    if (can_mirror(c, layers, n_layers, nullptr)) {
+        for (int l = 1; l < n_layers; ++l)
+            if (layers[l].hidden != layers[0].hidden) return set_error(HG_EINVAL, "layers differ in hidden size");
+        HG_TRY(run_stack_mirror(c, layers, n_layers, h, batch, s));
+    } else {
+        for (int l = 0; l < n_layers; ++l) HG_TRY(run_layer(c, layers[l], h, batch, nullptr, s));
+    }
     return end_call(c, s);
 }
 

@@ -66,13 +66,15 @@ class Config(ctypes.Structure):
                 ("max_k", ctypes.c_int64), ("max_n", ctypes.c_int64), ("cpu_threads", ctypes.c_int32),
                 ("cpu_first", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
                 ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double),
-                ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32)]
+                ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32),
+                ("mirror_glue", ctypes.c_int32), ("verify_mirror", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
-    _fields_ = ([(n, ctypes.c_double) for n in ("wall_s", "cpu_busy_s", "link_busy_s", "gpu_busy_s", "x_wait_s")]
+    _fields_ = ([(n, ctypes.c_double) for n in ("wall_s", "cpu_busy_s", "link_busy_s", "gpu_busy_s", "x_wait_s",
+                                                "glue_s")]
                 + [(n, ctypes.c_int64) for n in ("bytes_res", "bytes_str", "bytes_cpu", "n_chunks", "n_linears",
-                                                 "gpu_launches")])
+                                                 "gpu_launches", "mirror_linears", "mirror_mismatch")])
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -80,13 +82,14 @@ class Stats(ctypes.Structure):
 
 class LinearDesc(ctypes.Structure):
     _fields_ = [("W_dev", ctypes.c_void_p), ("W_host", ctypes.c_void_p), ("bias", ctypes.c_void_p),
-                ("plan", Plan)]
+                ("plan", Plan), ("bias_host", ctypes.c_void_p)]
 
 
 class OptLayer(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int64), ("ffn", ctypes.c_int64), ("lin", LinearDesc * 4),
                 ("ln1_g", ctypes.c_void_p), ("ln1_b", ctypes.c_void_p), ("ln2_g", ctypes.c_void_p),
-                ("ln2_b", ctypes.c_void_p)]
+                ("ln2_b", ctypes.c_void_p), ("ln1_g_host", ctypes.c_void_p), ("ln1_b_host", ctypes.c_void_p),
+                ("ln2_g_host", ctypes.c_void_p), ("ln2_b_host", ctypes.c_void_p)]
 
 
 class LayerTrace(ctypes.Structure):
@@ -307,16 +310,21 @@ class Context:
         _check(_lib.hg_reset_stats(self._h))
 
 
-def linear_desc(plan: Plan, W_dev=None, W_host=None, bias=None) -> LinearDesc:
-    return LinearDesc(_ptr(W_dev), _ptr(W_host), _ptr(bias), plan)
+def linear_desc(plan: Plan, W_dev=None, W_host=None, bias=None, bias_host=None) -> LinearDesc:
+    """bias: device fp32 [N_local]; bias_host: the same values in host memory (CPU tensor / numpy
+    float32), needed by the mirrored glue (hg_config.mirror_glue) when the plan has CPU rows."""
+    return LinearDesc(_ptr(W_dev), _ptr(W_host), _ptr(bias), plan, _ptr(bias_host))
 
 
-def opt_layer(hidden, ffn, descs, ln1_g=None, ln1_b=None, ln2_g=None, ln2_b=None) -> OptLayer:
+def opt_layer(hidden, ffn, descs, ln1_g=None, ln1_b=None, ln2_g=None, ln2_b=None, ln_host=None) -> OptLayer:
+    """ln_host: optional (g1, b1, g2, b2) host copies of the LN parameters (mirrored glue)."""
     L = OptLayer()
     L.hidden, L.ffn = hidden, ffn
     for i, d in enumerate(descs):
         L.lin[i] = d
     L.ln1_g, L.ln1_b, L.ln2_g, L.ln2_b = (_ptr(t) for t in (ln1_g, ln1_b, ln2_g, ln2_b))
+    if ln_host is not None:
+        L.ln1_g_host, L.ln1_b_host, L.ln2_g_host, L.ln2_b_host = (_ptr(t) for t in ln_host)
     return L
 
 

@@ -126,3 +126,66 @@ def test_stack_wrap_then_other_calls():
             h2 = dev(h0)
             c.hg_layer(layers[1], h2, B)  # diverges from the wrapped schedule
             torch.cuda.synchronize()
+
+
+def make_layer_mirror(ctx, H, F, B, layer=0, seed=21, r=0.0, alpha=0.5, keep=None, ln=False):
+    """make_layer with host copies of the biases (and LN parameters) for the mirrored glue."""
+    shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+    descs = []
+    for name in NAMES:
+        N, K = shapes[name]
+        _, W, b = gen.linear_inputs(seed, layer, name, 1, N, K)
+        n_res = oracle.resident_rows(r, N, ctx.config.granule)
+        p = ctx.plan(hg.make_rates(1, 1, 1), N, K, B, n_res, hg.FIXED, alpha)
+        W_dev = dev(W[:n_res]) if n_res else None
+        W_host = pinned(W[n_res:]) if n_res < N else None
+        bias, bias_h = dev_f32(b), torch.from_numpy(np.ascontiguousarray(b, np.float32))
+        keep += [W_dev, W_host, bias, bias_h]
+        descs.append(hg.linear_desc(p, W_dev, W_host, bias, bias_h))
+    lnp = {}
+    if ln:
+        for k, sd in (("g1", 1), ("b1", 2), ("g2", 3), ("b2", 4)):
+            v = gen.bf16_bits_to_f32(gen.uniform_bf16(seed + sd, 900 + layer, H, 0.5)) + (1.0 if k[0] == "g" else 0.0)
+            lnp[k] = (dev_f32(v), torch.from_numpy(np.ascontiguousarray(v, np.float32)))
+            keep += list(lnp[k])
+        return hg.opt_layer(H, F, descs, lnp["g1"][0], lnp["b1"][0], lnp["g2"][0], lnp["b2"][0],
+                            ln_host=(lnp["g1"][1], lnp["b1"][1], lnp["g2"][1], lnp["b2"][1]))
+    return hg.opt_layer(H, F, descs)
+
+
+@pytest.mark.parametrize("B,r,alpha,ln", [(1, 0.0, 0.5, False), (3, 0.25, 0.3, True), (2, 0.0, 0.0, True),
+                                          (1, 0.5, 1.0, False), (8, 0.0, 0.6, True)])
+def test_mirrored_glue_bit_exact(B, r, alpha, ln):
+    """The CPU lane's mirrored glue (reading R24) reproduces every GPU glue output bit for bit
+    (verify_mirror counts mismatching activation elements), and the stack output equals the
+    GPU-only glue path's."""
+    H, F = 512, 2048
+    outs = {}
+    for mirror in (1, 0):
+        with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=4096, max_n=8192,
+                        mirror_glue=mirror, verify_mirror=mirror) as c:
+            keep = []
+            layers = [make_layer_mirror(c, H, F, B, layer=l, r=r, alpha=alpha, keep=keep, ln=ln) for l in range(3)]
+            h0 = gen.uniform_bf16(9, 995, B * H, 1.0).reshape(B, H)
+            h = dev(h0)
+            c.hg_stack(layers, h, B)
+            torch.cuda.synchronize()
+            st = c.hg_stats()
+            if mirror:
+                assert st.mirror_linears == 12 and st.mirror_mismatch == 0, (st.mirror_linears, st.mirror_mismatch)
+            else:
+                assert st.mirror_linears == 0
+            outs[mirror] = bits(h)
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_mirror_falls_back_without_host_bias():
+    """Device biases without host copies on a plan with CPU rows: the GPU-only glue is used."""
+    H, F, B = 256, 1024, 1
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=32 << 20, max_k=4096, max_n=8192) as c:
+        keep = []
+        L = make_layer(c, H, F, B, alpha=0.5, keep=keep)[0]
+        h = dev(gen.uniform_bf16(10, 994, B * H, 1.0).reshape(B, H))
+        c.hg_layer(L, h, B)
+        torch.cuda.synchronize()
+        assert c.hg_stats().mirror_linears == 0
