@@ -182,13 +182,29 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20):
     if tot_time <= 0:
         return None
     gbps = tot_bytes / tot_time / 1e9
+    traffic, traffic_detail = ncu_traffic()
     return {"bound": "hbm", "kernel": "gemv_stream_kernel (persistent per-linear GEMV, TMA bulk staged)",
             "achieved": round(gbps, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4),
-            "traffic": None,
+            "traffic": traffic, "traffic_detail": traffic_detail,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy BW)" if "hbm_gbs" in pk else "fallback 6650 GB/s",
             "per_linear": detail,
             "note": "bytes = 2*K*(n_res+n_str) per launch; CUDA events around each hg_gemv_replay launch (the "
                     "step's launch configuration, arrival tags skipped), L2 flushed between launches; mean"}
+
+
+def ncu_traffic():
+    """DRAM traffic per launch of the dominant kernel from the committed `ncu --set full` capture
+    of the same launch configuration (profiles/r01/ncu_gemv_replay_traffic.json): mean over the
+    four linears of dram__bytes_read.sum + dram__bytes_write.sum, beside their algorithmic bytes."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_gemv_replay_traffic.json")))
+    except Exception:
+        return None, None
+    per = d["per_launch"]
+    traffic = statistics.mean((v["dram_read_MB"] + v["dram_write_MB"]) * 1e6 for v in per.values())
+    alg = statistics.mean(v["algorithmic_MB"] * 1e6 for v in per.values())
+    return round(traffic), {"algorithmic_bytes_per_launch": round(alg), "ratio": round(traffic / alg, 4),
+                            "source": d["source"]}
 
 
 # ---------------------------------------------------------------- our arm
@@ -316,11 +332,13 @@ def main_arm(args):
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     w0 = time.perf_counter()
+    torch.cuda.nvtx.range_push("hg_timed")  # ncu --nvtx --nvtx-include hg_timed/ selects these launches
     e0.record(s)
     for _ in range(args.steps):
         step_device()
     e1.record(s)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_pop()
     wall = time.perf_counter() - w0
     barrier()
     launches = ctx.hg_stats().gpu_launches
@@ -376,9 +394,13 @@ def main_arm(args):
     t_link_roof = plan_tot["bytes_str"] / rd["b_link"]
     t_cpu_roof = plan_tot["bytes_cpu"] / rd["b_cpu"]
     t_hbm_roof = 2 * plan_tot["bytes_str"] / (hbm_peak * 1e9)
+    # 4th term: every offloaded byte is read from host DRAM once, by the DMA or by the
+    # CPU lane, so the joint host-DRAM rate measured with both running bounds the sum
+    b_host = rd.get("b_host") or 0.0
+    t_host_roof = (plan_tot["bytes_str"] + plan_tot["bytes_cpu"]) / b_host if b_host > 0 else 0.0
     # best achievable over alpha: all host bytes shared by link + CPU at their peaks
     shard_bytes = STACK_BYTES / world * args.layers / LAYERS
-    t_opt = shard_bytes / (rd["b_link"] + rd["b_cpu"])
+    t_opt = shard_bytes / min(rd["b_link"] + rd["b_cpu"], b_host if b_host > 0 else math.inf)
     lanes = None
     if sctx_stats:
         wall_i = sctx_stats["wall_s"] or 1
@@ -389,7 +411,9 @@ def main_arm(args):
                  "busy_frac": {"cpu": round(sctx_stats["cpu_busy_s"] / wall_i, 3),
                                "link": round(sctx_stats["link_busy_s"] / wall_i, 3),
                                "gpu": round(sctx_stats["gpu_busy_s"] / wall_i, 4)},
-                 "x_wait_ms": round(sctx_stats["x_wait_s"] * 1e3, 2)}
+                 "x_wait_ms": round(sctx_stats["x_wait_s"] * 1e3, 2),
+                 "glue_ms": round(sctx_stats["glue_s"] * 1e3, 2),
+                 "steps": 2, "mirror_linears": sctx_stats["mirror_linears"]}
     line = {
         "metric": METRIC, "value": round(ms_tok, 3), "unit": "ms/token", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_tok, 3),
@@ -407,10 +431,12 @@ def main_arm(args):
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms/token", "h2d_bytes_per_step": B * H * 2,
                 "d2h_bytes_per_step": B * H * 2},
         "roofline": roof,
-        "path_roofline": {"bound": "host-link + host-CPU (+HBM)",
-                          "t_roof_ms_at_plan_alpha": round(max(t_link_roof, t_cpu_roof, t_hbm_roof) * 1e3, 3),
+        "path_roofline": {"bound": "max(host link, host CPU, HBM, joint host DRAM)",
+                          "terms_ms": {"link": round(t_link_roof * 1e3, 3), "cpu": round(t_cpu_roof * 1e3, 3),
+                                       "hbm": round(t_hbm_roof * 1e3, 3), "host_dram": round(t_host_roof * 1e3, 3)},
+                          "t_roof_ms_at_plan_alpha": round(max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof) * 1e3, 3),
                           "t_opt_ms_best_alpha": round(t_opt * 1e3, 3),
-                          "frac_of_roof_at_plan": round(max(t_link_roof, t_cpu_roof, t_hbm_roof) * 1e3 / ms_tok, 4),
+                          "frac_of_roof_at_plan": round(max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof) * 1e3 / ms_tok, 4),
                           "frac_of_best": round(t_opt * 1e3 / ms_tok, 4),
                           "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3)},
         "rates_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rd.items()},

@@ -101,6 +101,9 @@ typedef struct {
     double b_hbm;   /* HBM roofline peak                                             */
     double b_link;  /* host-link roofline peak                                       */
     double b_cpu;   /* host-DRAM roofline peak for the CPU lane's threads            */
+    double b_host;  /* joint host-DRAM rate: CPU-lane reads + DMA reads in one window
+                       (hg_measure flags bit 0; 0 = not measured).  Every offloaded weight
+                       byte is read from host DRAM once, by one lane or the other.       */
 } hg_rates;
 
 /* The per-linear plan.  Integers are exact;
@@ -234,7 +237,7 @@ HG_API hg_status hg_plan(const hg_rates *rates, int64_t N, int64_t K, int batch,
  * processing time"; the alpha benchmark's measurements).
  *   W_host: page-locked [N, K] bf16 weight to measure on (a real linear).
  *   flags bit 0: measure the CPU lane while the link is busy (shared host DRAM).
- * Fills v_cpu, v_gpu, v_link, b_link (large-chunk copy), b_cpu (host read rate
+ * Fills v_cpu, v_gpu, v_link, b_link (large-chunk copy), b_host (flags bit 0), b_cpu (host read rate
  * of the pool threads), b_hbm (device read rate); v_pin = +inf. */
 HG_API hg_status hg_measure(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch,
                             int flags, hg_rates *out);

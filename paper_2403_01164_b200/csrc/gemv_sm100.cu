@@ -248,16 +248,19 @@ __global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const 
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    // x part p -> shared memory, once per launch (every source has the same x)
-    {
+    __syncthreads();  // barriers initialised; the producer starts streaming W right away
+    constexpr int kConsumerThreads = kConsumerWarps * 32;
+    if (warp < kConsumerWarps) {
+        // x part p -> shared memory, once per launch (every source has the same x), overlapping
+        // the producer's first bulk copies; only the consumers wait for it
         const uint4 *xg = (const uint4 *)a.x;
         const int64_t Kv = a.K >> 3;
-        for (int64_t i = threadIdx.x; i < (int64_t)B * kv; i += blockDim.x) {
+        for (int64_t i = threadIdx.x; i < (int64_t)B * kv; i += kConsumerThreads) {
             const int64_t b = i / kv, v = i - b * kv;
             xs[b * kvmax + v] = xg[b * Kv + (k0 >> 3) + v];
         }
+        asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
     }
-    __syncthreads();
 
     const int64_t s_begin = a.n_res > 0 ? -1 : 0;
     if (warp == kConsumerWarps) {
@@ -403,7 +406,6 @@ __global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const 
     }
     if (a.P == 1) return;
     // ---------------------------------------------------------------- P > 1: parts -> y
-    constexpr int kConsumerThreads = kConsumerWarps * 32;
     asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
     if (threadIdx.x == 0) grid_barrier(a);
     asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");

@@ -1272,15 +1272,21 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
         c->st.wall_s = ms * 1e-3;
         if (c->cfg.collect_stats) {
             HG_CK(c, cudaStreamSynchronize(c->copy));
+            // busy time inside the calls' window [ev_call0, ev_call1]: the copy stream also runs
+            // ahead into chunks of later calls (prefetch), which belong to those calls
+            const double wall = c->st.wall_s;
+            auto clipped = [&](const std::pair<size_t, size_t> &pr) {
+                float a = 0, b = 0;
+                if (cudaEventElapsedTime(&a, c->ev_call0, c->tev[pr.first]) != cudaSuccess ||
+                    cudaEventElapsedTime(&b, c->ev_call0, c->tev[pr.second]) != cudaSuccess)
+                    return 0.0;
+                const double t0 = std::min(std::max(a * 1e-3, 0.0), wall);
+                const double t1 = std::min(std::max(b * 1e-3, 0.0), wall);
+                return t1 > t0 ? t1 - t0 : 0.0;
+            };
             double link = 0, gpu = 0;
-            for (auto &pr : c->copy_ev) {
-                if (cudaEventElapsedTime(&ms, c->tev[pr.first], c->tev[pr.second]) == cudaSuccess)
-                    link += ms * 1e-3;
-            }
-            for (auto &pr : c->gemv_ev) {
-                if (cudaEventElapsedTime(&ms, c->tev[pr.first], c->tev[pr.second]) == cudaSuccess)
-                    gpu += ms * 1e-3;
-            }
+            for (auto &pr : c->copy_ev) link += clipped(pr);
+            for (auto &pr : c->gemv_ev) gpu += clipped(pr);
             cudaGetLastError();
             c->st.link_busy_s = link;
             c->st.gpu_busy_s = gpu;
@@ -1444,32 +1450,32 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     }
     out->b_hbm = (double)ring_bytes / (best * 1e-3);
 
-    // CPU lane: the pool's GEMV over the whole weight; optionally under link load
+    // CPU lane: the pool's GEMV over the whole weight and the pool's read bandwidth, optionally
+    // while the link streams (flags bit 0: both lanes read the same host DRAM).  Medians of many
+    // short runs: single runs on a shared host are noisy.
     std::vector<uint16_t> xh((size_t)batch * K, 0x3f80);
     std::vector<float> yh((size_t)batch * N);
-    if (flags & 1) {  // keep the link busy for the duration of the CPU probe
-        for (int64_t off = 0, n = 0; n < 64; ++n, off = (off + chunk) % (wbytes - chunk + 1))
-            HG_CK(c, cudaMemcpyAsync(c->ring, src + off / 256 * 256, chunk, cudaMemcpyHostToDevice, c->copy));
+    const int NB = (flags & 1) ? 192 : 0;  // 192 chunks ~ 6 GiB ~ 110 ms of link time
+    std::vector<cudaEvent_t> evb((size_t)NB, nullptr);
+    for (int i = 0; i < NB; ++i) HG_CK(c, cudaEventCreateWithFlags(&evb[i], cudaEventDisableTiming));
+    for (int64_t off = 0, n = 0; n < NB; ++n, off = (off + chunk) % (wbytes - chunk + 1)) {
+        HG_CK(c, cudaMemcpyAsync(c->ring, src + off / 256 * 256, chunk, cudaMemcpyHostToDevice, c->copy));
+        HG_CK(c, cudaEventRecord(evb[n], c->copy));
     }
-    double best_cpu = 1e30;
-    for (int it = 0; it < 3; ++it) {
-        auto t0 = clk::now();
-        HG_TRY(hg_host_gemv(c, xh.data(), batch, N, K, W_host, nullptr, yh.data()));
-        best_cpu = std::min(best_cpu, secs(t0, clk::now()));
-    }
-    out->v_cpu = (double)wbytes / best_cpu;
-    // host read bandwidth of the pool (b_cpu)
+    auto completed = [&]() {
+        int n = 0;
+        while (n < NB && cudaEventQuery(evb[n]) == cudaSuccess) ++n;
+        cudaGetLastError();
+        return n;
+    };
     struct RJ { const uint8_t *p; int64_t bytes, block; std::atomic<int64_t> next; std::atomic<uint64_t> sum; };
     RJ rj;
     rj.p = src;
     rj.bytes = wbytes;
     rj.block = 1 << 20;
-    const char *isa = hg_host_isa();
-    double best_rd = 1e30;
-    for (int it = 0; it < 3; ++it) {
+    auto read_pass = [&]() {
         rj.next.store(0);
         rj.sum.store(0);
-        auto t0 = clk::now();
         pool_run(c->pool, [](void *a, int) {
             RJ *r = (RJ *)a;
             const int64_t nb = (r->bytes + r->block - 1) / r->block;
@@ -1483,10 +1489,41 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
             }
             r->sum.fetch_xor(s);
         }, &rj);
-        best_rd = std::min(best_rd, secs(t0, clk::now()));
+    };
+    auto median = [](std::vector<double> v) {
+        std::sort(v.begin(), v.end());
+        return v[v.size() / 2];
+    };
+    out->b_host = 0;
+    if (NB > 0) {  // joint host-DRAM rate: CPU reads + DMA reads in the same window
+        read_pass();  // warm
+        const int n0 = completed();
+        const auto t0 = clk::now();
+        int passes = 0;
+        while (secs(t0, clk::now()) < 0.03) {
+            read_pass();
+            ++passes;
+        }
+        const int n1 = completed();
+        const double dt = secs(t0, clk::now());
+        if (n1 < NB)
+            out->b_host = ((double)passes * wbytes + (double)(n1 - n0) * chunk) / dt;
     }
-    (void)isa;
-    out->b_cpu = (double)wbytes / best_rd;
+    std::vector<double> tg, tr;
+    for (int it = 0; it < 9; ++it) {
+        auto t0 = clk::now();
+        HG_TRY(hg_host_gemv(c, xh.data(), batch, N, K, W_host, nullptr, yh.data()));
+        tg.push_back(secs(t0, clk::now()));
+    }
+    out->v_cpu = (double)wbytes / median(tg);
+    for (int it = 0; it < 9; ++it) {
+        auto t0 = clk::now();
+        read_pass();
+        tr.push_back(secs(t0, clk::now()));
+    }
+    out->b_cpu = (double)wbytes / median(tr);
+    HG_CK(c, cudaStreamSynchronize(c->copy));
+    for (auto e : evb) cudaEventDestroy(e);
     out->v_pin = INFINITY;
     HG_CK(c, cudaStreamSynchronize(c->copy));
     cudaEventDestroy(e0);

@@ -45,7 +45,8 @@ def _check(st: int):
 
 # ---------------------------------------------------------------- structs (mirror hg.h)
 class Rates(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_double) for n in ("v_cpu", "v_gpu", "v_link", "v_pin", "b_hbm", "b_link", "b_cpu")]
+    _fields_ = [(n, ctypes.c_double) for n in ("v_cpu", "v_gpu", "v_link", "v_pin", "b_hbm", "b_link", "b_cpu",
+                                               "b_host")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -186,8 +187,8 @@ def hg_config_default() -> Config:
     return c
 
 
-def make_rates(v_cpu, v_gpu, v_link, v_pin=math.inf, b_hbm=None, b_link=None, b_cpu=None) -> Rates:
-    return Rates(v_cpu, v_gpu, v_link, v_pin, b_hbm or v_gpu, b_link or v_link, b_cpu or v_cpu)
+def make_rates(v_cpu, v_gpu, v_link, v_pin=math.inf, b_hbm=None, b_link=None, b_cpu=None, b_host=0.0) -> Rates:
+    return Rates(v_cpu, v_gpu, v_link, v_pin, b_hbm or v_gpu, b_link or v_link, b_cpu or v_cpu, b_host)
 
 
 def hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed=0.0, granule=128, chunk_bytes=16 << 20) -> Plan:

@@ -21,17 +21,24 @@ if has micro; then
   timeout 600 python tools/microbench.py > $out/micro.txt 2>&1; tail -30 $out/micro.txt
 fi
 if has launches; then
-  # launch list of the bench command (serialised, cold-cache: compare shares)
-  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
+  # launch list of the bench command's timed step (NVTX range hg_timed; serialised, cold-cache:
+  # compare shares, not absolutes)
+  timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --nvtx --nvtx-include "hg_timed/" \
+    --csv --log-file $out/launches.csv \
     python bench.py --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline > $out/launches_bench.json 2>&1
   echo "launches rc=$?"
   python tools/ncu_summary.py launches $out/launches.csv > $out/launches_summary.md 2>&1; head -20 $out/launches_summary.md
 fi
 if has full; then
-  # the top kernel (streamed-chunk GEMV) inside the step
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:gemv_stream -s 8 -c 4 \
-    -o $out/prof_gemv python bench.py --layers 4 --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline \
+  # the top kernel: the persistent GEMV inside the timed step (4 launches), and its replay
+  timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "hg_timed/" \
+    -k regex:gemv_stream -c 4 -o $out/prof_gemv_step \
+    python bench.py --layers 4 --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline --no-abench \
     > $out/full_bench.log 2>&1
   echo "full rc=$?"
-  python tools/ncu_summary.py full $out/prof_gemv.ncu-rep > $out/full_summary.md 2>&1; head -60 $out/full_summary.md
+  python tools/ncu_summary.py full $out/prof_gemv_step.ncu-rep > $out/full_summary_step.md 2>&1
+  REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_stream \
+    -o $out/prof_gemv_replay python tools/prof_replay.py > $out/full_replay.log 2>&1
+  python tools/ncu_summary.py full $out/prof_gemv_replay.ncu-rep > $out/full_summary_replay.md 2>&1
+  head -40 $out/full_summary_replay.md
 fi
