@@ -138,7 +138,7 @@ def run_reference(args):
     return 0
 
 
-def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20):
+def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     """Average device time of the step's GEMV launches -- one persistent launch per linear over
     its resident rows and all its streamed chunks (hg_gemv_replay: same kernel, grid and
     per-chunk work split as in the step, chunks read from ring slots 0..n_chunks-1 with the
@@ -158,9 +158,10 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20):
             continue
         x = torch.empty((B, p.K), dtype=torch.int16, device="cuda").random_(-3000, 3000)
         y = torch.empty((B, p.N), device="cuda")
+        Wd = (W_dev or {}).get(name)
         try:
             for _ in range(3):
-                ctx.hg_gemv_replay(p, x, None, None, y, stream=s)
+                ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s)
         except Exception as e:  # tcgen05 batches: no replay entry point
             return {"unavailable": str(e)}
         ts = []
@@ -168,7 +169,7 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
-            ctx.hg_gemv_replay(p, x, None, None, y, stream=s)
+            ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s)
             e1.record(s)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e-3)
@@ -208,7 +209,8 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------- our arm
-def main_arm(args):
+def prepare(args):
+    """Process-wide setup: context, this rank's pinned weights, measured rates."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -232,9 +234,8 @@ def main_arm(args):
         dist.broadcast_object_list(obj, src=0)
         ctx.hg_dist_init(world, rank, obj[0])
     B = args.batch
-    G = 128
 
-    # ---- weights: this rank's row shard of every linear, pinned host (r = 0) ----
+    # ---- weights: this rank's row shard of every linear, pinned host ----
     t_setup = time.perf_counter()
     host, biases, biases_h = [], [], []
     for l in range(args.layers):
@@ -255,38 +256,108 @@ def main_arm(args):
         biases_h.append(bh)
     t_setup = time.perf_counter() - t_setup
 
-    # ---- a1: measured rates -> alpha (Eq. 5), per-linear plans ----
+    # ---- a1: measured rates (Fig. 1's "parameter size divided by processing time") ----
     fc1 = host[0]["fc1"]
     rates = ctx.hg_measure(fc1, fc1.shape[0], H, B, under_load=True)
-    pk = peaks()
-    rd = rates.as_dict()
-    if args.alpha is not None:
-        mode, af = hg.FIXED, args.alpha
-    else:
-        mode, af = hg.EXACT, 0.0
-    layers = []
-    plans = {}
-    for l in range(args.layers):
-        descs = []
-        for name in NAMES:
-            N, K = SHAPES[name]
-            p = ctx.plan(rates, N // world, K, B, 0, mode, af)
-            plans[name] = p
-            descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name], biases_h[l][name]))
-        layers.append(hg.opt_layer(H, F, descs))
 
     h0 = gen.uniform_bf16(SEED + 1, 999, B * H, 1.0).reshape(B, H)
     h_host = torch.empty((B, H), dtype=torch.int16, pin_memory=True)
     h_host.numpy()[...] = h0.view(np.int16)
-    h_dev = h_host.cuda()
-    h_out = torch.empty_like(h_host, pin_memory=True)
-    s = torch.cuda.Stream()
+    return {"torch": torch, "dist": dist, "hg": hg, "rank": rank, "world": world, "local": local,
+            "threads": threads, "ctx": ctx, "B": B, "host": host, "biases": biases, "biases_h": biases_h,
+            "rates": rates, "t_setup": t_setup, "h_host": h_host, "h_dev": h_host.cuda(),
+            "h_out": torch.empty_like(h_host, pin_memory=True), "stream": torch.cuda.Stream(), "v_kind": None}
+
+
+def cpu_rate_per_kind(st):
+    """T-bar_CPU per module kind for the scheduler: the CPU lane's GEMV rate on layer 0's weight
+    of each kind (bytes/s, median of 3), measured like Fig. 1."""
+    if st["v_kind"] is None:
+        import numpy as np
+        ctx, B = st["ctx"], st["B"]
+        v = {}
+        for name in NAMES:
+            W = st["host"][0][name]
+            n, K = W.shape
+            x = np.full((B, K), 0x3F80, np.uint16)
+            y = np.zeros((B, n), np.float32)
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                ctx.hg_host_gemv(x, B, n, K, W, None, y)
+                ts.append(time.perf_counter() - t0)
+            v[name] = 2 * n * K / statistics.median(ts)
+        st["v_kind"] = v
+    return st["v_kind"]
+
+
+def build_layers(st, args, mode, af, n_res_map, W_dev_map):
+    hg = st["hg"]
+    ctx, world, B = st["ctx"], st["world"], st["B"]
+    layers, plans_l0, all_plans = [], {}, []
+    for l in range(args.layers):
+        descs = []
+        for name in NAMES:
+            N, K = SHAPES[name]
+            n_res = n_res_map.get((l, name), 0)
+            p = ctx.plan(st["rates"], N // world, K, B, n_res, mode, af)
+            if l == 0:
+                plans_l0[name] = p
+            all_plans.append(p)
+            W_h = st["host"][l][name][n_res:] if n_res < N // world else None
+            descs.append(hg.linear_desc(p, W_dev_map.get((l, name)), W_h, st["biases"][l][name],
+                                        st["biases_h"][l][name]))
+        layers.append(hg.opt_layer(H, F, descs))
+    return layers, plans_l0, all_plans
+
+
+def run_point(st, args, budget_gb=0.0):
+    """One measured configuration: schedule (HBM budget), plan, alpha benchmark, timed steps."""
+    torch, dist, hg = st["torch"], st["dist"], st["hg"]
+    rank, world, local, B = st["rank"], st["world"], st["local"], st["B"]
+    ctx, s, h_host, h_dev, h_out = st["ctx"], st["stream"], st["h_host"], st["h_dev"], st["h_out"]
+    rates = st["rates"]
+    rd = rates.as_dict()
+    pk = peaks()
+    if args.alpha is not None:
+        mode, af = hg.FIXED, args.alpha
+    else:
+        mode, af = hg.EXACT, 0.0
+
+    # ---- NEXT(3): heterogeneous module scheduler under an HBM budget (Sec. 4.5) ----
+    n_res_map, W_dev_map, sched = {}, {}, None
+    if budget_gb > 0:
+        p0 = ctx.plan(rates, SHAPES["fc1"][0] // world, H, B, 0, mode, af)
+        alpha0 = p0.alpha_eff
+        v_kind = cpu_rate_per_kind(st)
+        mods, keys = [], []
+        for l in range(args.layers):
+            for name in NAMES:
+                N, K = SHAPES[name]
+                n = N // world
+                mods.append((n, K, (1.0 - alpha0) * 2 * n * K / v_kind[name]))  # T-bar_CPU at alpha
+                keys.append((l, name))
+        n_res_list, used = hg.hg_schedule(mods, int(budget_gb * 1e9), 128, True)
+        for key, nr in zip(keys, n_res_list):
+            if nr > 0:
+                n_res_map[key] = nr
+                W_dev_map[key] = st["host"][key[0]][key[1]][:nr].cuda()
+        torch.cuda.synchronize()
+        sched = {"budget_GB": budget_gb, "placed_GB": round(used / 1e9, 3), "alpha_for_gain": alpha0,
+                 "gain_s_per_GB": {k: round((1.0 - alpha0) / v_kind[k] * 1e9, 6) for k in NAMES},
+                 "cpu_GBps_by_kind": {k: round(v_kind[k] / 1e9, 2) for k in NAMES},
+                 "resident_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if nr == n),
+                 "partial_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if 0 < nr < n)}
+    layers, plans, all_plans = build_layers(st, args, mode, af, n_res_map, W_dev_map)
+    h_dev.copy_(h_host)
 
     # ---- a1 refinement: the alpha benchmark (Sec. 4.4, P:252-266) around the Eq. (5) alpha: lane
     # times measured in this pipeline under real interference, fitted and solved F_CPU = F_COM ----
     abench = None
-    alpha_seed = plans["fc1"].alpha_req
-    if args.alpha is None and args.abench:
+    # Eq. (5) alpha from the measured rates (the same for every module: rates are per byte)
+    alpha_seed = ctx.plan(rates, SHAPES["fc1"][0] // world, H, B, 0, mode, af).alpha_req
+    any_host = any(p.n_res < p.N for p in all_plans)
+    if args.alpha is None and args.abench and any_host:
         if world > 1:  # every rank must sample the same alpha grid (the stack all-gathers)
             t = torch.tensor([alpha_seed], dtype=torch.float64, device="cuda")
             dist.broadcast(t, 0)
@@ -294,15 +365,7 @@ def main_arm(args):
         res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_seed, gamma=args.abench_gamma, lam=0.02, degree=2,
                                  reps=1, stream=s)
         abench = res.as_dict()
-        layers = []
-        for l in range(args.layers):
-            descs = []
-            for name in NAMES:
-                N, K = SHAPES[name]
-                p = ctx.plan(rates, N // world, K, B, 0, hg.FIXED, res.alpha_bar)
-                plans[name] = p
-                descs.append(hg.linear_desc(p, None, host[l][name], biases[l][name], biases_h[l][name]))
-            layers.append(hg.opt_layer(H, F, descs))
+        layers, plans, all_plans = build_layers(st, args, hg.FIXED, res.alpha_bar, n_res_map, W_dev_map)
         h_dev.copy_(h_host)
 
     def barrier():
@@ -359,20 +422,21 @@ def main_arm(args):
     # ---- lane breakdown (Table 2 analogue): instrumented steps after the timed region ----
     sctx_stats = None
     if args.breakdown and world == 1:
-        ctx.close()  # one ring at a time
-        ctx = hg.Context(local, cpu_threads=threads, cpu_first=-1, chunk_bytes=args.chunk_mb << 20,
-                         ring_bytes=args.ring_mb << 20, max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1)
-        ctx.hg_stack(layers, h_dev, B, stream=s)  # fill the prefetch pipeline
-        ctx.hg_reset_stats()
+        sctx = hg.Context(local, cpu_threads=st["threads"], cpu_first=-1, chunk_bytes=args.chunk_mb << 20,
+                          ring_bytes=args.ring_mb << 20, max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1)
+        sctx.hg_stack(layers, h_dev, B, stream=s)  # fill the prefetch pipeline
+        sctx.hg_reset_stats()
         for _ in range(2):
-            ctx.hg_stack(layers, h_dev, B, stream=s)
+            sctx.hg_stack(layers, h_dev, B, stream=s)
         torch.cuda.synchronize()
-        sctx_stats = ctx.hg_stats().as_dict()
+        sctx_stats = sctx.hg_stats().as_dict()
+        sctx.close()
 
-    # ---- dominant kernel: the streamed-chunk GEMV, replayed with CUDA events on cold data ----
+    # ---- dominant kernel: the per-linear GEMV launch, replayed with CUDA events on cold data ----
     roof = None
     if rank == 0:
-        roof = gemv_roofline(ctx, plans, args.layers, B, torch, pk)
+        roof = gemv_roofline(ctx, plans, args.layers, B, torch, pk,
+                             W_dev={name: W_dev_map.get((0, name)) for name in NAMES})
 
     times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
     if world > 1:
@@ -383,24 +447,25 @@ def main_arm(args):
 
     # ---- roofline numbers ----
     hbm_peak = pk.get("hbm_gbs", 6650.0)
-    plan_tot = {"t_roof": 0.0, "t_pred": 0.0, "bytes_str": 0, "bytes_cpu": 0}
-    for name in NAMES:
-        p = plans[name]
-        plan_tot["t_roof"] += p.t_roof * args.layers
-        plan_tot["t_pred"] += p.t_pred * args.layers
-        plan_tot["bytes_str"] += 2 * p.K * p.n_str * args.layers
-        plan_tot["bytes_cpu"] += 2 * p.K * p.n_cpu * args.layers
+    plan_tot = {"t_pred": 0.0, "bytes_str": 0, "bytes_cpu": 0, "bytes_res": 0}
+    for p in all_plans:
+        plan_tot["t_pred"] += p.t_pred
+        plan_tot["bytes_str"] += 2 * p.K * p.n_str
+        plan_tot["bytes_cpu"] += 2 * p.K * p.n_cpu
+        plan_tot["bytes_res"] += 2 * p.K * p.n_res
     # stack roofline: the link runs ahead across linears, so lanes add up over the stack
     t_link_roof = plan_tot["bytes_str"] / rd["b_link"]
     t_cpu_roof = plan_tot["bytes_cpu"] / rd["b_cpu"]
-    t_hbm_roof = 2 * plan_tot["bytes_str"] / (hbm_peak * 1e9)
+    t_hbm_roof = (plan_tot["bytes_res"] + 2 * plan_tot["bytes_str"]) / (hbm_peak * 1e9)
     # 4th term: every offloaded byte is read from host DRAM once, by the DMA or by the
     # CPU lane, so the joint host-DRAM rate measured with both running bounds the sum
     b_host = rd.get("b_host") or 0.0
     t_host_roof = (plan_tot["bytes_str"] + plan_tot["bytes_cpu"]) / b_host if b_host > 0 else 0.0
     # best achievable over alpha: all host bytes shared by link + CPU at their peaks
     shard_bytes = STACK_BYTES / world * args.layers / LAYERS
-    t_opt = shard_bytes / min(rd["b_link"] + rd["b_cpu"], b_host if b_host > 0 else math.inf)
+    host_bytes = plan_tot["bytes_str"] + plan_tot["bytes_cpu"]
+    t_opt = max(host_bytes / min(rd["b_link"] + rd["b_cpu"], b_host if b_host > 0 else math.inf), t_hbm_roof)
+    t_roof = max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof)
     lanes = None
     if sctx_stats:
         wall_i = sctx_stats["wall_s"] or 1
@@ -420,12 +485,16 @@ def main_arm(args):
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator; random-init OPT-30B-shaped weights)",
         "config": {"workload": "OPT-30B 48-layer decode linear stack (qkv,o,fc1,fc2 x48), batch %d" % B,
-                   "batch": B, "hidden": H, "ffn": F, "layers": args.layers, "r_resident": 0.0,
+                   "batch": B, "hidden": H, "ffn": F, "layers": args.layers,
+                   "r_resident": round(plan_tot["bytes_res"] / shard_bytes, 4),
+                   "hbm_budget_GB": budget_gb,
                    "alpha_mode": "fixed" if args.alpha is not None else (
                        "Eq5 (measured rates) refined by the alpha benchmark (Sec. 4.4)" if abench else
                        "Eq5 exact (measured rates)"),
-                   "alpha": plans["fc1"].alpha_eff, "alpha_seed_eq5": alpha_seed, "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
-                   "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": threads,
+                   "alpha": next((p.alpha_eff for p in all_plans if p.n_res < p.N), 0.0),
+                   "alpha_seed_eq5": alpha_seed,
+                   "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
+                   "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": st["threads"],
                    "l2": "inputs larger than L2: %.1f GB of weights streamed/computed per step" % (shard_bytes / 1e9)},
         "gpu_launches": int(launches),
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms/token", "h2d_bytes_per_step": B * H * 2,
@@ -434,13 +503,14 @@ def main_arm(args):
         "path_roofline": {"bound": "max(host link, host CPU, HBM, joint host DRAM)",
                           "terms_ms": {"link": round(t_link_roof * 1e3, 3), "cpu": round(t_cpu_roof * 1e3, 3),
                                        "hbm": round(t_hbm_roof * 1e3, 3), "host_dram": round(t_host_roof * 1e3, 3)},
-                          "t_roof_ms_at_plan_alpha": round(max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof) * 1e3, 3),
+                          "t_roof_ms_at_plan_alpha": round(t_roof * 1e3, 3),
                           "t_opt_ms_best_alpha": round(t_opt * 1e3, 3),
-                          "frac_of_roof_at_plan": round(max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof) * 1e3 / ms_tok, 4),
+                          "frac_of_roof_at_plan": round(t_roof * 1e3 / ms_tok, 4),
                           "frac_of_best": round(t_opt * 1e3 / ms_tok, 4),
                           "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3)},
         "rates_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rd.items()},
         "lanes": lanes,
+        "scheduler": sched,
         "alpha_bench": None if abench is None else {
             "alpha_bar": abench["alpha_bar"], "clamped": abench["clamped"],
             "points": [[round(a, 4), round(tc * 1e3, 3), round(tl * 1e3, 3), round(ts * 1e3, 3)] for a, tc, tl, ts in
@@ -448,19 +518,28 @@ def main_arm(args):
             "points_cols": ["alpha", "t_cpu_ms", "t_link_ms", "t_step_ms"]},
         "clocks": ck,
         "wall_ms_per_step": round(wall / args.steps * 1e3, 3),
-        "setup_s": round(t_setup, 1),
+        "setup_s": round(st["t_setup"], 1),
     }
+    del W_dev_map, layers
+    torch.cuda.empty_cache()
+    return line
+
+
+def main_arm(args):
+    st = prepare(args)
+    line = run_point(st, args, args.hbm_budget_gb)
+    rank, world = st["rank"], st["world"]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ts, nthr = oracle_layer_sample(reps=2, batch=B)
+        ts, nthr = oracle_layer_sample(reps=2, batch=st["B"])
         line["cpu_baseline"] = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr,
                                 "kind": "oracle",
                                 "sample": "layer 0's four linears (1.233 GB), fp64 naive C loops on all host "
                                           "cores, best of 2, scaled x48 to a token"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
+    st["ctx"].close()
     if world > 1:
-        dist.destroy_process_group()
+        st["dist"].destroy_process_group()
     return 0
 
 
@@ -480,6 +559,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-abench", dest="abench", action="store_false", help="use Eq. (5) alpha unrefined")
     ap.add_argument("--abench-gamma", type=float, default=0.06)
+    ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
+                    help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -281,6 +281,23 @@ HG_API hg_status hg_alpha_bench(hg_ctx *ctx, const hg_opt_layer *layers, int n_l
                                 int batch, double alpha_seed, const hg_abench_cfg *cfg,
                                 hg_abench_result *out, void *stream);
 
+/* ---------------------------------------------------------------- module scheduler (Sec. 4.5) */
+/* One module (weight) competing for HBM: its [N, K] rows and its benchmarked CPU time T̄_CPU. */
+typedef struct {
+    int64_t N, K;
+    double t_cpu;   /* seconds the CPU lane spends on this module at the chosen alpha (T̄_CPU) */
+} hg_module;
+
+/* Heterogeneous module scheduler: gain g_i = T̄_CPU,i / Mem_i, Mem_i = 2 N_i K_i
+ * bytes (reading R20).  Modules are taken in descending g (ties: lower index first) and made
+ * fully GPU-resident (n_res_out[i] = N_i) while they fit in budget_bytes; one that does not fit is
+ * skipped, unless allow_partial: then it gets the largest multiple of `granule` rows that fits and
+ * the scan stops.  Every other n_res_out[i] = 0.  *used_bytes (may be NULL) = bytes placed.  Pure
+ * function, no device work.  Errors: HG_EINVAL for n < 0, NULL arrays, budget < 0, granule < 1,
+ * N_i % granule, K_i <= 0, t_cpu negative / non-finite. */
+HG_API hg_status hg_schedule(const hg_module *mods, int n, int64_t budget_bytes, int64_t granule,
+                             int allow_partial, int64_t *n_res_out, int64_t *used_bytes);
+
 /* ---------------------------------------------------------------- a2-a6: one linear */
 /* y[:, 0:N) = x . W^T (+ bias) with the rows of W split by `alpha`:
  *   x_dev [batch, K] bf16 device; W_dev [n_res, K] device (NULL iff n_res == 0);

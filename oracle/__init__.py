@@ -373,6 +373,41 @@ def alpha_bench_solve(alphas, t_cpu, t_com, degree: int, lo: float, hi: float, s
 # c2.6 One OPT pre-LN decoder layer at decode position 0 (reading R22)
 #   All non-linear modules stay on the GPU; the four linears are the
 #   heterogeneous modules.  bf16 storage points mirror the GPU path.
+def schedule(modules, budget_bytes: int, G: int, allow_partial: bool = True):
+    """Heterogeneous module scheduler, Sec. 4.5, step by step.
+
+    "we can quantify it by considering the ratio of the time saved to the GPU memory
+    consumption ... the saved time equals ... our benchmarked CPU time T_CPU":
+    g = T_CPU / Mem, Eq. (13), with Mem = the module's weight bytes 2*N*K (SURVEY 8(c) c3 #20,
+    DESIGN.md R20).  "establish the ranking of each parameter by comparing their schedule gain
+    (g). We then proceed to migrate the weight with the highest g to the GPU ... until the memory
+    limit is reached": rank by g (exact rationals, ties to the lower index), place whole
+    modules while they fit; a module that does not fit is passed over, or -- allow_partial --
+    receives the largest multiple of G rows that fits, after which the budget is exhausted.
+
+    modules: list of (N, K, t_cpu).  Returns (n_res list, bytes used).
+    """
+    mods = list(modules)
+    gains = []
+    for i, (N, K, t) in enumerate(mods):
+        mem = 2 * N * K
+        gains.append(Fraction(t) / mem if mem else Fraction(0))
+    ranking = sorted(range(len(mods)), key=lambda i: (-gains[i], i))
+    left = budget_bytes
+    n_res = [0] * len(mods)
+    for i in ranking:
+        N, K, _ = mods[i]
+        if 2 * N * K <= left:
+            n_res[i] = N
+            left -= 2 * N * K
+        elif allow_partial:
+            rows = (left // (2 * K)) // G * G
+            n_res[i] = rows
+            left -= 2 * K * rows
+            break
+    return n_res, budget_bytes - left
+
+
 # ----------------------------------------------------------------------------
 LN_EPS = 1e-5
 

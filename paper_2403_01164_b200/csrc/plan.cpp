@@ -7,6 +7,8 @@
 // reading R3).
 #include <cmath>
 #include <cstring>
+#include <vector>
+#include <algorithm>
 
 #include "hg.h"
 #include "hg_internal.h"
@@ -226,5 +228,59 @@ extern "C" HG_API hg_status hg_plan(const hg_rates *r, int64_t N, int64_t K, int
     p.t_roof = std::fmax(p.t_hbm, std::fmax(row * (double)n_str / r->b_link,
                                             row * (double)n_cpu / r->b_cpu));
     *out = p;
+    return HG_OK;
+}
+
+// ---------------------------------------------------------------- module scheduler (Sec. 4.5)
+// "the ratio of the time saved to the GPU memory consumption ... g = T_CPU / Mem";
+// "migrate the weight with the highest g to the GPU for each layer until the memory limit is
+// reached".  Mem is the module's whole weight (nothing of it is resident before: reading
+// R20).  Greedy by descending g, ties to the lower index (stable); a module that does not fit is
+// skipped (a later, smaller one may still fit) unless allow_partial, in which case it receives
+// the largest multiple of `granule` rows that fits and the scan stops (the budget is then used up
+// to less than one granule).
+extern "C" HG_API hg_status hg_schedule(const hg_module *mods, int n, int64_t budget_bytes, int64_t granule,
+                                        int allow_partial, int64_t *n_res_out, int64_t *used_bytes) {
+    if (n < 0 || (n > 0 && (!mods || !n_res_out)) || budget_bytes < 0 || granule < 1)
+        return set_error(HG_EINVAL, "hg_schedule: bad arguments");
+    for (int i = 0; i < n; ++i) {
+        if (mods[i].N < 0 || mods[i].K <= 0 || mods[i].N % granule || !(mods[i].t_cpu >= 0.0) ||
+            !std::isfinite(mods[i].t_cpu))
+            return set_error(HG_EINVAL, "hg_schedule: module %d (N=%lld K=%lld t_cpu=%g)", i,
+                             (long long)mods[i].N, (long long)mods[i].K, mods[i].t_cpu);
+    }
+    std::vector<int> order((size_t)n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    // g_a > g_b compared exactly (t_a * Mem_b vs t_b * Mem_a on 128-bit integers), so equal gains
+    // tie to the lower index whatever the rounding of a division would have been
+    auto greater = [&](int a, int b) {
+        const int64_t ma = 2 * mods[a].N * mods[a].K, mb = 2 * mods[b].N * mods[b].K;
+        if (ma == 0 || mb == 0) return ma != 0 && mb == 0 && mods[a].t_cpu > 0;  // empty modules last
+        int ea = 0, eb = 0;
+        const double fa = std::frexp(mods[a].t_cpu, &ea), fb = std::frexp(mods[b].t_cpu, &eb);
+        const unsigned __int128 A = (unsigned __int128)(uint64_t)std::ldexp(fa, 53) * (uint64_t)mb;
+        const unsigned __int128 Bv = (unsigned __int128)(uint64_t)std::ldexp(fb, 53) * (uint64_t)ma;
+        if (A == 0 || Bv == 0) return A != 0;
+        auto bitlen = [](unsigned __int128 v) { int l = 0; while (v) { v >>= 1; ++l; } return l; };
+        const int la = bitlen(A) + ea, lb = bitlen(Bv) + eb;
+        if (la != lb) return la > lb;
+        return ea >= eb ? (A << (ea - eb)) > Bv : A > (Bv << (eb - ea));
+    };
+    std::stable_sort(order.begin(), order.end(), greater);
+    int64_t left = budget_bytes;
+    for (int i = 0; i < n; ++i) n_res_out[i] = 0;
+    for (int i : order) {
+        const int64_t bytes = 2 * mods[i].N * mods[i].K;
+        if (bytes <= left) {
+            n_res_out[i] = mods[i].N;
+            left -= bytes;
+        } else if (allow_partial) {
+            const int64_t rows = left / (2 * mods[i].K) / granule * granule;
+            n_res_out[i] = rows;
+            left -= 2 * mods[i].K * rows;
+            break;
+        }
+    }
+    if (used_bytes) *used_bytes = budget_bytes - left;
     return HG_OK;
 }

@@ -81,6 +81,10 @@ class Stats(ctypes.Structure):
         return {n: getattr(self, n) for n, _ in self._fields_}
 
 
+class Module(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int64), ("K", ctypes.c_int64), ("t_cpu", ctypes.c_double)]
+
+
 class LinearDesc(ctypes.Structure):
     _fields_ = [("W_dev", ctypes.c_void_p), ("W_host", ctypes.c_void_p), ("bias", ctypes.c_void_p),
                 ("plan", Plan), ("bias_host", ctypes.c_void_p)]
@@ -133,6 +137,7 @@ _sig = {
     "hg_stack": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _vp]),
     "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
     "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp]),
+    "hg_schedule": (_i32, [_P(Module), _i32, _i64, _i64, _i32, _P(_i64), _P(_i64)]),
     "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "hg_host_isa": (ctypes.c_char_p, []),
     "hg_dist_unique_id": (_i32, [_vp]),
@@ -189,6 +194,17 @@ def hg_config_default() -> Config:
 
 def make_rates(v_cpu, v_gpu, v_link, v_pin=math.inf, b_hbm=None, b_link=None, b_cpu=None, b_host=0.0) -> Rates:
     return Rates(v_cpu, v_gpu, v_link, v_pin, b_hbm or v_gpu, b_link or v_link, b_cpu or v_cpu, b_host)
+
+
+def hg_schedule(modules, budget_bytes, granule=128, allow_partial=True):
+    """modules: iterable of (N, K, t_cpu).  Returns (n_res list, used_bytes)."""
+    mods = list(modules)
+    arr = (Module * max(1, len(mods)))(*[Module(int(n), int(k), float(t)) for n, k, t in mods])
+    out = (_i64 * max(1, len(mods)))()
+    used = _i64(0)
+    _check(_lib.hg_schedule(arr, len(mods), int(budget_bytes), int(granule), int(bool(allow_partial)), out,
+                            ctypes.byref(used)))
+    return [int(out[i]) for i in range(len(mods))], int(used.value)
 
 
 def hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed=0.0, granule=128, chunk_bytes=16 << 20) -> Plan:

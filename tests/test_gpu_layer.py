@@ -172,7 +172,8 @@ def test_mirrored_glue_bit_exact(B, r, alpha, ln):
             torch.cuda.synchronize()
             st = c.hg_stats()
             if mirror:
-                assert st.mirror_linears == 12 and st.mirror_mismatch == 0, (st.mirror_linears, st.mirror_mismatch)
+                expect = 12 if alpha < 1.0 else 0  # no CPU rows at alpha = 1: nothing to mirror
+                assert st.mirror_linears == expect and st.mirror_mismatch == 0, (st.mirror_linears, st.mirror_mismatch)
             else:
                 assert st.mirror_linears == 0
             outs[mirror] = bits(h)
@@ -189,3 +190,41 @@ def test_mirror_falls_back_without_host_bias():
         c.hg_layer(L, h, B)
         torch.cuda.synchronize()
         assert c.hg_stats().mirror_linears == 0
+
+
+def test_mirrored_glue_mixed_residency():
+    """Scheduler-style placement: some linears fully GPU-resident (no CPU rows), others split.  The
+    host catches up on the glue of the resident ones lazily; activations stay bit-exact and the
+    output equals the GPU-only glue path's."""
+    H, F, B = 512, 2048, 2
+    shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+    resident = [{"qkv", "o"}, {"qkv", "o", "fc1"}, set(), {"fc2"}, {"qkv", "o", "fc1", "fc2"}, {"o"}]
+    outs = {}
+    for mirror in (1, 0):
+        with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=4096, max_n=8192,
+                        mirror_glue=mirror, verify_mirror=mirror) as c:
+            keep, layers = [], []
+            for l, res in enumerate(resident):
+                descs = []
+                for name in NAMES:
+                    N, K = shapes[name]
+                    _, W, b = gen.linear_inputs(41, l, name, 1, N, K)
+                    n_res = N if name in res else 0
+                    p = c.plan(hg.make_rates(1, 1, 1), N, K, B, n_res, hg.FIXED, 0.4)
+                    W_dev = dev(W[:n_res]) if n_res else None
+                    W_host = pinned(W[n_res:]) if n_res < N else None
+                    bias, bias_h = dev_f32(b), torch.from_numpy(np.ascontiguousarray(b, np.float32))
+                    keep += [W_dev, W_host, bias, bias_h]
+                    descs.append(hg.linear_desc(p, W_dev, W_host, bias, bias_h))
+                layers.append(hg.opt_layer(H, F, descs))
+            h0 = gen.uniform_bf16(11, 993, B * H, 1.0).reshape(B, H)
+            for rep in range(2):
+                h = dev(h0)
+                c.hg_stack(layers, h, B)
+                torch.cuda.synchronize()
+            st = c.hg_stats()
+            if mirror:
+                cpu_linears = sum(1 for res in resident for name in NAMES if name not in res)
+                assert st.mirror_linears == 2 * cpu_linears and st.mirror_mismatch == 0
+            outs[mirror] = bits(h)
+    assert np.array_equal(outs[0], outs[1])
