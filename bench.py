@@ -31,12 +31,29 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# OPT decoder dimensions (hidden, ffn, layers) and BASELINE.json config index (seed offset)
+MODELS = {"opt-6.7b": (4096, 16384, 32, 1), "opt-13b": (5120, 20480, 40, 2), "opt-30b": (7168, 28672, 48, 3),
+          "opt-66b": (9216, 36864, 64, 3)}
+MODEL = "opt-30b"
 H, F, LAYERS = 7168, 28672, 48
 SHAPES = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
 NAMES = ("qkv", "o", "fc1", "fc2")
 STACK_BYTES = LAYERS * sum(2 * n * k for n, k in SHAPES.values())  # 59,190,018,048
 METRIC = "ms/token offloaded OPT-30B decode linears; HBM & H2D GB/s vs roofline"
 SEED = 1164 + 3  # base seed + config index (BJ:10 is configs[3])
+
+
+def set_model(name):
+    """Select the OPT shape the stack is built from (default opt-30b: the headline, BJ:10)."""
+    global MODEL, H, F, LAYERS, SHAPES, STACK_BYTES, METRIC, SEED
+    H, F, LAYERS, cfg = MODELS[name]
+    MODEL = name
+    SHAPES = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+    STACK_BYTES = LAYERS * sum(2 * n * k for n, k in SHAPES.values())
+    METRIC = "ms/token offloaded %s decode linears; HBM & H2D GB/s vs roofline" % name.upper().replace("OPT-", "OPT-")
+    if name == "opt-30b":
+        METRIC = "ms/token offloaded OPT-30B decode linears; HBM & H2D GB/s vs roofline"
+    SEED = 1164 + cfg
 
 
 def env_rank():
@@ -127,11 +144,13 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": ms_tok, "unit": "ms/token", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_tok, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "OPT-30B 48-layer decode linear stack (bounded sample: layer 0's 4 linears x48)",
+        "config": {"workload": "%s %d-layer decode linear stack (qkv,o,fc1,fc2 x%d), batch %d" % (
+                       MODEL.upper(), LAYERS, LAYERS, args.batch), "model": MODEL,
+                   "sample": "layer 0's 4 linears per step, scaled x%d" % LAYERS,
                    "batch": args.batch, "hidden": H, "ffn": F, "layers": LAYERS},
         "cpu_baseline": {"value": ms_tok, "unit": "ms/token", "cores": nthr, "kind": "oracle",
-                         "sample": "one layer (qkv,o,fc1,fc2: 1.233 GB of weights) per step, fp64 naive C "
-                                   "loops, scaled x48 to a token"},
+                         "sample": "one layer (qkv,o,fc1,fc2: %.3f GB of weights) per step, fp64 naive C "
+                                   "loops, scaled x%d to a token" % (STACK_BYTES / LAYERS / 1e9, LAYERS)},
         "e2e": {"value": ms_tok, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -484,7 +503,9 @@ def run_point(st, args, budget_gb=0.0):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_tok, 3),
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded counter-based generator; random-init OPT-30B-shaped weights)",
-        "config": {"workload": "OPT-30B 48-layer decode linear stack (qkv,o,fc1,fc2 x48), batch %d" % B,
+        "config": {"workload": "%s %d-layer decode linear stack (qkv,o,fc1,fc2 x%d), batch %d" % (
+                       MODEL.upper().replace("OPT-", "OPT-"), args.layers, args.layers, B),
+                   "model": MODEL,
                    "batch": B, "hidden": H, "ffn": F, "layers": args.layers,
                    "r_resident": round(plan_tot["bytes_res"] / shard_bytes, 4),
                    "hbm_budget_GB": budget_gb,
@@ -533,8 +554,8 @@ def main_arm(args):
         ts, nthr = oracle_layer_sample(reps=2, batch=st["B"])
         line["cpu_baseline"] = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr,
                                 "kind": "oracle",
-                                "sample": "layer 0's four linears (1.233 GB), fp64 naive C loops on all host "
-                                          "cores, best of 2, scaled x48 to a token"}
+                                "sample": "layer 0's four linears (%.3f GB), fp64 naive C loops on all host "
+                                          "cores, best of 2, scaled x%d to a token" % (STACK_BYTES / LAYERS / 1e9, LAYERS)}
     if rank == 0:
         print(json.dumps(line), flush=True)
     st["ctx"].close()
@@ -550,7 +571,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--layers", type=int, default=LAYERS, help="(development only; the metric needs 48)")
+    ap.add_argument("--model", default="opt-30b", choices=sorted(MODELS),
+                    help="OPT shape (default opt-30b, the headline; opt-6.7b = C2, opt-13b = C3)")
+    ap.add_argument("--layers", type=int, default=None, help="(development only; the metric needs all layers)")
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--chunk-mb", type=int, default=32)
     ap.add_argument("--ring-mb", type=int, default=4096)
@@ -562,6 +585,9 @@ def main():
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
     args = ap.parse_args()
+    set_model(args.model)
+    if args.layers is None:
+        args.layers = LAYERS
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":

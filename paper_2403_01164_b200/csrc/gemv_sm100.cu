@@ -56,7 +56,7 @@ template <> struct Cfg<5> { static constexpr int R = 4, S = 4, W = 4, PART = 409
 template <> struct Cfg<6> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <> struct Cfg<7> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <> struct Cfg<8> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
-template <int B> constexpr int threads_for() { return (Cfg<B>::W + 1) * 32; }
+template <int W> constexpr int threads_for() { return (W + 1) * 32; }
 
 inline int part_max(int B) { return B <= 1 ? 8192 : 4096; }
 
@@ -221,9 +221,8 @@ __device__ void signal_consumed(const SArgs &a, int64_t slot, uint32_t tag) {
     }
 }
 
-template <int B>
-__global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const __grid_constant__ SArgs a) {
-    constexpr int R = Cfg<B>::R, S = Cfg<B>::S, kConsumerWarps = Cfg<B>::W;
+template <int B, int R, int S, int kConsumerWarps>
+__global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_kernel(const __grid_constant__ SArgs a) {
     static_assert(S % kConsumerWarps == 0, "stage count must be a multiple of the consumer warps");
     extern __shared__ __align__(128) uint8_t smem[];
     const int64_t kvmax = a.len >> 3;            // vectors per (full) part
@@ -421,9 +420,9 @@ __global__ void __launch_bounds__(threads_for<B>(), 1) gemv_stream_kernel(const 
     }
 }
 
-template <int B>
+template <int B, int R, int S>
 constexpr size_t smem_bytes_for(int64_t len) {
-    return 128 + (size_t)Cfg<B>::S * Cfg<B>::R * len * 2 + (size_t)B * len * 2;
+    return 128 + (size_t)S * R * len * 2 + (size_t)B * len * 2;
 }
 
 // ---------------------------------------------------------------- read-BW probe
@@ -447,30 +446,44 @@ __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float 
 
 int g_sms = 148;
 
-template <int B>
-int launch_b(const SArgs &a, cudaStream_t st) {
+template <int B, int R, int S, int W>
+int launch_v(const SArgs &a, cudaStream_t st) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.P * a.gp));
-    cfg.blockDim = dim3(threads_for<B>());
-    cfg.dynamicSmemBytes = smem_bytes_for<B>(a.len);
+    cfg.blockDim = dim3(threads_for<W>());
+    cfg.dynamicSmemBytes = smem_bytes_for<B, R, S>(a.len);
     cfg.stream = st;
     // With tags every CTA must be resident at once: a chunk's slot is only refilled after all
-    // CTAs drained its previous occupant (one CTA per SM; cooperative launch guarantees it).
+    // CTAs drained its previous occupant (cooperative launch guarantees co-residency).
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeCooperative;
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = (a.arrived || a.P > 1) ? 1 : 0;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B>, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B, R, S, W>, a);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
 
+template <int B, int R, int S, int W>
+int prepare_v(int64_t part) {
+    return (int)cudaFuncSetAttribute(gemv_stream_kernel<B, R, S, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem_bytes_for<B, R, S>(part));
+}
+
+template <int B>
+int launch_b(const SArgs &a, cudaStream_t st) {
+    return launch_v<B, Cfg<B>::R, Cfg<B>::S, Cfg<B>::W>(a, st);
+}
+
 template <int B>
 int prepare_b() {
-    return (int)cudaFuncSetAttribute(gemv_stream_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem_bytes_for<B>(Cfg<B>::PART));
+    return prepare_v<B, Cfg<B>::R, Cfg<B>::S, Cfg<B>::W>(Cfg<B>::PART);
 }
+
+// CTAs per SM for B = 1 (A/B switch HG_GEMV_CPS): 1 = Cfg<1> (8 stages, 8 consumer warps);
+// 2 or 3 = smaller CTAs (4 stages, 4 consumer warps, ~70 KB smem) sharing each SM.
+int g_cps1 = 1;
 
 }  // namespace
 
@@ -523,7 +536,8 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.K = L.K;
     a.len = g.ks;
     a.P = g.s;
-    a.gp = g_sms / a.P;
+    const int cps = (L.batch == 1) ? g_cps1 : 1;
+    a.gp = cps * g_sms / a.P;
     if (a.gp < 1) return (int)cudaErrorInvalidValue;
     a.W_res = (const uint8_t *)L.W_res;
     a.n_res = L.n_res;
@@ -548,7 +562,7 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
     switch (L.batch) {
-        case 1: return launch_b<1>(a, st);
+        case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
         case 3: return launch_b<3>(a, st);
         case 4: return launch_b<4>(a, st);
@@ -586,6 +600,8 @@ int gemv_prepare() {
     cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     int e = 0;
     e |= prepare_b<1>();
+    e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
+    if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     e |= prepare_b<2>();
     e |= prepare_b<3>();
     e |= prepare_b<4>();

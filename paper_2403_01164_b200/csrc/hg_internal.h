@@ -95,7 +95,9 @@ host_rows_fn host_rows_select(const char **name);
 uint64_t host_read_avx512(const void *p, int64_t bytes);
 
 // ---------------------------------------------------------------- host_glue.cpp
-// Bit-exact host mirrors of the glue_sm100.cu kernels (bf16 = uint16 bit patterns).
+// Bit-exact host mirrors of the glue_sm100.cu kernels (bf16 = uint16 bit patterns).  Built with
+// AVX2+FMA: hglue_supported() must be true before any of them is called.
+bool hglue_supported();
 void hglue_layernorm(const uint16_t *h, int64_t H, int batch, const float *g, const float *b, uint16_t *out);
 void hglue_residual_ln(const uint16_t *h, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *h1,
                        const float *g, const float *b, uint16_t *a2);

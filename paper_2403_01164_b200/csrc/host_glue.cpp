@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <vector>
 
 #include "hg_internal.h"
 
@@ -32,13 +33,12 @@ inline float bf2f(uint16_t v) {
     return f;
 }
 
-// __float2bfloat16_rn: round to nearest even; NaN -> canonical 0x7FFF
+// __float2bfloat16_rn: round to nearest even; NaN -> canonical 0x7FFF (branch-free: vectorises)
 inline uint16_t f2bf(float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
-    if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fff;
-    u += 0x7fffu + ((u >> 16) & 1u);
-    return (uint16_t)(u >> 16);
+    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    return (u & 0x7fffffffu) > 0x7f800000u ? (uint16_t)0x7fff : (uint16_t)r;
 }
 
 // glue_sm100.cu block_sum: per-thread partials -> xor butterfly in each warp (all lanes equal) ->
@@ -65,48 +65,62 @@ float block_sum(const float (&part)[kThreads]) {
     return t[0];
 }
 
-template <typename Get>
-void layernorm_row(Get get, int64_t H, const float *g, const float *b, uint16_t *out) {
-    float part[kThreads];
-    for (int t = 0; t < kThreads; ++t) {
-        float s = 0.f;
-        for (int64_t i = t; i < H; i += kThreads) s = s + get(i);
-        part[t] = s;
-    }
+// LayerNorm of one fp32 row.  Thread t of the GPU kernel accumulates elements t, t+256, ... in
+// ascending order; here the same 256 accumulators advance together (k outer, t inner), which
+// keeps each accumulator's order and lets the compiler vectorise across t.
+void layernorm_row(const float *v, int64_t H, const float *g, const float *b, uint16_t *out) {
+    alignas(64) float part[kThreads];
+    const int64_t full = H / kThreads * kThreads;
+    for (int t = 0; t < kThreads; ++t) part[t] = 0.f;
+    for (int64_t k = 0; k < full; k += kThreads)
+        for (int t = 0; t < kThreads; ++t) part[t] = part[t] + v[k + t];
+    for (int64_t t = 0; t < H - full; ++t) part[t] = part[t] + v[full + t];
     const float mean = block_sum(part) / (float)H;
-    for (int t = 0; t < kThreads; ++t) {
-        float q = 0.f;
-        for (int64_t i = t; i < H; i += kThreads) {
-            const float d = get(i) - mean;
-            q = std::fma(d, d, q);
+    for (int t = 0; t < kThreads; ++t) part[t] = 0.f;
+    for (int64_t k = 0; k < full; k += kThreads)
+        for (int t = 0; t < kThreads; ++t) {
+            const float d = v[k + t] - mean;
+            part[t] = std::fma(d, d, part[t]);
         }
-        part[t] = q;
+    for (int64_t t = 0; t < H - full; ++t) {
+        const float d = v[full + t] - mean;
+        part[t] = std::fma(d, d, part[t]);
     }
     const float var = block_sum(part) / (float)H;
     const float rstd = 1.0f / std::sqrt(var + kLnEps);
-    for (int64_t i = 0; i < H; ++i) {
-        float v = (get(i) - mean) * rstd;
-        if (g) v = v * g[i];
-        if (b) v = v + b[i];
-        out[i] = f2bf(v);
+    if (g && b) {
+        for (int64_t i = 0; i < H; ++i) out[i] = f2bf(((v[i] - mean) * rstd) * g[i] + b[i]);
+    } else {
+        for (int64_t i = 0; i < H; ++i) {
+            float x = (v[i] - mean) * rstd;
+            if (g) x = x * g[i];
+            if (b) x = x + b[i];
+            out[i] = f2bf(x);
+        }
     }
 }
 
+thread_local std::vector<float> t_row;
+
 }  // namespace
 
+bool hglue_supported() { return __builtin_cpu_supports("avx2") && __builtin_cpu_supports("fma"); }
+
 void hglue_layernorm(const uint16_t *h, int64_t H, int batch, const float *g, const float *b, uint16_t *out) {
+    t_row.resize((size_t)H);
     for (int r = 0; r < batch; ++r) {
-        const uint16_t *row = h + r * H;
-        layernorm_row([&](int64_t i) { return bf2f(row[i]); }, H, g, b, out + r * H);
+        for (int64_t i = 0; i < H; ++i) t_row[i] = bf2f(h[r * H + i]);
+        layernorm_row(t_row.data(), H, g, b, out + r * H);
     }
 }
 
 void hglue_residual_ln(const uint16_t *h, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *h1,
                        const float *g, const float *b, uint16_t *a2) {
+    t_row.resize((size_t)H);
     for (int r = 0; r < batch; ++r) {
         for (int64_t i = 0; i < H; ++i) h1[r * H + i] = f2bf(bf2f(h[r * H + i]) + y[r * ldy + i]);
-        const uint16_t *row = h1 + r * H;
-        layernorm_row([&](int64_t i) { return bf2f(row[i]); }, H, g, b, a2 + r * H);
+        for (int64_t i = 0; i < H; ++i) t_row[i] = bf2f(h1[r * H + i]);
+        layernorm_row(t_row.data(), H, g, b, a2 + r * H);
     }
 }
 

@@ -790,7 +790,7 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
 
 // ---------------------------------------------------------------- mirrored glue (reading R24)
 bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n, hg_layer_trace *tr) {
-    if (!c->cfg.mirror_glue || tr || dist_nranks(c->dist) != 1) return false;
+    if (!c->cfg.mirror_glue || tr || dist_nranks(c->dist) != 1 || !hglue_supported()) return false;
     bool any_cpu = false;  // without CPU rows nobody needs the glue on the host
     for (int l = 0; l < n; ++l)
         for (int i = 0; i < 4; ++i) any_cpu |= layers[l].lin[i].plan.n_cpu > 0;

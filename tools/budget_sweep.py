@@ -23,7 +23,8 @@ def main():
     ap.add_argument("--steps", type=int, default=8)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--batch", type=int, default=1)
-    ap.add_argument("--layers", type=int, default=bench.LAYERS)
+    ap.add_argument("--model", default="opt-30b", choices=sorted(bench.MODELS))
+    ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--alpha", type=float, default=None)
     ap.add_argument("--chunk-mb", type=int, default=32)
     ap.add_argument("--ring-mb", type=int, default=4096)
@@ -33,6 +34,9 @@ def main():
     ap.add_argument("--abench-gamma", type=float, default=0.06)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
+    bench.set_model(args.model)
+    if args.layers is None:
+        args.layers = bench.LAYERS
     args.warmup = max(args.warmup, 3)
     st = bench.prepare(args)
     rows = []

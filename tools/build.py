@@ -61,7 +61,7 @@ PRODUCT_SOURCES = [
     ("host_gemv.cpp", "cxx_avx512"),
     ("host_gemv_avx2.cpp", "cxx_avx2"),
     ("threadpool.cpp", "cxx"),
-    ("host_glue.cpp", "cxx"),
+    ("host_glue.cpp", "cxx_avx2"),
     ("gemv_sm100.cu", "cu"),
     ("gemv_tc_sm100.cu", "cu"),
     ("glue_sm100.cu", "cu"),
