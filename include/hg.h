@@ -158,7 +158,8 @@ typedef struct {
 typedef struct {
     double wall_s;          /* host wall time of the call (enqueue to GPU completion)   */
     double cpu_busy_s;      /* host GEMV time (sum over linears)                        */
-    double link_busy_s;     /* H2D chunk copy time (collect_stats=1)                    */
+    double link_busy_s;     /* link time of the calls' streamed bytes: bytes_str at the copy
+                               rate measured in the window (collect_stats=1)              */
     double gpu_busy_s;      /* GEMV kernel time, resident + streamed (collect_stats=1)  */
     double x_wait_s;        /* host time waiting for activations to reach the host     */
     double glue_s;          /* host time in the mirrored glue (critical path, per call)   */

@@ -197,6 +197,7 @@ struct hg_ctx {
     std::vector<cudaEvent_t> tev;
     size_t tev_used = 0;
     std::vector<std::pair<size_t, size_t>> copy_ev, gemv_ev;
+    std::vector<int64_t> copy_bytes;  // bytes of each timed chunk copy (copy_ev order)
     cudaEvent_t ev_call0 = nullptr, ev_call1 = nullptr;
     bool call_timed = false;
     bool stats_open = false;  // ev_call0 recorded since the last reset
@@ -337,6 +338,7 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
         if (e1) {
             HG_CK(c, cudaEventRecord(e1, c->copy));
             c->copy_ev.push_back({i0, i1});
+            c->copy_bytes.push_back(r.bytes);
         }
     }
     c->slot_used[slot] = 1;
@@ -1356,11 +1358,22 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
                 const double t1 = std::min(std::max(b * 1e-3, 0.0), wall);
                 return t1 > t0 ? t1 - t0 : 0.0;
             };
-            double link = 0, gpu = 0;
-            for (auto &pr : c->copy_ev) link += clipped(pr);
+            // Link time of these calls = the bytes they streamed at the link's measured copy rate.
+            // (Busy time inside the window is not it: with a ring larger than a call's streamed
+            // bytes the copy stream keeps prefetching later calls' chunks the whole time.)
+            double dur = 0, bytes = 0, gpu = 0;
+            for (size_t k = 0; k < c->copy_ev.size(); ++k) {
+                const double d = clipped(c->copy_ev[k]);
+                float full = 0;
+                if (d > 0 && cudaEventElapsedTime(&full, c->tev[c->copy_ev[k].first], c->tev[c->copy_ev[k].second]) ==
+                                 cudaSuccess && full > 0) {
+                    dur += d;
+                    bytes += (double)c->copy_bytes[k] * d / (full * 1e-3);
+                }
+            }
             for (auto &pr : c->gemv_ev) gpu += clipped(pr);
             cudaGetLastError();
-            c->st.link_busy_s = link;
+            c->st.link_busy_s = (bytes > 0 && dur > 0) ? (double)c->st.bytes_str / (bytes / dur) : 0.0;
             c->st.gpu_busy_s = gpu;
         }
     }
@@ -1377,6 +1390,7 @@ HG_API hg_status hg_reset_stats(hg_ctx *c) {
     }
     c->tev_used = 0;
     c->copy_ev.clear();
+    c->copy_bytes.clear();
     c->gemv_ev.clear();
     c->stats_open = false;
     c->call_timed = false;
@@ -1527,6 +1541,10 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     // short runs: single runs on a shared host are noisy.
     std::vector<uint16_t> xh((size_t)batch * K, 0x3f80);
     std::vector<float> yh((size_t)batch * N);
+    // A weight that is not much larger than the host's last-level cache would be measured from
+    // cache: every timed CPU probe is preceded by a read of a 256 MiB scratch buffer.
+    const int64_t sbytes = 256ll << 20;
+    std::vector<uint8_t> scratch((size_t)sbytes, 1);
     const int NB = (flags & 1) ? 192 : 0;  // 192 chunks ~ 6 GiB ~ 110 ms of link time
     std::vector<cudaEvent_t> evb((size_t)NB, nullptr);
     for (int i = 0; i < NB; ++i) HG_CK(c, cudaEventCreateWithFlags(&evb[i], cudaEventDisableTiming));
@@ -1542,10 +1560,10 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     };
     struct RJ { const uint8_t *p; int64_t bytes, block; std::atomic<int64_t> next; std::atomic<uint64_t> sum; };
     RJ rj;
-    rj.p = src;
-    rj.bytes = wbytes;
     rj.block = 1 << 20;
-    auto read_pass = [&]() {
+    auto read_region = [&](const uint8_t *p, int64_t bytes) {
+        rj.p = p;
+        rj.bytes = bytes;
         rj.next.store(0);
         rj.sum.store(0);
         pool_run(c->pool, [](void *a, int) {
@@ -1562,6 +1580,8 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
             r->sum.fetch_xor(s);
         }, &rj);
     };
+    auto flush_llc = [&]() { read_region(scratch.data(), sbytes); };
+    auto read_pass = [&]() { read_region(src, wbytes); };
     auto median = [](std::vector<double> v) {
         std::sort(v.begin(), v.end());
         return v[v.size() / 2];
@@ -1572,25 +1592,28 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
         for (int w = 0; w < 3; ++w) {
             const int n0 = completed();
             const auto t0 = clk::now();
-            int passes = 0;
-            while (secs(t0, clk::now()) < 0.02) {
+            int64_t cpu_bytes = 0;
+            while (secs(t0, clk::now()) < 0.02) {  // weight + scratch: a footprint far above the LLC
                 read_pass();
-                ++passes;
+                flush_llc();
+                cpu_bytes += wbytes + sbytes;
             }
             const int n1 = completed();
             const double dt = secs(t0, clk::now());
             if (n1 < NB && n1 > n0)
-                out->b_host = std::max(out->b_host, ((double)passes * wbytes + (double)(n1 - n0) * chunk) / dt);
+                out->b_host = std::max(out->b_host, ((double)cpu_bytes + (double)(n1 - n0) * chunk) / dt);
         }
     }
     std::vector<double> tg, tr;
     for (int it = 0; it < 9; ++it) {
+        flush_llc();
         auto t0 = clk::now();
         HG_TRY(hg_host_gemv(c, xh.data(), batch, N, K, W_host, nullptr, yh.data()));
         tg.push_back(secs(t0, clk::now()));
     }
     out->v_cpu = (double)wbytes / median(tg);
     for (int it = 0; it < 9; ++it) {
+        flush_llc();
         auto t0 = clk::now();
         read_pass();
         tr.push_back(secs(t0, clk::now()));
