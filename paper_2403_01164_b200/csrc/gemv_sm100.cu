@@ -43,6 +43,15 @@
 namespace hg {
 namespace {
 
+// Named barrier among a subset of warps.  PTX bar.sync is barrier.sync.aligned, which requires the
+// whole warp to execute it convergently; call sites follow lane-divergent code (a lane-0-only grid
+// barrier, loops with lane-dependent trip counts), so reconverge first and use the non-aligned form.
+__device__ __forceinline__ void named_barrier(int id, int nthreads) {
+    __syncwarp();
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+
 // Per-batch configuration: rows per stage R (x reuse across rows), stages S, consumer warps W,
 // max part length.  S must be a multiple of W: consumer warp w takes the groups it = w (mod W),
 // so it only ever waits for the phase right after the one it consumed itself from the same
@@ -57,6 +66,8 @@ template <> struct Cfg<6> { static constexpr int R = 4, S = 4, W = 4, PART = 409
 template <> struct Cfg<7> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <> struct Cfg<8> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <int W> constexpr int threads_for() { return (W + 1) * 32; }
+// Shared memory: [full[S] empty[S] mbarriers, padded to 128 B][S stages of R rows][x part]
+template <int S> __host__ __device__ constexpr int bars_bytes() { return (2 * S * 8 + 127) / 128 * 128; }
 
 inline int part_max(int B) { return B <= 1 ? 8192 : 4096; }
 
@@ -80,6 +91,8 @@ struct SArgs {
     float *ws;
     uint32_t *gbar;  // [2]: arrival count, generation (grid barrier for P > 1)
     uint32_t *err;
+    volatile uint32_t *trace;  // debug (HG_SYNC_DEBUG=3): mapped host words, see runtime.cu
+    uint32_t trace_id;
     unsigned long long timeout_ns;
 };
 
@@ -228,7 +241,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     const int64_t kvmax = a.len >> 3;            // vectors per (full) part
     const int64_t unit_bytes = a.len * 2;        // stage slot per row
     uint64_t *bars = (uint64_t *)smem;           // full[S], empty[S]
-    uint8_t *stages = smem + 128;                // S * R * unit_bytes
+    uint8_t *stages = smem + bars_bytes<S>();    // S * R * unit_bytes
     uint4 *xs = (uint4 *)(stages + (int64_t)S * R * unit_bytes);  // [B][kvmax]
     const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
     const uint32_t stage0 = smem_u32(stages);
@@ -258,9 +271,13 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
             const int64_t b = i / kv, v = i - b * kv;
             xs[b * kvmax + v] = xg[b * Kv + (k0 >> 3) + v];
         }
-        asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
+        named_barrier(1, kConsumerThreads);
     }
 
+    if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {  // debug trace (mapped host memory)
+        a.trace[1] = a.trace_id;
+        __threadfence_system();
+    }
     const int64_t s_begin = a.n_res > 0 ? -1 : 0;
     if (warp == kConsumerWarps) {
         // ------------------------------------------------------------ producer
@@ -403,11 +420,15 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
                         a.ws[((src.g0 + r + q) * a.P + p) * B + b] = acc[q][b];
         }
     }
+    if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
+        a.trace[2] = a.trace_id;  // CTA 0 past its groups
+        __threadfence_system();
+    }
     if (a.P == 1) return;
     // ---------------------------------------------------------------- P > 1: parts -> y
-    asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
+    named_barrier(1, kConsumerThreads);
     if (threadIdx.x == 0) grid_barrier(a);
-    asm volatile("bar.sync 1, %0;" ::"r"(kConsumerThreads) : "memory");
+    named_barrier(1, kConsumerThreads);
     const int64_t n = a.n_res + a.n_str;
     const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
     for (int64_t i = threadIdx.x; i < (r1 - r0) * B; i += kConsumerThreads) {
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
 
 template <int B, int R, int S>
 constexpr size_t smem_bytes_for(int64_t len) {
-    return 128 + (size_t)S * R * len * 2 + (size_t)B * len * 2;
+    return (size_t)bars_bytes<S>() + (size_t)S * R * len * 2 + (size_t)B * len * 2;
 }
 
 // ---------------------------------------------------------------- read-BW probe
@@ -484,6 +505,7 @@ int prepare_b() {
 // CTAs per SM for B = 1 (A/B switch HG_GEMV_CPS): 1 = Cfg<1> (8 stages, 8 consumer warps);
 // 2 or 3 = smaller CTAs (4 stages, 4 consumer warps, ~70 KB smem) sharing each SM.
 int g_cps1 = 1;
+int g_b34 = 0;  // A/B (HG_GEMV_B34): B = 3, 4 kernel shape 0 = Cfg (R2,S10,W10), 1 = (R2,S8,W8), 2 = (R4,S4,W4)
 
 }  // namespace
 
@@ -557,6 +579,8 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.ws = L.ws;
     a.gbar = L.gbar;
     a.err = L.err;
+    a.trace = L.trace;
+    a.trace_id = L.trace_id;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
     if (a.P > 1 && (!a.ws || !a.gbar || !a.err)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
@@ -564,8 +588,10 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     switch (L.batch) {
         case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
-        case 3: return launch_b<3>(a, st);
-        case 4: return launch_b<4>(a, st);
+        case 3:
+            return g_b34 == 1 ? launch_v<3, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<3, 4, 4, 4>(a, st) : launch_b<3>(a, st);
+        case 4:
+            return g_b34 == 1 ? launch_v<4, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<4, 4, 4, 4>(a, st) : launch_b<4>(a, st);
         case 5: return launch_b<5>(a, st);
         case 6: return launch_b<6>(a, st);
         case 7: return launch_b<7>(a, st);
@@ -601,6 +627,11 @@ int gemv_prepare() {
     int e = 0;
     e |= prepare_b<1>();
     e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
+    e |= prepare_v<3, 2, 8, 8>(4096);
+    e |= prepare_v<3, 4, 4, 4>(4096);
+    e |= prepare_v<4, 2, 8, 8>(4096);
+    e |= prepare_v<4, 4, 4, 4>(4096);
+    if (const char *v = getenv("HG_GEMV_B34")) g_b34 = atoi(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     e |= prepare_b<2>();
     e |= prepare_b<3>();

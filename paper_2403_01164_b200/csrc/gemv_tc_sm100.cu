@@ -33,6 +33,15 @@
 namespace hg {
 namespace {
 
+// Named barrier among a subset of warps.  PTX bar.sync is barrier.sync.aligned, which requires the
+// whole warp to execute it convergently; call sites follow lane-divergent code (a lane-0-only grid
+// barrier, loops with lane-dependent trip counts), so reconverge first and use the non-aligned form.
+__device__ __forceinline__ void named_barrier(int id, int nthreads) {
+    __syncwarp();
+    asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+
 constexpr int kTileM = 128;        // W rows per tile (UMMA M)
 constexpr int kTileK = 64;         // k per stage (one 128-byte swizzle atom of bf16)
 constexpr int kUmmaN = 16;         // batch padded to N = 16
@@ -258,9 +267,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int b = 0; b < B; ++b) ws[((int64_t)s * B + b) * n + row] = __uint_as_float(r[b]);
             }
             __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            named_barrier(1, 128);
             if (et == 0) *last_flag = (atomicAdd(&counters[tile], 1) == U.S - 1);
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            named_barrier(1, 128);
             if (*last_flag) {
                 __threadfence();
                 if (row < n) {
@@ -282,7 +291,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 if (et == 0) counters[tile] = 0;
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            named_barrier(1, 128);
         }
     }
     tc_fence_before();

@@ -62,6 +62,8 @@ struct StreamLaunch {
     uint32_t *gbar;
     uint32_t *err;
     double timeout_s;
+    volatile uint32_t *trace = nullptr;  // debug trace words (mapped host) or NULL
+    uint32_t trace_id = 0;
 };
 int launch_gemv_stream(const StreamLaunch &L, void *stream);
 

@@ -172,6 +172,10 @@ struct hg_ctx {
     float *ymap[kMirrorRing] = {};
     cudaEvent_t ev_g[kMirrorRing] = {}, ev_yg[kMirrorRing] = {}, ev_use[kMirrorRing] = {};
     cudaStream_t d2h = nullptr;                    // side stream for the GPU rows' D2H
+    uint32_t *trace = nullptr;                     // HG_SYNC_DEBUG=3: mapped host trace words
+    uint64_t trace_seq = 0;
+    struct TraceLin { uint32_t id; int64_t seq0, n_chunks, n_res, n_str, K; };
+    std::vector<TraceLin> trace_lin;
     cudaStream_t last_stream = nullptr;
     bool have_last = false;
 
@@ -249,6 +253,29 @@ hg_status kerr(hg_ctx *c, int e, const char *what) {
         return set_error(HG_ECUDA, "%s: %s", what, cudaGetErrorString((cudaError_t)e));
     }
     return HG_OK;
+}
+
+// HG_SYNC_DEBUG=3: GEMV launches record their id and CTA progress in mapped host words.
+volatile uint32_t *dbg_trace(hg_ctx *c) {
+    static const int mode = getenv("HG_SYNC_DEBUG") ? atoi(getenv("HG_SYNC_DEBUG")) : 0;
+    if (mode != 3) return nullptr;
+    if (!c->trace) {
+        if (cudaHostAlloc((void **)&c->trace, 64, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+        std::memset(c->trace, 0, 64);
+    }
+    return c->trace;
+}
+
+void dbg_trace_report(hg_ctx *c) {
+    if (!c->trace) return;
+    const uint32_t id = c->trace[1], ctas_done = c->trace[2];
+    fprintf(stderr, "hg trace: last GEMV started id=%u, last past its groups (CTA 0) id=%u, launches=%zu\n", id,
+            ctas_done, c->trace_lin.size());
+    for (const auto &t : c->trace_lin)
+        if (t.id + 3 >= id && t.id <= id + 1)
+            fprintf(stderr, "  id %u: seq0=%lld n_chunks=%lld n_res=%lld n_str=%lld K=%lld (slots %lld..)\n", t.id,
+                    (long long)t.seq0, (long long)t.n_chunks, (long long)t.n_res, (long long)t.n_str, (long long)t.K,
+                    (long long)(t.seq0 % c->nslots));
 }
 
 // A tag wait inside a kernel that timed out leaves err != 0 (read at synchronising calls).
@@ -527,6 +554,11 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         S.gbar = c->gbar;
         S.err = c->err;
         S.timeout_s = c->cfg.timeout_s;
+        S.trace = dbg_trace(c);
+        S.trace_id = (uint32_t)(c->trace_seq++);
+        if (S.trace) {
+            c->trace_lin.push_back({S.trace_id, (int64_t)seq0, (int64_t)S.n_chunks, p.n_res, p.n_str, p.K});
+        }
         if (n > 0) {
             size_t i0 = 0, i1 = 0;
             cudaEvent_t e0 = nullptr;
@@ -817,6 +849,35 @@ hg_status verify_act(hg_ctx *c, const uint16_t *xh, const void *xd, int64_t n, c
     return HG_OK;
 }
 
+// HG_SYNC_DEBUG=1: synchronise after every GPU step of the mirrored stack and name the one that
+// failed (development aid for asynchronous device faults).
+hg_status dbg_sync(hg_ctx *c, cudaStream_t s, const char *what, int k) {
+    static const int mode = getenv("HG_SYNC_DEBUG") ? atoi(getenv("HG_SYNC_DEBUG")) : 0;
+    if (!mode) return HG_OK;
+    if (mode == 2) {  // no synchronisation: report the first sticky error seen after this step
+        const cudaError_t e = cudaPeekAtLastError();
+        if (e != cudaSuccess) {
+            fprintf(stderr, "hg debug: error seen after %s (linear %d): %s\n", what, k, cudaGetErrorString(e));
+            return set_error(HG_ECUDA, "%s (linear %d): %s", what, k, cudaGetErrorString(e));
+        }
+        const cudaError_t q = cudaStreamQuery(s);
+        if (q != cudaSuccess && q != cudaErrorNotReady) {
+            fprintf(stderr, "hg debug: stream error after %s (linear %d): %s\n", what, k, cudaGetErrorString(q));
+            return set_error(HG_ECUDA, "%s (linear %d): %s", what, k, cudaGetErrorString(q));
+        }
+        return HG_OK;
+    }
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(c->copy);
+    if (e == cudaSuccess && c->d2h) e = cudaStreamSynchronize(c->d2h);
+    if (e != cudaSuccess) {
+        c->error = true;
+        fprintf(stderr, "hg debug: %s (linear %d): %s\n", what, k, cudaGetErrorString(e));
+        return set_error(HG_ECUDA, "%s (linear %d): %s", what, k, cudaGetErrorString(e));
+    }
+    return HG_OK;
+}
+
 hg_status ensure_mirror(hg_ctx *c) {
     if (c->yring) return HG_OK;
     const size_t per = (size_t)HG_MAX_BATCH * c->cfg.max_n;
@@ -911,6 +972,7 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             HG_TRY(kerr(c, launch_relu_bf16(yprev_d, F, B, c->act, s), "relu"));
         }
         c->st.gpu_launches++;
+        HG_TRY(dbg_sync(c, s, "glue", k));
         // ---- this slot's previous occupant (k - R): its D2H must be done before y is overwritten,
         // and the host must have consumed its host copy before the new D2H / CPU rows land there
         if (k >= R) {
@@ -960,11 +1022,13 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             c->st.bytes_cpu += 2 * K * p.n_cpu;
         }
         if (gst != HG_OK) return gst;
+        HG_TRY(dbg_sync(c, s, "gemv + y D2H", k));
         // ---- join: the CPU rows (bias already added on the host) into the ring slot on the device
         if (p.n_cpu > 0) {
             HG_TRY(kerr(c, launch_join(yd, N, n_gpu, p.n_cpu, B, c->ymap[slot] + n_gpu, N,
                                        d.bias_host ? nullptr : d.bias, s), "join"));
             c->st.gpu_launches++;
+            HG_TRY(dbg_sync(c, s, "join", k));
         }
         HG_CK(c, cudaEventRecord(c->ev_use[slot], s));
         c->st.n_linears++;
@@ -1385,6 +1449,7 @@ HG_API hg_status hg_reset_stats(hg_ctx *c) {
     if (!c) return set_error(HG_EINVAL, "NULL ctx");
     if (c->device >= 0 && c->have_last) {  // pending timing events belong to the old window
         HG_CK(c, cudaSetDevice(c->device));
+        if (cudaEventSynchronize(c->ev_done) != cudaSuccess) dbg_trace_report(c);
         HG_CK(c, cudaEventSynchronize(c->ev_done));
         HG_CK(c, cudaStreamSynchronize(c->copy));
     }
@@ -1444,8 +1509,8 @@ HG_API hg_status hg_alpha_bench(hg_ctx *c, const hg_opt_layer *layers, int n_lay
         }
     }
     c->cfg.collect_stats = saved_stats;
-    hg_reset_stats(c);
-    if (st != HG_OK) return st;
+    if (st != HG_OK) return st;  // keep the failing call's message (hg_reset_stats would overwrite it)
+    HG_TRY(hg_reset_stats(c));
     out->n = (int)pts.size();
     return hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, nullptr, out->n, cfg.degree, pts.front(),
                           pts.back(), alpha_seed, &out->alpha_bar, &out->clamped);

@@ -1,6 +1,5 @@
-out=gpurun_out/r01t; mkdir -p $out
-timeout 600 python -m pytest tests/test_gpu_linear.py -q -k "stats or tags" > $out/pytest.txt 2>&1; tail -2 $out/pytest.txt
-for m in opt-6.7b opt-13b opt-30b; do
-  timeout 900 python bench.py --model $m --no-cpu-baseline > $out/bench_$m.json 2> $out/bench_$m.err; echo "$m rc=$?"
-  python -c "import json; d=json.loads(open('$out/bench_$m.json').read().strip().splitlines()[-1]); print('$m', d['value'], d['e2e']['value'], d['config']['alpha'], d['path_roofline']['frac_of_roof_at_plan'], d['rates_GBps'], d['lanes']['busy_frac'], d['alpha_bench']['alpha_bar'], d['alpha_bench']['clamped'])"
-done
+out=gpurun_out/r01z9; mkdir -p $out
+run() { tag=$1; shift; timeout 900 env "$@" > $out/$tag.json 2> $out/$tag.err; rc=$?; echo "$tag rc=$rc $(grep -o 'HgError:.*' $out/$tag.err | head -1 | cut -c1-200) $(grep -o '"value": [0-9.]*' $out/$tag.json | head -1)"; }
+timeout 900 python -m pytest tests -m gpu -x -q > $out/pytest.txt 2>&1; tail -1 $out/pytest.txt
+python tools/microbench.py 2>&1 | head -4
+for i in 1 2; do run b3_$i python bench.py --batch 3 --no-cpu-baseline --no-breakdown --steps 2; run b4_$i python bench.py --batch 4 --no-cpu-baseline --no-breakdown --steps 2; run b2_$i python bench.py --batch 2 --no-cpu-baseline --no-breakdown --steps 2; done
