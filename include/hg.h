@@ -148,6 +148,11 @@ typedef struct {
                             CPU rows) and LN parameters, else the call uses the GPU-only glue      */
     int32_t verify_mirror; /* 1: after every mirrored glue step compare the host activation with
                             the device one (synchronising; tests) -> hg_stats.mirror_mismatch     */
+    int32_t stream_mode; /* how the streamed slice reaches the SMs: 0 (default) = copy-engine chunks
+                            through the device ring; 1 = zero-copy: the GEMV's TMA bulk copies read
+                            the pinned host rows over the link directly (no ring, no tags; SIMT
+                            batches only -- tcgen05 batches keep mode 0)                          */
+    int32_t _pad0;
 } hg_config;
 
 /* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last

@@ -77,6 +77,8 @@ struct SArgs {
     int P, gp;
     const uint8_t *W_res;
     int64_t n_res;
+    const uint8_t *W_dir;  // zero-copy streamed rows (pinned host memory, device-mapped)
+    int64_t n_dir;
     const uint8_t *ring;
     int64_t slot_bytes;
     int64_t nslots;
@@ -104,12 +106,13 @@ struct Src {
     bool flagged;
 };
 
-__device__ __forceinline__ Src source(const SArgs &a, int64_t s) {  // s = -1: resident block
+// s = -2: resident block (HBM), s = -1: zero-copy rows read over the host link, s >= 0: chunk s
+__device__ __forceinline__ Src source(const SArgs &a, int64_t s) {
     Src r;
     if (s < 0) {
-        r.base = a.W_res;
-        r.rows = a.n_res;
-        r.g0 = 0;
+        r.base = s == -2 ? a.W_res : a.W_dir;
+        r.rows = s == -2 ? a.n_res : a.n_dir;
+        r.g0 = s == -2 ? 0 : a.n_res;
         r.slot = -1;
         r.tag = 0;
         r.flagged = false;
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
         a.trace[1] = a.trace_id;
         __threadfence_system();
     }
-    const int64_t s_begin = a.n_res > 0 ? -1 : 0;
+    const int64_t s_begin = a.n_res > 0 ? -2 : (a.n_dir > 0 ? -1 : 0);
     if (warp == kConsumerWarps) {
         // ------------------------------------------------------------ producer
         if (lane != 0) return;
@@ -429,7 +432,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     named_barrier(1, kConsumerThreads);
     if (threadIdx.x == 0) grid_barrier(a);
     named_barrier(1, kConsumerThreads);
-    const int64_t n = a.n_res + a.n_str;
+    const int64_t n = a.n_res + a.n_dir + a.n_str;
     const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
     for (int64_t i = threadIdx.x; i < (r1 - r0) * B; i += kConsumerThreads) {
         const int64_t g = r0 + i / B;
@@ -550,7 +553,7 @@ int64_t gemv_counters(int64_t n, int64_t K, int batch) {
 }
 
 int launch_gemv_stream(const StreamLaunch &L, void *stream) {
-    if (L.n_res + L.n_str <= 0) return 0;
+    if (L.n_res + L.n_str + (L.W_dir ? L.n_dir : 0) <= 0) return 0;
     if (L.batch < 1 || L.batch > HG_MAX_BATCH) return (int)cudaErrorInvalidValue;
     const GemvGeom g = gemv_geom(L.K, L.batch);
     SArgs a;
@@ -563,6 +566,8 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     if (a.gp < 1) return (int)cudaErrorInvalidValue;
     a.W_res = (const uint8_t *)L.W_res;
     a.n_res = L.n_res;
+    a.W_dir = (const uint8_t *)L.W_dir;
+    a.n_dir = L.W_dir ? L.n_dir : 0;
     a.ring = L.ring;
     a.slot_bytes = L.slot_bytes;
     a.nslots = L.nslots > 0 ? L.nslots : 1;

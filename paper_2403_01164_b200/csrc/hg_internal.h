@@ -50,6 +50,8 @@ struct StreamLaunch {
     int64_t K;
     const void *W_res;
     int64_t n_res;
+    const void *W_dir = nullptr;  // zero-copy streamed rows [n_res, n_res + n_dir) (mapped pinned host)
+    int64_t n_dir = 0;
     const uint8_t *ring;
     int64_t slot_bytes, nslots;
     int64_t seq0, n_chunks, chunk_rows, n_str;

@@ -478,6 +478,12 @@ void push_chunks(std::vector<ChunkReq> &v, const hg_plan_t &p, const void *W_hos
 }
 
 void set_future(hg_ctx *c, std::vector<ChunkReq> &&list, bool wrap) {
+    if (c->cfg.stream_mode == 1) {  // zero-copy streaming: nothing for the copy engine
+        c->future.clear();
+        c->fpos = 0;
+        c->fwrap = false;
+        return;
+    }
     if (wrap && c->fwrap && list.size() == c->future.size() &&
         std::equal(list.begin(), list.end(), c->future.begin()))
         return;  // same stack as last call: keep streaming where we are
@@ -521,12 +527,16 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const hg_plan_t &p = L.plan;
     const int B = (int)p.batch;
     const int64_t K = p.K;
-    if (c->tags && !gemv_use_tc(B)) {
+    const bool direct = c->cfg.stream_mode == 1 && !gemv_use_tc(B);
+    if ((c->tags || direct) && !gemv_use_tc(B)) {
         // a3 + a4 in ONE persistent launch: resident rows, then each chunk as its arrival tag lands
+        // (stream_mode 1: the streamed rows are read by the kernel itself over the link, zero-copy)
         std::vector<ChunkReq> mine;
-        push_chunks(mine, p, L.W_host);
         int64_t seq0 = 0;
-        if (p.n_str > 0) HG_TRY(bind_chunks(c, mine, &seq0));
+        if (!direct) {
+            push_chunks(mine, p, L.W_host);
+            if (p.n_str > 0) HG_TRY(bind_chunks(c, mine, &seq0));
+        }
         const int64_t n = p.n_res + p.n_str;
         if (gemv_ws_floats(n, K, B) > c->ws_floats || gemv_counters(n, K, B) > c->n_counters)
             return set_error(HG_EINVAL, "GEMV of %lld rows x K=%lld exceeds the context workspace", (long long)n,
@@ -541,10 +551,19 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         S.slot_bytes = c->slot_bytes;
         S.nslots = c->nslots;
         S.seq0 = seq0;
-        S.n_chunks = p.n_str > 0 ? p.n_chunks : 0;
+        S.n_chunks = (p.n_str > 0 && !direct) ? p.n_chunks : 0;
         S.chunk_rows = p.chunk_rows;
-        S.n_str = p.n_str;
-        S.arrived = c->arrived;
+        S.n_str = direct ? 0 : p.n_str;
+        const void *wdir = nullptr;
+        if (direct && p.n_str > 0) {  // the device address of the pinned host rows (UVA mapping)
+            cudaPointerAttributes at;
+            HG_CK(c, cudaPointerGetAttributes(&at, L.W_host));
+            if (!at.devicePointer) return set_error(HG_ENOTPINNED, "W_host is not mapped into the device address space");
+            wdir = at.devicePointer;
+        }
+        S.W_dir = wdir;
+        S.n_dir = direct ? p.n_str : 0;
+        S.arrived = direct ? nullptr : c->arrived;
         S.consumed = c->consumed;
         S.slot_cnt = c->slot_cnt;
         S.bias = L.bias;
@@ -577,8 +596,8 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         }
         c->st.bytes_res += 2 * K * p.n_res;
         c->st.bytes_str += 2 * K * p.n_str;
-        if (p.n_str > 0) c->st.n_chunks += p.n_chunks;
-        return pump(c);
+        if (p.n_str > 0 && !direct) c->st.n_chunks += p.n_chunks;
+        return direct ? HG_OK : pump(c);
     }
     if (p.n_res > 0) {  // a3
         HG_TRY(gemv(c, L.x, B, K, L.W_dev, p.n_res, L.bias, L.y, L.ldy, s));
@@ -1072,6 +1091,8 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     if (const char *v = getenv("HG_HANDSHAKE")) cfg->handshake = atoi(v);
     cfg->mirror_glue = 1;
     if (const char *v = getenv("HG_MIRROR_GLUE")) cfg->mirror_glue = atoi(v);
+    cfg->stream_mode = 0;
+    if (const char *v = getenv("HG_STREAM_MODE")) cfg->stream_mode = atoi(v);
     cfg->verify_mirror = 0;
     return HG_OK;
 }
@@ -1438,6 +1459,7 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
             for (auto &pr : c->gemv_ev) gpu += clipped(pr);
             cudaGetLastError();
             c->st.link_busy_s = (bytes > 0 && dur > 0) ? (double)c->st.bytes_str / (bytes / dur) : 0.0;
+            if (c->cfg.stream_mode == 1) c->st.link_busy_s = gpu;  // zero-copy: the GEMVs are the transfer
             c->st.gpu_busy_s = gpu;
         }
     }

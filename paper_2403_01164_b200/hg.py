@@ -68,7 +68,8 @@ class Config(ctypes.Structure):
                 ("cpu_first", ctypes.c_int32), ("collect_stats", ctypes.c_int32),
                 ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double),
                 ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32),
-                ("mirror_glue", ctypes.c_int32), ("verify_mirror", ctypes.c_int32)]
+                ("mirror_glue", ctypes.c_int32), ("verify_mirror", ctypes.c_int32),
+                ("stream_mode", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):

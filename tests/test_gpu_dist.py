@@ -1,0 +1,55 @@
+"""a8 plumbing on one GPU: NCCL is loaded, a one-rank communicator is created through
+hg_dist_unique_id / hg_dist_init, and hg_linear_sharded / hg_stack run through it with results
+equal to the unsharded calls (the P > 1 exchange itself is covered on CPU by test_dist_gloo.py
+with the same [P][B][N/P] layout and permutation)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_util import bits, dev, dev_f32, split_weight
+from harness import gen
+from paper_2403_01164_b200 import hg
+
+pytestmark = pytest.mark.gpu
+
+
+def test_one_rank_communicator_linear_and_stack():
+    from test_gpu_layer import make_layer_mirror
+    uid = hg.hg_dist_unique_id()
+    assert len(uid) == 128
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=32 << 20, max_k=4096, max_n=8192) as c:
+        c.hg_dist_init(1, 0, uid)
+        with pytest.raises(hg.HgError):
+            c.hg_dist_init(1, 0, uid)  # once per context
+        x, W, b = gen.linear_inputs(51, 0, "fc1", 2, 2048, 1024)
+        p = c.plan(hg.make_rates(1, 1, 1), 2048, 1024, 2, 256, hg.FIXED, 0.5)
+        Wd, Wh = split_weight(W, 256)
+        y = torch.full((2, 2048), float("nan"), device="cuda")
+        c.hg_linear_sharded(p, dev(x), Wd, Wh, dev_f32(b), y)
+        torch.cuda.synchronize()
+        assert oracle.within_tol(y.cpu().numpy(), oracle.linear(x, W, b))[0]
+        keep = []
+        layers = [make_layer_mirror(c, 256, 1024, 2, layer=l, alpha=0.5, keep=keep) for l in range(2)]
+        h0 = gen.uniform_bf16(12, 992, 2 * 256, 1.0).reshape(2, 256)
+        h_a = dev(h0)
+        c.hg_stack(layers, h_a, 2)
+        torch.cuda.synchronize()
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=32 << 20, max_k=4096, max_n=8192) as c2:
+        keep = []
+        layers = [make_layer_mirror(c2, 256, 1024, 2, layer=l, alpha=0.5, keep=keep) for l in range(2)]
+        h_b = dev(h0)
+        c2.hg_stack(layers, h_b, 2)
+        torch.cuda.synchronize()
+    assert np.array_equal(bits(h_a), bits(h_b))
+
+
+def test_sharded_without_init_is_an_error():
+    with hg.Context(0, max_k=1024, max_n=2048) as c:
+        x, W, b = gen.linear_inputs(52, 0, "o", 1, 256, 128)
+        p = c.plan(hg.make_rates(1, 1, 1), 256, 128, 1, 0, hg.FIXED, 0.5)
+        _, Wh = split_weight(W, 0)
+        y = torch.zeros((1, 256), device="cuda")
+        with pytest.raises(hg.HgError) as e:
+            c.hg_linear_sharded(p, dev(x), None, Wh, dev_f32(b), y)
+        assert e.value.status == hg.HG_ESTATE

@@ -257,3 +257,15 @@ def test_schedule_divergence_drops_prefetch():
             y2 = _linear(c, x2, W2, b2, 1, 128, 0.5)
             assert oracle.within_tol(y1, oracle.linear(x1, W1, b1))[0], it
             assert oracle.within_tol(y2, oracle.linear(x2, W2, b2))[0], it
+
+
+@pytest.mark.parametrize("B", [1, 3])
+def test_zero_copy_stream_mode_equals_ring(ctx, B):
+    """stream_mode 1: the GEMV reads the streamed rows straight from pinned host memory over the
+    link (TMA bulk copies from mapped memory) -- same kernel arithmetic, identical bits."""
+    x, W, b = gen.linear_inputs(35, 0, "fc1", B, 3072, 7168)
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=8192, max_n=4096, stream_mode=1) as cz:
+        y_zc = _linear(cz, x, W, b, B, 512, 0.6)
+    y_ring = _linear(ctx, x, W, b, B, 512, 0.6)
+    assert np.array_equal(y_zc, y_ring)
+    assert oracle.within_tol(y_zc, oracle.linear(x, W, b))[0]

@@ -10,6 +10,10 @@ bench.py's timed protocol on the OPT-30B stack, batch 1, r = 0 unless stated:
   no hybrid: CPU only   alpha = 0: every host row on the CPU lane
   no mirrored glue      GPU-only glue: the CPU lane waits for x to cross the link (reading R24 off)
   host events           handshake = 0: one GEMV launch per chunk, host events (pre-tag pipeline)
+  zero-copy streaming   stream_mode = 1: the GEMV's TMA bulk copies read the pinned host rows over
+                        PCIe themselves (no copy engine, no ring, no tags, no cross-linear prefetch)
+  one chunk per linear  1 GiB chunks: the GEMV of a linear starts after its whole slice arrived
+                        (the pinned-but-blocking strategy of Fig. 5b, with pre-pinned weights)
   + module scheduler    HBM budget 10 GB placed by hg_schedule (Sec. 4.5)          (P:366 row)
 
   python tools/ablation.py [--out file.json]
@@ -31,6 +35,8 @@ VARIANTS = [
     ("no hybrid: CPU only (alpha=0)", {"alpha": 0.0}, {}),
     ("no mirrored glue", {}, {"mirror_glue": 0}),
     ("host events, GEMV per chunk", {}, {"handshake": 0}),
+    ("zero-copy streaming (SM TMA reads over PCIe)", {}, {"stream_mode": 1}),
+    ("one chunk per linear (no chunk pipelining)", {"chunk_mb": 1024}, {}),
     ("+ module scheduler, 10 GB HBM", {"budget": 10.0}, {}),
 ]
 
@@ -59,7 +65,7 @@ def main():
         for k, v in over.items():
             if k != "budget":
                 setattr(va, k, v)
-        ctx = hg.Context(st["local"], cpu_threads=st["threads"], cpu_first=-1, chunk_bytes=args.chunk_mb << 20,
+        ctx = hg.Context(st["local"], cpu_threads=st["threads"], cpu_first=-1, chunk_bytes=va.chunk_mb << 20,
                          ring_bytes=args.ring_mb << 20, max_k=bench.F, max_n=bench.F, wrap_prefetch=1,
                          collect_stats=0, **cfg)
         st["ctx"] = ctx
