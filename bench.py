@@ -243,10 +243,12 @@ def prepare(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ncores = os.cpu_count() or 1
     per = max(1, ncores // world)
-    threads = args.threads or per
+    pin_threads = 4 if args.pageable else 0  # the pin lane's memcpy threads get their own cores
+    threads = args.threads or max(1, per - pin_threads)
     ctx = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
                      chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
-                     max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0)
+                     max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
+                     pageable=int(args.pageable), pin_threads=max(1, pin_threads))
     if world > 1:
         uid = hg.hg_dist_unique_id() if rank == 0 else None
         obj = [uid]
@@ -262,7 +264,7 @@ def prepare(args):
         for name in NAMES:
             N, K = SHAPES[name]
             r0, r1 = rank * N // world, (rank + 1) * N // world
-            Wt = torch.empty((r1 - r0, K), dtype=torch.int16, pin_memory=True)
+            Wt = torch.empty((r1 - r0, K), dtype=torch.int16, pin_memory=not args.pageable)
             gen.uniform_bf16(SEED, gen.tensor_id(l, name, "W"), (r1 - r0) * K, gen.w_scale(K),
                              offset=r0 * K, out=Wt.data_ptr())
             b = gen.bf16_bits_to_f32(gen.uniform_bf16(SEED, gen.tensor_id(l, name, "bias"), r1 - r0,
@@ -340,8 +342,8 @@ def run_point(st, args, budget_gb=0.0):
     pk = peaks()
     if args.alpha is not None:
         mode, af = hg.FIXED, args.alpha
-    else:
-        mode, af = hg.EXACT, 0.0
+    else:  # pageable weights: Eq. (9), T_COM = max(T_PIN, T_TRANS); pinned: Eq. (5)
+        mode, af = (hg.ASYNC if args.pageable else hg.EXACT), 0.0
 
     # ---- NEXT(3): heterogeneous module scheduler under an HBM budget (Sec. 4.5) ----
     n_res_map, W_dev_map, sched = {}, {}, None
@@ -442,7 +444,8 @@ def run_point(st, args, budget_gb=0.0):
     sctx_stats = None
     if args.breakdown and world == 1:
         sctx = hg.Context(local, cpu_threads=st["threads"], cpu_first=-1, chunk_bytes=args.chunk_mb << 20,
-                          ring_bytes=args.ring_mb << 20, max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1)
+                          ring_bytes=args.ring_mb << 20, max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1,
+                          pageable=int(args.pageable), pin_threads=4)
         sctx.hg_stack(layers, h_dev, B, stream=s)  # fill the prefetch pipeline
         sctx.hg_reset_stats()
         for _ in range(2):
@@ -496,6 +499,8 @@ def run_point(st, args, budget_gb=0.0):
                                "link": round(sctx_stats["link_busy_s"] / wall_i, 3),
                                "gpu": round(sctx_stats["gpu_busy_s"] / wall_i, 4)},
                  "x_wait_ms": round(sctx_stats["x_wait_s"] * 1e3, 2),
+                 "pin_GBps": round(sctx_stats["bytes_pinned"] / sctx_stats["pin_busy_s"] / 1e9, 2)
+                 if sctx_stats["pin_busy_s"] > 0 else None,
                  "glue_ms": round(sctx_stats["glue_s"] * 1e3, 2),
                  "steps": 2, "mirror_linears": sctx_stats["mirror_linears"]}
     line = {
@@ -510,8 +515,9 @@ def run_point(st, args, budget_gb=0.0):
                    "r_resident": round(plan_tot["bytes_res"] / shard_bytes, 4),
                    "hbm_budget_GB": budget_gb,
                    "alpha_mode": "fixed" if args.alpha is not None else (
-                       "Eq5 (measured rates) refined by the alpha benchmark (Sec. 4.4)" if abench else
-                       "Eq5 exact (measured rates)"),
+                       ("Eq9" if args.pageable else "Eq5") + (" (measured rates) refined by the alpha benchmark "
+                                                              "(Sec. 4.4)" if abench else " (measured rates)")),
+                   "host_weights": "pageable, pin lane (Sec. 4.3)" if args.pageable else "pinned once at load",
                    "alpha": next((p.alpha_eff for p in all_plans if p.n_res < p.N), 0.0),
                    "alpha_seed_eq5": alpha_seed,
                    "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
@@ -582,6 +588,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-abench", dest="abench", action="store_false", help="use Eq. (5) alpha unrefined")
     ap.add_argument("--abench-gamma", type=float, default=0.06)
+    ap.add_argument("--pageable", action="store_true",
+                    help="NEXT(1): host weights not page-locked; streamed chunks go through the pin lane")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
     args = ap.parse_args()

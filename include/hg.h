@@ -152,7 +152,12 @@ typedef struct {
                             through the device ring; 1 = zero-copy: the GEMV's TMA bulk copies read
                             the pinned host rows over the link directly (no ring, no tags; SIMT
                             batches only -- tcgen05 batches keep mode 0)                          */
-    int32_t _pad0;
+    int32_t pageable;    /* 1: W_host may be pageable (not page-locked): streamed chunks of such
+                            weights go through the pin lane -- the asynchronous parameter manager of
+                            Sec. 4.3 -- into a pinned staging ring; 0 (default): HG_ENOTPINNED     */
+    int32_t pin_threads; /* memcpy threads of the pin lane (default 4)                           */
+    int32_t _pad1;
+    int64_t staging_bytes; /* pinned staging ring of the pin lane (default 512 MiB, >= 2 slots)  */
 } hg_config;
 
 /* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last
@@ -174,6 +179,8 @@ typedef struct {
     int64_t n_chunks;       /* streamed chunks consumed                                 */
     int64_t n_linears;
     int64_t gpu_launches;   /* kernels this library launched                            */
+    int64_t bytes_pinned;   /* bytes the pin lane staged (pageable weights)              */
+    double pin_busy_s;      /* pin lane time of the calls' streamed bytes at the lane's rate */
     int64_t mirror_linears; /* linears whose input the CPU lane computed itself          */
     int64_t mirror_mismatch; /* verify_mirror: activation elements host != device         */
 } hg_stats_t;
@@ -243,6 +250,8 @@ HG_API hg_status hg_plan(const hg_rates *rates, int64_t N, int64_t K, int batch,
  * processing time"; the alpha benchmark's measurements).
  *   W_host: page-locked [N, K] bf16 weight to measure on (a real linear).
  *   flags bit 0: measure the CPU lane while the link is busy (shared host DRAM).
+ * For a pageable W_host (hg_config.pageable) v_pin is the pin lane's rate into its staging ring and
+ * the link is probed from staging; otherwise v_pin = +inf (weights pinned once, reading R7).
  * Fills v_cpu, v_gpu, v_link, b_link (large-chunk copy), b_host (flags bit 0), b_cpu (host read rate
  * of the pool threads), b_hbm (device read rate); v_pin = +inf. */
 HG_API hg_status hg_measure(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch,
@@ -277,6 +286,7 @@ typedef struct {
     double t_cpu[HG_ABENCH_MAX];   /* CPU-lane busy seconds per step (host clock)             */
     double t_com[HG_ABENCH_MAX];   /* link busy seconds per step (CUDA events on copies)      */
     double t_step[HG_ABENCH_MAX];  /* wall seconds per step (CUDA events)                     */
+    double t_pin[HG_ABENCH_MAX];   /* pin-lane busy seconds per step (pageable weights; else 0) */
 } hg_abench_result;
 
 /* Measure the lane times of hg_stack(layers) at every alpha of the window around

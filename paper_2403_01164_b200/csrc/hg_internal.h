@@ -109,6 +109,17 @@ void hglue_residual(const uint16_t *h1, const float *y, int64_t ldy, int64_t H, 
 void hglue_slice_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, uint16_t *out);
 void hglue_relu_bf16(const float *y, int64_t ldy, int64_t n, int batch, uint16_t *out);
 
+// ---------------------------------------------------------------- pinlane.cpp
+struct PinLane;
+PinLane *pinlane_create(int threads, uint8_t *staging, int64_t slot_bytes, int nslots, volatile uint32_t *pinned,
+                        volatile uint32_t *freed, double timeout_s);
+void pinlane_destroy(PinLane *p);
+// Copy [src, src+bytes) into staging slot `slot`, then publish pinned[slot] = tag (asynchronous, FIFO).
+void pinlane_submit(PinLane *p, const void *src, int64_t bytes, int slot, uint32_t tag);
+bool pinlane_error(const PinLane *p);
+void pinlane_stats(PinLane *p, double *busy_s, int64_t *bytes, bool reset);
+double pinlane_copy_timed(PinLane *p, void *dst, const void *src, int64_t bytes);
+
 // ---------------------------------------------------------------- threadpool.cpp
 class ThreadPool;
 ThreadPool *pool_create(int nthreads, int first_core);

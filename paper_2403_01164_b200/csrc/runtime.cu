@@ -172,6 +172,13 @@ struct hg_ctx {
     float *ymap[kMirrorRing] = {};
     cudaEvent_t ev_g[kMirrorRing] = {}, ev_yg[kMirrorRing] = {}, ev_use[kMirrorRing] = {};
     cudaStream_t d2h = nullptr;                    // side stream for the GPU rows' D2H
+    // pin lane (pageable weights, Sec. 4.3): pinned staging ring + mapped tag words
+    PinLane *pin = nullptr;
+    uint8_t *staging = nullptr;
+    int nstage = 0;
+    uint32_t *pinflags = nullptr;       // mapped host: pinned[nstage], freed[nstage]
+    uint32_t *pinflags_dev = nullptr;   // device address of the same words (stream memops)
+    int64_t pin_seq = 0;
     uint32_t *trace = nullptr;                     // HG_SYNC_DEBUG=3: mapped host trace words
     uint64_t trace_seq = 0;
     struct TraceLin { uint32_t id; int64_t seq0, n_chunks, n_res, n_str, K; };
@@ -234,6 +241,7 @@ hg_status check_ptr(hg_ctx *c, const void *p, bool want_device, const char *what
     cudaError_t e = cudaPointerGetAttributes(&at, p);
     if (e != cudaSuccess) {
         cudaGetLastError();
+        if (!want_device && c->cfg.pageable) return HG_OK;
         return set_error(want_device ? HG_ENOTDEVICE : HG_ENOTPINNED, "%s: %s", what,
                          cudaGetErrorString(e));
     }
@@ -241,10 +249,21 @@ hg_status check_ptr(hg_ctx *c, const void *p, bool want_device, const char *what
         if (at.type != cudaMemoryTypeDevice || at.device != c->device)
             return set_error(HG_ENOTDEVICE, "%s is not device memory of device %d", what, c->device);
     } else {
+        if (at.type == cudaMemoryTypeUnregistered && c->cfg.pageable) return HG_OK;  // pin lane stages it
         if (at.type != cudaMemoryTypeHost)
             return set_error(HG_ENOTPINNED, "%s is not page-locked host memory", what);
     }
     return HG_OK;
+}
+
+// true when p is host memory that is not page-locked (pageable); such weights need the pin lane
+bool is_pageable(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return at.type == cudaMemoryTypeUnregistered;
 }
 
 hg_status kerr(hg_ctx *c, int e, const char *what) {
@@ -330,6 +349,18 @@ hg_status memop(hg_ctx *c, memop_fn_t fn, cudaStream_t s, const uint32_t *addr, 
     return HG_OK;
 }
 
+hg_status ensure_pinlane(hg_ctx *c) {
+    if (c->pin) return HG_OK;
+    c->nstage = (int)std::max<int64_t>(2, c->cfg.staging_bytes / c->slot_bytes);
+    HG_CK(c, cudaHostAlloc((void **)&c->staging, (size_t)c->nstage * c->slot_bytes, cudaHostAllocDefault));
+    HG_CK(c, cudaHostAlloc((void **)&c->pinflags, (size_t)2 * c->nstage * 4, cudaHostAllocMapped));
+    std::memset(c->pinflags, 0, (size_t)2 * c->nstage * 4);
+    HG_CK(c, cudaHostGetDevicePointer((void **)&c->pinflags_dev, c->pinflags, 0));
+    c->pin = pinlane_create(c->cfg.pin_threads, c->staging, c->slot_bytes, c->nstage, c->pinflags,
+                            c->pinflags + c->nstage, c->cfg.timeout_s);
+    return HG_OK;
+}
+
 // Enqueue chunk `r` into the next ring slot on the copy stream.  `bound`: a GEMV that consumes
 // it is already enqueued (tags mode), so it is not tracked as in flight.
 hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
@@ -356,8 +387,23 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
         e0 = tev_get(c, &i0);
         if (e0) HG_CK(c, cudaEventRecord(e0, c->copy));
     }
-    HG_CK(c, cudaMemcpyAsync(c->ring + (int64_t)slot * c->slot_bytes, r.src, (size_t)r.bytes,
+    const void *src = r.src;
+    int pslot = -1;
+    uint32_t ptag = 0;
+    if (c->cfg.pageable && is_pageable(r.src)) {  // pin lane: pageable chunk -> pinned staging slot
+        if (!c->tags) return set_error(HG_EUNSUPPORTED, "pageable weights need the device-tag pipeline");
+        HG_TRY(ensure_pinlane(c));
+        const int64_t ps = c->pin_seq++;
+        pslot = (int)(ps % c->nstage);
+        ptag = (uint32_t)(ps + 1);
+        pinlane_submit(c->pin, r.src, r.bytes, pslot, ptag);
+        HG_TRY(memop(c, g_wait_value, c->copy, c->pinflags_dev + pslot, ptag, kWaitGeq));
+        src = c->staging + (int64_t)pslot * c->slot_bytes;
+    }
+    HG_CK(c, cudaMemcpyAsync(c->ring + (int64_t)slot * c->slot_bytes, src, (size_t)r.bytes,
                              cudaMemcpyHostToDevice, c->copy));
+    if (pslot >= 0)  // the staging slot may be refilled
+        HG_TRY(memop(c, g_write_value, c->copy, c->pinflags_dev + c->nstage + pslot, ptag, kWriteDefault));
     if (c->tags) HG_TRY(memop(c, g_write_value, c->copy, c->arrived + slot, (uint32_t)(seq + 1), kWriteDefault));
     else HG_CK(c, cudaEventRecord(c->ev_arrived[slot], c->copy));
     if (c->cfg.collect_stats && e0) {
@@ -1093,6 +1139,9 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     if (const char *v = getenv("HG_MIRROR_GLUE")) cfg->mirror_glue = atoi(v);
     cfg->stream_mode = 0;
     if (const char *v = getenv("HG_STREAM_MODE")) cfg->stream_mode = atoi(v);
+    cfg->pageable = 0;
+    cfg->pin_threads = 4;
+    cfg->staging_bytes = 512ll << 20;
     cfg->verify_mirror = 0;
     return HG_OK;
 }
@@ -1209,6 +1258,9 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
             if (c->yhost[r]) cudaFreeHost(c->yhost[r]);
         }
         if (c->yring) cudaFree(c->yring);
+        if (c->pin) pinlane_destroy(c->pin);
+        if (c->staging) cudaFreeHost(c->staging);
+        if (c->pinflags) cudaFreeHost(c->pinflags);
         if (c->d2h) cudaStreamDestroy(c->d2h);
         for (cudaEvent_t e : {c->ev_x, c->ev_ycpu[0], c->ev_ycpu[1], c->ev_done, c->ev_call0, c->ev_call1})
             if (e) cudaEventDestroy(e);
@@ -1463,6 +1515,19 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
             c->st.gpu_busy_s = gpu;
         }
     }
+    if (c->pin) {
+        double busy = 0;
+        int64_t pinned = 0;
+        pinlane_stats(c->pin, &busy, &pinned, false);
+        // like the link: the lane runs ahead into later calls' chunks, so the calls' pin time is
+        // their streamed bytes at the lane's measured rate
+        c->st.bytes_pinned = pinned;
+        c->st.pin_busy_s = pinned > 0 ? (double)c->st.bytes_str * busy / (double)pinned : 0.0;
+        if (pinlane_error(c->pin)) {
+            c->error = true;
+            return set_error(HG_ETIMEOUT, "the pin lane waited longer than %.1f s for a staging slot", c->cfg.timeout_s);
+        }
+    }
     *out = c->st;
     return HG_OK;
 }
@@ -1474,6 +1539,11 @@ HG_API hg_status hg_reset_stats(hg_ctx *c) {
         if (cudaEventSynchronize(c->ev_done) != cudaSuccess) dbg_trace_report(c);
         HG_CK(c, cudaEventSynchronize(c->ev_done));
         HG_CK(c, cudaStreamSynchronize(c->copy));
+    }
+    if (c->pin) {
+        double b;
+        int64_t n;
+        pinlane_stats(c->pin, &b, &n, true);
     }
     c->tev_used = 0;
     c->copy_ev.clear();
@@ -1528,14 +1598,18 @@ HG_API hg_status hg_alpha_bench(hg_ctx *c, const hg_opt_layer *layers, int n_lay
             out->t_cpu[i] = s.cpu_busy_s / cfg.reps;
             out->t_com[i] = s.link_busy_s / cfg.reps;
             out->t_step[i] = s.wall_s / cfg.reps;
+            out->t_pin[i] = s.pin_busy_s / cfg.reps;
         }
     }
     c->cfg.collect_stats = saved_stats;
     if (st != HG_OK) return st;  // keep the failing call's message (hg_reset_stats would overwrite it)
     HG_TRY(hg_reset_stats(c));
     out->n = (int)pts.size();
-    return hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, nullptr, out->n, cfg.degree, pts.front(),
-                          pts.back(), alpha_seed, &out->alpha_bar, &out->clamped);
+    // F_COM = max(F_PIN, F_TRANS): the pin lane counts when it did any work
+    bool pinned_any = false;
+    for (int i = 0; i < out->n; ++i) pinned_any |= out->t_pin[i] > 0;
+    return hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, pinned_any ? out->t_pin : nullptr, out->n, cfg.degree,
+                          pts.front(), pts.back(), alpha_seed, &out->alpha_bar, &out->clamped);
 }
 
 // ---------------------------------------------------------------- measurement
@@ -1565,17 +1639,31 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     HG_CK(c, cudaEventCreate(&e0));
     HG_CK(c, cudaEventCreate(&e1));
     float ms = 0;
+    // pageable weight (hg_config.pageable): the link is probed from the pin lane's staging ring and
+    // V_PIN is the lane's own rate (Eq. (9)); pinned weight: V_PIN = +inf (reading R7)
+    const bool pageable = c->cfg.pageable && is_pageable(W_host);
     const uint8_t *src = (const uint8_t *)W_host;
+    int64_t lbytes = wbytes;
+    double v_pin = INFINITY;
+    if (pageable) {
+        HG_TRY(ensure_pinlane(c));
+        lbytes = std::min<int64_t>(wbytes, (int64_t)c->nstage * c->slot_bytes);
+        std::vector<double> tp;
+        for (int it = 0; it < 3; ++it) tp.push_back(pinlane_copy_timed(c->pin, c->staging, W_host, lbytes));
+        std::sort(tp.begin(), tp.end());
+        v_pin = (double)lbytes / tp[1];
+        src = c->staging;
+    }
 
     // link: chunk-sized copies (v_link) and one large copy (b_link)
     const int64_t C = chunk_rows_for(K, c->cfg.granule, c->cfg.chunk_bytes);
-    const int64_t chunk = std::min<int64_t>(C * K * 2, wbytes);
+    const int64_t chunk = std::min<int64_t>(C * K * 2, lbytes);
     int64_t total = 0;
     // warm-up: first DMA over these pages and ring addresses is not representative
-    HG_CK(c, cudaMemcpyAsync(c->ring, src, std::min<int64_t>(wbytes, ring_bytes), cudaMemcpyHostToDevice,
+    HG_CK(c, cudaMemcpyAsync(c->ring, src, std::min<int64_t>(lbytes, ring_bytes), cudaMemcpyHostToDevice,
                              c->copy));
     HG_CK(c, cudaEventRecord(e0, c->copy));
-    for (int64_t off = 0; off + chunk <= wbytes && total < (512ll << 20); off += chunk) {
+    for (int64_t off = 0; off + chunk <= lbytes && total < (512ll << 20); off += chunk) {
         HG_CK(c, cudaMemcpyAsync(c->ring + (total % (ring_bytes - chunk + 1)) / 256 * 256, src + off,
                                  chunk, cudaMemcpyHostToDevice, c->copy));
         total += chunk;
@@ -1584,7 +1672,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     HG_CK(c, cudaEventSynchronize(e1));
     HG_CK(c, cudaEventElapsedTime(&ms, e0, e1));
     out->v_link = (double)total / (ms * 1e-3);
-    const int64_t big = std::min<int64_t>(std::min<int64_t>(wbytes, ring_bytes), 512ll << 20);
+    const int64_t big = std::min<int64_t>(std::min<int64_t>(lbytes, ring_bytes), 512ll << 20);
     HG_CK(c, cudaEventRecord(e0, c->copy));
     HG_CK(c, cudaMemcpyAsync(c->ring, src, big, cudaMemcpyHostToDevice, c->copy));
     HG_CK(c, cudaEventRecord(e1, c->copy));
@@ -1635,7 +1723,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     const int NB = (flags & 1) ? 192 : 0;  // 192 chunks ~ 6 GiB ~ 110 ms of link time
     std::vector<cudaEvent_t> evb((size_t)NB, nullptr);
     for (int i = 0; i < NB; ++i) HG_CK(c, cudaEventCreateWithFlags(&evb[i], cudaEventDisableTiming));
-    for (int64_t off = 0, n = 0; n < NB; ++n, off = (off + chunk) % (wbytes - chunk + 1)) {
+    for (int64_t off = 0, n = 0; n < NB; ++n, off = (off + chunk) % (lbytes - chunk + 1)) {
         HG_CK(c, cudaMemcpyAsync(c->ring, src + off / 256 * 256, chunk, cudaMemcpyHostToDevice, c->copy));
         HG_CK(c, cudaEventRecord(evb[n], c->copy));
     }
@@ -1668,7 +1756,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
         }, &rj);
     };
     auto flush_llc = [&]() { read_region(scratch.data(), sbytes); };
-    auto read_pass = [&]() { read_region(src, wbytes); };
+    auto read_pass = [&]() { read_region((const uint8_t *)W_host, wbytes); };
     auto median = [](std::vector<double> v) {
         std::sort(v.begin(), v.end());
         return v[v.size() / 2];
@@ -1708,7 +1796,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     out->b_cpu = (double)wbytes / median(tr);
     HG_CK(c, cudaStreamSynchronize(c->copy));
     for (auto e : evb) cudaEventDestroy(e);
-    out->v_pin = INFINITY;
+    out->v_pin = v_pin;
     HG_CK(c, cudaStreamSynchronize(c->copy));
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -69,14 +69,17 @@ class Config(ctypes.Structure):
                 ("wrap_prefetch", ctypes.c_int32), ("timeout_s", ctypes.c_double),
                 ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32),
                 ("mirror_glue", ctypes.c_int32), ("verify_mirror", ctypes.c_int32),
-                ("stream_mode", ctypes.c_int32), ("_pad0", ctypes.c_int32)]
+                ("stream_mode", ctypes.c_int32), ("pageable", ctypes.c_int32), ("pin_threads", ctypes.c_int32),
+                ("_pad1", ctypes.c_int32), ("staging_bytes", ctypes.c_int64)]
 
 
 class Stats(ctypes.Structure):
     _fields_ = ([(n, ctypes.c_double) for n in ("wall_s", "cpu_busy_s", "link_busy_s", "gpu_busy_s", "x_wait_s",
                                                 "glue_s")]
                 + [(n, ctypes.c_int64) for n in ("bytes_res", "bytes_str", "bytes_cpu", "n_chunks", "n_linears",
-                                                 "gpu_launches", "mirror_linears", "mirror_mismatch")])
+                                                 "gpu_launches", "bytes_pinned")]
+                + [("pin_busy_s", ctypes.c_double)]
+                + [(n, ctypes.c_int64) for n in ("mirror_linears", "mirror_mismatch")])
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -113,13 +116,13 @@ class AbenchCfg(ctypes.Structure):
 class AbenchResult(ctypes.Structure):
     _fields_ = [("alpha_seed", ctypes.c_double), ("alpha_bar", ctypes.c_double), ("n", ctypes.c_int32),
                 ("clamped", ctypes.c_int32)] + [(f, ctypes.c_double * HG_ABENCH_MAX)
-                                                for f in ("alpha", "t_cpu", "t_com", "t_step")]
+                                                for f in ("alpha", "t_cpu", "t_com", "t_step", "t_pin")]
 
     def as_dict(self):
         n = self.n
         return {"alpha_seed": self.alpha_seed, "alpha_bar": self.alpha_bar, "clamped": bool(self.clamped),
                 "alpha": list(self.alpha[:n]), "t_cpu": list(self.t_cpu[:n]), "t_com": list(self.t_com[:n]),
-                "t_step": list(self.t_step[:n])}
+                "t_step": list(self.t_step[:n]), "t_pin": list(self.t_pin[:n])}
 
 
 _vp, _i32, _i64, _dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double

@@ -5,6 +5,8 @@ oracle fed the GPU's own bf16 input to that linear (from the layer trace); each
 glue step likewise.  bf16 glue outputs may differ from the fp64 oracle by the
 rounding of an fp32 intermediate, so they use the same elementwise tolerance.
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -227,4 +229,37 @@ def test_mirrored_glue_mixed_residency():
                 cpu_linears = sum(1 for res in resident for name in NAMES if name not in res)
                 assert st.mirror_linears == 2 * cpu_linears and st.mirror_mismatch == 0
             outs[mirror] = bits(h)
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_stack_pageable_weights_equal_pinned():
+    """A stack whose host weights are pageable (pin lane, Sec. 4.3) gives the same bits as pinned."""
+    H, F, B = 256, 1024, 2
+    outs = []
+    for pageable in (1, 0):
+        with hg.Context(0, chunk_bytes=256 << 10, ring_bytes=4 << 20, max_k=4096, max_n=8192, pageable=pageable,
+                        staging_bytes=1 << 20, wrap_prefetch=1) as c:
+            keep, layers = [], []
+            for l in range(2):
+                L = make_layer_mirror(c, H, F, B, layer=l, alpha=0.6, keep=keep)
+                if pageable:  # swap every pinned host weight for a pageable copy
+                    for i in range(4):
+                        d = L.lin[i]
+                        if d.W_host:
+                            n = d.plan.N - d.plan.n_res
+                            t = torch.empty((n, d.plan.K), dtype=torch.int16)
+                            ctypes_src = torch.from_numpy(np.ctypeslib.as_array(
+                                (ctypes.c_int16 * (n * d.plan.K)).from_address(d.W_host)).reshape(n, d.plan.K).copy())
+                            t.copy_(ctypes_src)
+                            keep.append(t)
+                            L.lin[i].W_host = t.data_ptr()
+                layers.append(L)
+            h0 = gen.uniform_bf16(13, 991, B * H, 1.0).reshape(B, H)
+            for _ in range(2):
+                h = dev(h0)
+                c.hg_stack(layers, h, B)
+                torch.cuda.synchronize()
+            outs.append(bits(h))
+            if pageable:
+                assert c.hg_stats().bytes_pinned > 0
     assert np.array_equal(outs[0], outs[1])

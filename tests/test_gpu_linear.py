@@ -269,3 +269,40 @@ def test_zero_copy_stream_mode_equals_ring(ctx, B):
     y_ring = _linear(ctx, x, W, b, B, 512, 0.6)
     assert np.array_equal(y_zc, y_ring)
     assert oracle.within_tol(y_zc, oracle.linear(x, W, b))[0]
+
+
+def _pageable(bits):
+    """uint16 bits -> a plain (pageable) host int16 tensor."""
+    return torch.from_numpy(np.ascontiguousarray(bits, np.uint16).view(np.int16).copy())
+
+
+@pytest.mark.parametrize("B,stage_mb", [(1, 512), (2, 2), (8, 2)])
+def test_pageable_weights_pin_lane(B, stage_mb):
+    """hg_config.pageable: streamed chunks of a pageable weight go through the pin lane (pinned staging
+    ring, tags in mapped memory) -- results bit-identical to the pinned-weight path; a 2-slot staging
+    ring (1 MiB chunks) forces slot reuse."""
+    N, K = 3072, 1024
+    x, W, b = gen.linear_inputs(36, 0, "fc1", B, N, K)
+    with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=4096, max_n=4096, pageable=1,
+                    staging_bytes=stage_mb << 20) as cp, \
+            hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=4096, max_n=4096) as cq:
+        for n_res, alpha in ((0, 0.7), (512, 1.0)):
+            Wd = dev(W[:n_res]) if n_res else None
+            y_pg = torch.full((B, N), float("nan"), device="cuda")
+            cp.hg_linear(dev(x), B, N, K, Wd, n_res, _pageable(W[n_res:]), alpha, dev_f32(b), y_pg)
+            y_pin = torch.full((B, N), float("nan"), device="cuda")
+            cq.hg_linear(dev(x), B, N, K, Wd, n_res, pinned(W[n_res:]), alpha, dev_f32(b), y_pin)
+            torch.cuda.synchronize()
+            assert np.array_equal(y_pg.cpu().numpy(), y_pin.cpu().numpy()), (n_res, alpha)
+            assert oracle.within_tol(y_pg.cpu().numpy(), oracle.linear(x, W, b))[0]
+        s = cp.hg_stats()
+        assert s.bytes_pinned > 0 and s.pin_busy_s > 0
+
+
+def test_pageable_measure_reports_pin_rate():
+    N, K = 4096, 2048
+    _, W, _ = gen.linear_inputs(37, 0, "fc1", 1, N, K)
+    with hg.Context(0, chunk_bytes=4 << 20, ring_bytes=64 << 20, max_k=4096, max_n=8192, pageable=1,
+                    staging_bytes=64 << 20) as c:
+        r = c.hg_measure(_pageable(W), N, K, 1)
+        assert np.isfinite(r.v_pin) and r.v_pin > 0 and r.v_link > 0 and r.v_cpu > 0

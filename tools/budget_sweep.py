@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--no-abench", dest="abench", action="store_false")
     ap.add_argument("--abench-gamma", type=float, default=0.06)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--pageable", action="store_true")
     args = ap.parse_args()
     bench.set_model(args.model)
     if args.layers is None:

@@ -62,6 +62,7 @@ PRODUCT_SOURCES = [
     ("host_gemv_avx2.cpp", "cxx_avx2"),
     ("threadpool.cpp", "cxx"),
     ("host_glue.cpp", "cxx_avx2"),
+    ("pinlane.cpp", "cxx"),
     ("gemv_sm100.cu", "cu"),
     ("gemv_tc_sm100.cu", "cu"),
     ("glue_sm100.cu", "cu"),
