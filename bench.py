@@ -385,7 +385,14 @@ def run_point(st, args, budget_gb=0.0):
             alpha_seed = float(t.item())
         res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_seed, gamma=args.abench_gamma, lam=0.02, degree=2,
                                  reps=1, stream=s)
+        rounds = 1
+        # no balance point inside the window: re-centre it on the clamped edge (at most 3 more rounds)
+        while res.clamped and rounds < 4 and 0.0 < res.alpha_bar < 1.0:
+            res = ctx.hg_alpha_bench(layers, h_dev, B, res.alpha_bar, gamma=args.abench_gamma, lam=0.02,
+                                     degree=2, reps=1, stream=s)
+            rounds += 1
         abench = res.as_dict()
+        abench["rounds"] = rounds
         layers, plans, all_plans = build_layers(st, args, hg.FIXED, res.alpha_bar, n_res_map, W_dev_map)
         h_dev.copy_(h_host)
 
@@ -539,7 +546,7 @@ def run_point(st, args, budget_gb=0.0):
         "lanes": lanes,
         "scheduler": sched,
         "alpha_bench": None if abench is None else {
-            "alpha_bar": abench["alpha_bar"], "clamped": abench["clamped"],
+            "alpha_bar": abench["alpha_bar"], "clamped": abench["clamped"], "rounds": abench["rounds"],
             "points": [[round(a, 4), round(tc * 1e3, 3), round(tl * 1e3, 3), round(ts * 1e3, 3)] for a, tc, tl, ts in
                        zip(abench["alpha"], abench["t_cpu"], abench["t_com"], abench["t_step"])],
             "points_cols": ["alpha", "t_cpu_ms", "t_link_ms", "t_step_ms"]},

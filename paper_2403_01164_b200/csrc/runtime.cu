@@ -1794,6 +1794,8 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
         tr.push_back(secs(t0, clk::now()));
     }
     out->b_cpu = (double)wbytes / median(tr);
+    // both lanes together move at least what either moves alone; a lower joint probe is noise
+    if (out->b_host > 0) out->b_host = std::max(out->b_host, std::max(out->b_cpu, out->b_link));
     HG_CK(c, cudaStreamSynchronize(c->copy));
     for (auto e : evb) cudaEventDestroy(e);
     out->v_pin = v_pin;
