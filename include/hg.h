@@ -228,6 +228,10 @@ typedef struct {
 
 /* ---------------------------------------------------------------- lifetime */
 HG_API int hg_abi_version(void);
+/* sizeof of the ABI structs, for bindings to check their mirrors: which = 0 hg_rates, 1 hg_plan_t,
+ * 2 hg_config, 3 hg_stats_t, 4 hg_linear_desc, 5 hg_opt_layer, 6 hg_layer_trace, 7 hg_abench_cfg,
+ * 8 hg_abench_result, 9 hg_module; 0 for an unknown index. */
+HG_API size_t hg_struct_size(int which);
 HG_API const char *hg_last_error(void);
 HG_API hg_status hg_config_default(hg_config *cfg);
 

@@ -1116,6 +1116,22 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
 extern "C" {
 
 HG_API int hg_abi_version(void) { return HG_ABI_VERSION; }
+
+HG_API size_t hg_struct_size(int which) {
+    switch (which) {
+        case 0: return sizeof(hg_rates);
+        case 1: return sizeof(hg_plan_t);
+        case 2: return sizeof(hg_config);
+        case 3: return sizeof(hg_stats_t);
+        case 4: return sizeof(hg_linear_desc);
+        case 5: return sizeof(hg_opt_layer);
+        case 6: return sizeof(hg_layer_trace);
+        case 7: return sizeof(hg_abench_cfg);
+        case 8: return sizeof(hg_abench_result);
+        case 9: return sizeof(hg_module);
+        default: return 0;
+    }
+}
 HG_API const char *hg_last_error(void) { return g_err; }
 
 HG_API hg_status hg_config_default(hg_config *cfg) {

@@ -129,6 +129,7 @@ _vp, _i32, _i64, _dbl = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_
 _P = ctypes.POINTER
 _sig = {
     "hg_abi_version": (ctypes.c_int, []),
+    "hg_struct_size": (ctypes.c_size_t, [ctypes.c_int]),
     "hg_last_error": (ctypes.c_char_p, []),
     "hg_config_default": (_i32, [_P(Config)]),
     "hg_create": (_i32, [_P(_vp), _i32, _P(Config)]),

@@ -140,3 +140,15 @@ def test_hg_alpha_solve_closed_forms_and_errors():
         hg.hg_alpha_solve([0.1, 0.2], [1, 2], [2, 1], 2, 0.1, 0.2, 0.1)   # n < degree + 1
     with pytest.raises(hg.HgError):
         hg.hg_alpha_solve([0.1, 0.1, 0.1], [1, 2, 3], [2, 1, 0], 1, 0.1, 0.1, 0.1)  # singular fit
+
+
+def test_struct_mirrors_match_the_c_layout():
+    """Every ctypes mirror in hg.py has the size of its C struct (ABI drift check)."""
+    mirrors = [hg.Rates, hg.Plan, hg.Config, hg.Stats, hg.LinearDesc, hg.OptLayer, hg.LayerTrace, hg.AbenchCfg,
+               hg.AbenchResult, hg.Module]
+    lib = ctypes.CDLL(hg.LIB_PATH)
+    lib.hg_struct_size.restype = ctypes.c_size_t
+    lib.hg_struct_size.argtypes = [ctypes.c_int]
+    for i, m in enumerate(mirrors):
+        assert lib.hg_struct_size(i) == ctypes.sizeof(m), (m.__name__, lib.hg_struct_size(i), ctypes.sizeof(m))
+    assert lib.hg_struct_size(99) == 0
