@@ -95,6 +95,11 @@ void host_rows_avx2(const uint16_t *x, int batch, int64_t K, const uint16_t *W, 
 void host_rows_scalar(const uint16_t *x, int batch, int64_t K, const uint16_t *W, int64_t r0,
                       int64_t r1, const float *bias, float *y, int64_t ldy);
 host_rows_fn host_rows_select(const char **name);
+// AMX-BF16 tiles (batch >= 4 by default); host_amx_enable() asks the OS for tile state once.
+void host_rows_amx(const uint16_t *x, int batch, int64_t K, const uint16_t *W, int64_t r0, int64_t r1,
+                   const float *bias, float *y, int64_t ldy);
+bool host_amx_enable();
+void host_gemv_new_job();  // call before posting a CPU-lane job (AMX repacks its x)
 // Host read-bandwidth kernel (probe): returns a checksum so the loads are not elided.
 uint64_t host_read_avx512(const void *p, int64_t bytes);
 

@@ -113,6 +113,17 @@ void host_job_run(void *a, int) {
     }
 }
 
+}  // namespace
+}  // namespace hg
+struct hg_ctx;
+namespace hg {
+namespace {
+host_rows_fn host_fn_for(hg_ctx *c, int batch);
+}  // namespace
+}  // namespace hg
+namespace hg {
+namespace {
+
 // One heterogeneous linear, internal form.
 struct Lin {
     hg_plan_t plan;
@@ -134,6 +145,7 @@ struct hg_ctx {
     hg_config cfg;
     ThreadPool *pool = nullptr;
     host_rows_fn host_fn = nullptr;
+    int amx_min_batch = 0;  // batches >= this use AMX tiles on the CPU lane (0: never)
     bool error = false;
 
     // ---- CUDA resources (device contexts only)
@@ -213,6 +225,14 @@ struct hg_ctx {
     bool call_timed = false;
     bool stats_open = false;  // ev_call0 recorded since the last reset
 };
+
+namespace hg {
+namespace {
+host_rows_fn host_fn_for(hg_ctx *c, int batch) {
+    return (c->amx_min_batch > 0 && batch >= c->amx_min_batch) ? host_rows_amx : c->host_fn;
+}
+}  // namespace
+}  // namespace hg
 
 namespace {
 
@@ -693,7 +713,7 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         HG_TRY(wait_event(c, c->ev_ycpu[yb], nullptr));  // this buffer's previous join has read it
         const auto t0 = clk::now();
         HostJob job;
-        job.fn = c->host_fn;
+        job.fn = host_fn_for(c, B);
         job.x = c->x_host;
         job.batch = B;
         job.K = K;
@@ -705,10 +725,12 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
         job.block = 16;
         job.next.store(0);
         if (async_post) {
+            host_gemv_new_job();
             pool_post(c->pool, host_job_run, &job);
             gst = enqueue_gpu_lanes(c, L, s);
             pool_join(c->pool);  // always: workers reference `job`
         } else {
+            host_gemv_new_job();
             pool_run(c->pool, host_job_run, &job);
         }
         if (gst != HG_OK) return gst;
@@ -1051,7 +1073,7 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             c->st.mirror_linears++;
             if (c->cfg.verify_mirror) HG_TRY(verify_act(c, xh, c->act, (int64_t)B * K, s));
             HG_TRY(wait_event(c, c->ev_use[slot], nullptr));  // the join that read this slot is done
-            job.fn = c->host_fn;
+            job.fn = host_fn_for(c, B);
             job.x = xh;
             job.batch = B;
             job.K = K;
@@ -1063,6 +1085,7 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             job.block = 16;
             job.next.store(0);
             t0 = clk::now();  // CPU-lane busy time starts here (catch-up waits are x_wait)
+            host_gemv_new_job();
             pool_post(c->pool, host_job_run, &job);
         }
         // ---- GPU rows into the ring slot, then (side stream) their copy to the host slot
@@ -1184,6 +1207,11 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     int nthr = cfg.cpu_threads > 0 ? cfg.cpu_threads : (int)sysconf(_SC_NPROCESSORS_ONLN);
     c->pool = pool_create(nthr, cfg.cpu_first);
     c->host_fn = host_rows_select(nullptr);
+    {
+        const char *v = getenv("HG_AMX_MIN_BATCH");
+        const int want = v ? atoi(v) : 4;
+        c->amx_min_batch = (want > 0 && !getenv("HG_HOST_ISA") && host_amx_enable()) ? want : 0;
+    }
     if (device < 0) {
         *out = c;
         return HG_OK;
@@ -1457,7 +1485,7 @@ HG_API hg_status hg_host_gemv(hg_ctx *c, const void *x, int batch, int64_t n, in
         return set_error(HG_EINVAL, "hg_host_gemv: bad shape");
     if (K % 8) return set_error(HG_EALIGN, "K %% 8 != 0");
     HostJob job;
-    job.fn = c->host_fn;
+    job.fn = host_fn_for(c, batch);
     job.x = (const uint16_t *)x;
     job.batch = batch;
     job.K = K;
@@ -1468,6 +1496,7 @@ HG_API hg_status hg_host_gemv(hg_ctx *c, const void *x, int batch, int64_t n, in
     job.ldy = n;
     job.block = 16;
     job.next.store(0);
+    host_gemv_new_job();
     pool_run(c->pool, host_job_run, &job);
     return HG_OK;
 }

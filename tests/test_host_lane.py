@@ -83,3 +83,16 @@ def test_bad_shapes(ctx):
     with pytest.raises(hg.HgError) as e:
         ctx.hg_host_gemv(x, 9, 4, 8, W, None, y)
     assert e.value.status == hg.HG_EINVAL
+
+
+@pytest.mark.parametrize("B", [4, 8])
+def test_amx_lane_matches_oracle(B, monkeypatch):
+    """Batches >= 4 use AMX tiles when the host has them (HG_AMX_MIN_BATCH); rows not a multiple of
+    16 fall back to AVX-512 for the tail.  Tolerance parity with the fp64 oracle either way."""
+    monkeypatch.setenv("HG_AMX_MIN_BATCH", "4")
+    x, W, b = gen.linear_inputs(44, 0, "fc1", B, 1000, 4096)
+    y = np.zeros((B, 1000), np.float32)
+    with hg.Context(-1, cpu_threads=3) as c:
+        c.hg_host_gemv(x, B, 1000, 4096, W, b, y)
+    ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+    assert ok, worst

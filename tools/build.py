@@ -60,6 +60,7 @@ PRODUCT_SOURCES = [
     ("plan.cpp", "cxx"),
     ("host_gemv.cpp", "cxx_avx512"),
     ("host_gemv_avx2.cpp", "cxx_avx2"),
+    ("host_gemv_amx.cpp", "cxx_amx"),
     ("threadpool.cpp", "cxx"),
     ("host_glue.cpp", "cxx_avx2"),
     ("pinlane.cpp", "cxx"),
@@ -88,7 +89,9 @@ def _product_objs(force=False, verbose=False):
         else:
             isa = {"cxx": [], "cxx_avx512": ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512bf16",
                                                "-mfma"],
-                   "cxx_avx2": ["-mavx2", "-mfma", "-mf16c"]}[kind]
+                   "cxx_avx2": ["-mavx2", "-mfma", "-mf16c"],
+                   "cxx_amx": ["-mavx512f", "-mavx512bw", "-mavx512vl", "-mavx512bf16", "-mfma", "-mamx-tile",
+                               "-mamx-bf16"]}[kind]
             cmd = ["g++", "-std=c++17", *common, *isa, "-I" + os.path.join(CUDA, "include"),
                    "-c", s, "-o", o]
         jobs.append((cmd, o, [s] + hdrs))
