@@ -160,9 +160,14 @@ def run_reference(args):
 def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     """Average device time of the step's GEMV launches -- one persistent launch per linear over
     its resident rows and all its streamed chunks (hg_gemv_replay: same kernel, grid and
-    per-chunk work split as in the step, chunks read from ring slots 0..n_chunks-1 with the
-    arrival tags skipped) -- timed with CUDA events on the launching stream, L2 flushed (a
-    256 MiB write) between launches so W comes from HBM.
+    per-chunk work split as in the step, arrival tags skipped) -- timed with CUDA events on the
+    launching stream over `iters` back-to-back launches.  Each launch reads its chunks from the
+    next ring slots (seq0 rotates through the 4 GiB ring), so the launches together read far
+    more than L2 holds and every chunk comes from HBM; a GPU spin kernel holds the stream while
+    the host enqueues them, so the device never waits for the host.  The per-launch time thus
+    includes the launch gap, as in the step.  (The older single-launch-after-L2-flush figure is
+    kept as `single_launch`: it is dominated by event/launch latency -- a 1-element torch kernel
+    times 11-13 us that way, profiles/r01/gemv_latency.md.)
 
     Algorithmic bytes per launch = 2*K*(n_res + n_str) (the W rows the GPU lanes must read;
     x, bias and y are < 0.1%).  Returns None when the GEMV runs on the tcgen05 path.
@@ -170,7 +175,7 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     hbm_peak = pk.get("hbm_gbs", 6650.0)
     s = torch.cuda.current_stream()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    tot_bytes, tot_time, detail = 0.0, 0.0, {}
+    tot_bytes, tot_time, tot_time1, detail = 0.0, 0.0, 0.0, {}
     for name, p in plans.items():
         n_gpu = p.n_res + p.n_str
         if n_gpu <= 0:
@@ -178,26 +183,41 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
         x = torch.empty((B, p.K), dtype=torch.int16, device="cuda").random_(-3000, 3000)
         y = torch.empty((B, p.N), device="cuda")
         Wd = (W_dev or {}).get(name)
+        step = max(1, p.n_chunks)
+        seqs = [i * step for i in range(iters)]  # slot = seq mod nslots (128 slots in the bench's ring)
         try:
-            for _ in range(3):
-                ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s)
+            for q in seqs[:3]:
+                ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s, seq0=q)
         except Exception as e:  # tcgen05 batches: no replay entry point
             return {"unavailable": str(e)}
-        ts = []
-        for _ in range(iters):
+        torch.cuda.synchronize()
+        # back to back, GPU held by a spin kernel while the host enqueues
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(4_000_000)
+        e0.record(s)
+        for q in seqs:
+            ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s, seq0=q)
+        e1.record(s)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) * 1e-3 / iters
+        # single launch after an L2 flush (reported beside it)
+        ts1 = []
+        for i in range(5):
             flush.zero_()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s)
-            e1.record(s)
+            torch.cuda._sleep(200_000)
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(s)
+            ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s, seq0=seqs[i])
+            f1.record(s)
             torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) * 1e-3)
-        t = statistics.mean(ts)
+            ts1.append(f0.elapsed_time(f1) * 1e-3)
+        t1 = statistics.mean(ts1)
         nbytes = 2 * p.K * n_gpu
         tot_bytes += nbytes * layers
         tot_time += t * layers
+        tot_time1 += t1 * layers
         detail[name] = {"rows": n_gpu, "chunks": p.n_chunks, "K": p.K, "us": round(t * 1e6, 2),
-                        "GBps": round(nbytes / t / 1e9, 1)}
+                        "GBps": round(nbytes / t / 1e9, 1), "single_launch_us": round(t1 * 1e6, 2)}
     del flush
     if tot_time <= 0:
         return None
@@ -208,8 +228,12 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
             "traffic": traffic, "traffic_detail": traffic_detail,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy BW)" if "hbm_gbs" in pk else "fallback 6650 GB/s",
             "per_linear": detail,
-            "note": "bytes = 2*K*(n_res+n_str) per launch; CUDA events around each hg_gemv_replay launch (the "
-                    "step's launch configuration, arrival tags skipped), L2 flushed between launches; mean"}
+            "single_launch": {"GBps": round(tot_bytes / tot_time1 / 1e9, 1),
+                              "frac": round(tot_bytes / tot_time1 / 1e9 / hbm_peak, 4),
+                              "note": "one launch after a 256 MiB L2 flush, event to event"},
+            "note": "bytes = 2*K*(n_res+n_str) per launch; CUDA events around %d back-to-back hg_gemv_replay "
+                    "launches (the step's launch configuration, arrival tags skipped) whose chunks walk the "
+                    "ring (inputs larger than L2); mean per launch" % iters}
 
 
 def ncu_traffic():

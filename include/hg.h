@@ -357,13 +357,24 @@ HG_API hg_status hg_gemv(hg_ctx *ctx, const void *x_dev, int batch, int64_t n, i
 
 /* Measurement entry point: the persistent GEMV launch hg_linear_planned would enqueue for
  * `plan` (resident rows from W_dev, then the plan's n_chunks streamed chunks read from ring
- * slots 0..n_chunks-1), with the chunks taken as already present -- no arrival tags, nothing
- * released -- so its CUDA-event time is the kernel's own duration in the step's launch
- * configuration.  Streamed outputs are computed from whatever the ring holds (timing only);
- * resident outputs are exact.  y [batch, N] fp32 device.  Batches on the tcgen05 path and
- * plans with more chunks than ring slots return HG_EUNSUPPORTED / HG_EINVAL. */
+ * slots (seq0 + i) mod nslots, i < n_chunks), with the chunks taken as already present -- no
+ * arrival tags, nothing released -- so its CUDA-event time is the kernel's own duration in the
+ * step's launch configuration.  Rotating seq0 across calls walks the whole ring (the bench uses
+ * it so that back-to-back replays read more than L2 holds).  Streamed outputs are computed from
+ * whatever the ring holds (timing only); resident outputs are exact.  y [batch, N] fp32 device.
+ * Batches on the tcgen05 path, seq0 < 0 and plans with more chunks than ring slots return
+ * HG_EUNSUPPORTED / HG_EINVAL. */
 HG_API hg_status hg_gemv_replay(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
-                                const void *W_dev, const float *bias_dev, float *y_dev, void *stream);
+                                const void *W_dev, const float *bias_dev, float *y_dev, int64_t seq0,
+                                void *stream);
+
+/* Measurement only (tools/gemv_latency.py): from now on every SIMT GEMV launch of this process
+ * writes four globaltimer stamps (ns) per CTA -- [cta*4 + 0] entry, [1] first stage full in
+ * consumer warp 0, [2] consumer warp 0 done, [3] producer done -- into a mapped pinned host
+ * array of 4096*4 uint64 owned by the library (never freed); *out receives its host address.
+ * out == NULL turns the stamps off again.
+ * Stamps slow each launch slightly (posted writes over the host link); never on in the bench. */
+HG_API hg_status hg_debug_gemv_stamps(uint64_t **out);
 
 /* CPU lane alone: y_host[b*n + j] = x_host[b,:] . W_host[j,:] (+ bias_host[j]) on
  * the context's thread pool.  All host pointers (need not be pinned).  Works on

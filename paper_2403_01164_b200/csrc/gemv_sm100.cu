@@ -30,8 +30,12 @@
 //   * a part sum: lane l accumulates 16-byte vectors l, l+32, l+64, ... in ascending order
 //     (8 fmaf each, k ascending), then a butterfly over the 32 lanes;
 //   * y = (((S_0 + S_1) + ...) + S_{P-1}) + bias: for P > 1 the part sums are stored to a
-//     global workspace; after one grid-wide barrier at the end of the (cooperative) launch each
-//     CTA adds the parts of its share of the rows in part order.
+//     global workspace; the last of the P CTAs (p, j) sharing row group j to finish (a per-group
+//     arrival counter, self-resetting) adds the parts of the group's rows in part order.  No
+//     grid-wide barrier, so the launch needs no co-residency: it is cooperative only when a
+//     streamed chunk would reuse a ring slot of the same launch (n_chunks > nslots), and it is
+//     launched with programmatic stream serialization (PDL) so it starts streaming W while the
+//     previous kernel drains.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -66,8 +70,8 @@ template <> struct Cfg<6> { static constexpr int R = 4, S = 4, W = 4, PART = 409
 template <> struct Cfg<7> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <> struct Cfg<8> { static constexpr int R = 4, S = 4, W = 4, PART = 4096; };
 template <int W> constexpr int threads_for() { return (W + 1) * 32; }
-// Shared memory: [full[S] empty[S] mbarriers, padded to 128 B][S stages of R rows][x part]
-template <int S> __host__ __device__ constexpr int bars_bytes() { return (2 * S * 8 + 127) / 128 * 128; }
+// Shared memory: [full[S] empty[S] xfull mbarriers, padded to 128 B][S stages of R rows][x part]
+template <int S> __host__ __device__ constexpr int bars_bytes() { return ((2 * S + 1) * 8 + 127) / 128 * 128; }
 
 inline int part_max(int B) { return B <= 1 ? 8192 : 4096; }
 
@@ -91,11 +95,12 @@ struct SArgs {
     float *y;
     int64_t ldy;
     float *ws;
-    uint32_t *gbar;  // [2]: arrival count, generation (grid barrier for P > 1)
+    uint32_t *gbar;  // [4 + kGroupCounters]: words 4.. are the per-row-group part counters (P > 1)
     uint32_t *err;
     volatile uint32_t *trace;  // debug (HG_SYNC_DEBUG=3): mapped host words, see runtime.cu
     uint32_t trace_id;
     unsigned long long timeout_ns;
+    unsigned long long *stamps;  // measurement (hg_debug_gemv_stamps): [CTA][4] globaltimer or NULL
 };
 
 struct Src {
@@ -205,28 +210,6 @@ __device__ __forceinline__ float warp_sum(float v) {
     return v;
 }
 
-// All CTAs of the launch meet here (one thread per CTA; co-residency from the cooperative launch).
-__device__ void grid_barrier(const SArgs &a) {
-    volatile uint32_t *gen = a.gbar + 1;
-    const uint32_t g0 = *gen;
-    __threadfence();
-    if (atomicAdd(a.gbar, 1u) == gridDim.x - 1) {
-        atomicExch(a.gbar, 0u);
-        __threadfence();
-        atomicAdd(a.gbar + 1, 1u);
-    } else {
-        const unsigned long long t0 = globaltimer();
-        while (*gen == g0) {
-            __nanosleep(32);
-            if (globaltimer() - t0 > a.timeout_ns) {
-                atomicOr(a.err, 2u);
-                break;
-            }
-        }
-    }
-    __threadfence();
-}
-
 __device__ void signal_consumed(const SArgs &a, int64_t slot, uint32_t tag) {
     __threadfence();
     const uint32_t old = atomicAdd(&a.slot_cnt[slot], 1u);
@@ -243,10 +226,10 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     extern __shared__ __align__(128) uint8_t smem[];
     const int64_t kvmax = a.len >> 3;            // vectors per (full) part
     const int64_t unit_bytes = a.len * 2;        // stage slot per row
-    uint64_t *bars = (uint64_t *)smem;           // full[S], empty[S]
+    uint64_t *bars = (uint64_t *)smem;           // full[S], empty[S], xfull
     uint8_t *stages = smem + bars_bytes<S>();    // S * R * unit_bytes
     uint4 *xs = (uint4 *)(stages + (int64_t)S * R * unit_bytes);  // [B][kvmax]
-    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S);
+    const uint32_t full0 = smem_u32(bars), empty0 = smem_u32(bars + S), xfull = smem_u32(bars + 2 * S);
     const uint32_t stage0 = smem_u32(stages);
 
     const int p = blockIdx.x / a.gp, j = blockIdx.x - p * a.gp;
@@ -255,27 +238,24 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     const int kv = (int)(klen >> 3);
     const uint32_t bytes_p = (uint32_t)(klen * 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 0] = globaltimer();
+    // Programmatic dependent launch: the next kernel in the stream may be scheduled as soon as
+    // every CTA of this one is running.  Nothing here depends on the previous kernel except x
+    // (and the order of writes to y / the workspace, which all come after x): W rows are
+    // resident or gated by arrival tags.  So W streaming starts at once, and only the x copy
+    // waits for the previous grid (griddepcontrol.wait; a no-op without PDL).
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(full0 + 8 * s, 1);
             mbar_init(empty0 + 8 * s, 1);
         }
+        mbar_init(xfull, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    __syncthreads();  // barriers initialised; the producer starts streaming W right away
+    __syncthreads();  // barriers initialised; the producer starts with x, then streams W
     constexpr int kConsumerThreads = kConsumerWarps * 32;
-    if (warp < kConsumerWarps) {
-        // x part p -> shared memory, once per launch (every source has the same x), overlapping
-        // the producer's first bulk copies; only the consumers wait for it
-        const uint4 *xg = (const uint4 *)a.x;
-        const int64_t Kv = a.K >> 3;
-        for (int64_t i = threadIdx.x; i < (int64_t)B * kv; i += kConsumerThreads) {
-            const int64_t b = i / kv, v = i - b * kv;
-            xs[b * kvmax + v] = xg[b * Kv + (k0 >> 3) + v];
-        }
-        named_barrier(1, kConsumerThreads);
-    }
 
     if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {  // debug trace (mapped host memory)
         a.trace[1] = a.trace_id;
@@ -284,6 +264,20 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     const int64_t s_begin = a.n_res > 0 ? -2 : (a.n_dir > 0 ? -1 : 0);
     if (warp == kConsumerWarps) {
         // ------------------------------------------------------------ producer
+        if (lane == 1) {
+            // x part p -> shared memory, once per launch (every source has the same x), by bulk
+            // copies of its own (a loop of dependent global loads here cost ~3 us before the first
+            // row could be consumed), after the previous grid's writes are visible
+            uint64_t xpolicy;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(xpolicy));
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            mbar_expect_tx(xfull, (uint32_t)B * bytes_p);
+#pragma unroll 1
+            for (int b = 0; b < B; ++b)
+                bulk_g2s(smem_u32(xs) + (uint32_t)(b * kvmax * 16), (const uint8_t *)a.x + (b * a.K + k0) * 2,
+                         bytes_p, xfull, xpolicy);
+            return;
+        }
         if (lane != 0) return;
         uint64_t policy;
         asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
@@ -354,10 +348,12 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
         }
         consume_upto(issued - 1);
         flush();
+        if (a.stamps) a.stamps[blockIdx.x * 4 + 3] = globaltimer();
         return;
     }
 
     // ---------------------------------------------------------------- consumers
+    mbar_wait(xfull, 0);
     int64_t it = 0;
     for (int64_t s = s_begin; s < a.n_chunks; ++s) {
         const Src src = source(a, s);
@@ -367,6 +363,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
             const int st = (int)(it % S);
             const int nrows = rb - r < R ? (int)(rb - r) : R;
             mbar_wait(full0 + 8 * st, (uint32_t)((it / S) & 1));
+            if (a.stamps && it == 0 && lane == 0) a.stamps[blockIdx.x * 4 + 1] = globaltimer();
             const uint4 *sw = (const uint4 *)(stages + (int64_t)st * R * unit_bytes);
             float acc[R][B];
 #pragma unroll
@@ -423,24 +420,38 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
                         a.ws[((src.g0 + r + q) * a.P + p) * B + b] = acc[q][b];
         }
     }
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 2] = globaltimer();
     if (a.trace && threadIdx.x == 0 && blockIdx.x == 0) {
         a.trace[2] = a.trace_id;  // CTA 0 past its groups
         __threadfence_system();
     }
     if (a.P == 1) return;
     // ---------------------------------------------------------------- P > 1: parts -> y
+    // The last of the P CTAs sharing row group j sums the group's rows (release: every thread
+    // fences its part-sum stores, then one arrival per CTA; acquire: fence after the arrival).
+    __shared__ uint32_t s_last;
+    __threadfence();
     named_barrier(1, kConsumerThreads);
-    if (threadIdx.x == 0) grid_barrier(a);
+    if (threadIdx.x == 0) {
+        uint32_t *cnt = a.gbar + 4 + j;
+        const uint32_t old = atomicAdd(cnt, 1u);
+        s_last = old == (uint32_t)(a.P - 1);
+        if (s_last) atomicExch(cnt, 0u);  // ready for the next launch (stream-ordered after this one)
+        __threadfence();
+    }
     named_barrier(1, kConsumerThreads);
-    const int64_t n = a.n_res + a.n_dir + a.n_str;
-    const int64_t r0 = (int64_t)blockIdx.x * n / gridDim.x, r1 = (int64_t)(blockIdx.x + 1) * n / gridDim.x;
-    for (int64_t i = threadIdx.x; i < (r1 - r0) * B; i += kConsumerThreads) {
-        const int64_t g = r0 + i / B;
-        const int b = (int)(i % B);
-        const float *w = a.ws + g * a.P * B + b;
-        float sum = 0.f;
-        for (int pp = 0; pp < a.P; ++pp) sum += __ldcg(w + pp * B);
-        a.y[b * a.ldy + g] = sum + (a.bias ? a.bias[g] : 0.f);
+    if (!s_last) return;
+    for (int64_t s = s_begin; s < a.n_chunks; ++s) {
+        const Src src = source(a, s);
+        const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
+        for (int64_t i = threadIdx.x; i < (rb - ra) * B; i += kConsumerThreads) {
+            const int64_t g = src.g0 + ra + i / B;
+            const int b = (int)(i % B);
+            const float *w = a.ws + g * a.P * B + b;
+            float sum = 0.f;
+            for (int pp = 0; pp < a.P; ++pp) sum += __ldcg(w + pp * B);
+            a.y[b * a.ldy + g] = sum + (a.bias ? a.bias[g] : 0.f);
+        }
     }
 }
 
@@ -469,6 +480,8 @@ __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float 
 }
 
 int g_sms = 148;
+bool g_pdl = true;            // launch with programmatic stream serialization (HG_GEMV_PDL=0: off)
+bool g_pdl_coop_bad = false;  // set if the driver rejects PDL together with a cooperative launch
 
 template <int B, int R, int S, int W>
 int launch_v(const SArgs &a, cudaStream_t st) {
@@ -477,14 +490,32 @@ int launch_v(const SArgs &a, cudaStream_t st) {
     cfg.blockDim = dim3(threads_for<W>());
     cfg.dynamicSmemBytes = smem_bytes_for<B, R, S>(a.len);
     cfg.stream = st;
-    // With tags every CTA must be resident at once: a chunk's slot is only refilled after all
-    // CTAs drained its previous occupant (cooperative launch guarantees co-residency).
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
+    // A chunk's slot is only refilled after every CTA drained its previous occupant.  If that
+    // occupant belongs to an earlier launch, those CTAs finish on their own; co-residency is needed only when a streamed chunk reuses a ring slot of this same launch
+    // (its previous occupant is drained by CTAs of this grid): then every CTA must be resident.
+    const bool coop = a.arrived && a.n_chunks > a.nslots;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (coop) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    const bool pdl = g_pdl && !(coop && g_pdl_coop_bad);
+    if (pdl) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = (a.arrived || a.P > 1) ? 1 : 0;
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B, R, S, W>, a);
+    if (e != cudaSuccess && pdl && coop) {  // PDL not accepted with a cooperative launch: drop it
+        (void)cudaGetLastError();
+        g_pdl_coop_bad = true;
+        cfg.numAttrs = 1;
+        e = cudaLaunchKernelEx(&cfg, gemv_stream_kernel<B, R, S, W>, a);
+    }
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
@@ -508,6 +539,9 @@ int prepare_b() {
 // CTAs per SM for B = 1 (A/B switch HG_GEMV_CPS): 1 = Cfg<1> (8 stages, 8 consumer warps);
 // 2 or 3 = smaller CTAs (4 stages, 4 consumer warps, ~70 KB smem) sharing each SM.
 int g_cps1 = 1;
+unsigned long long *g_stamps = nullptr;  // device view of mapped host stamps (measurement only)
+unsigned long long *g_stamps_host = nullptr;
+int g_b1s = 8;  // A/B (HG_GEMV_B1S): B = 1 stage count 8 (one CTA per SM) or 6 (~100 KB: two fit, PDL overlap)
 int g_b34 = 0;  // A/B (HG_GEMV_B34): B = 3, 4 kernel shape 0 = Cfg (R2,S10,W10), 1 = (R2,S8,W8), 2 = (R4,S4,W4)
 
 }  // namespace
@@ -587,11 +621,12 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.trace = L.trace;
     a.trace_id = L.trace_id;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
-    if (a.P > 1 && (!a.ws || !a.gbar || !a.err)) return (int)cudaErrorInvalidValue;
+    a.stamps = g_stamps;
+    if (a.P > 1 && (!a.ws || !a.gbar || !a.err || a.gp > kGroupCounters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
     switch (L.batch) {
-        case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
+        case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : g_b1s == 6 ? launch_v<1, 1, 6, 6>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
         case 3:
             return g_b34 == 1 ? launch_v<3, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<3, 4, 4, 4>(a, st) : launch_b<3>(a, st);
@@ -632,11 +667,14 @@ int gemv_prepare() {
     int e = 0;
     e |= prepare_b<1>();
     e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
+    e |= prepare_v<1, 1, 6, 6>(Cfg<1>::PART);
+    if (const char *v = getenv("HG_GEMV_B1S")) g_b1s = atoi(v) == 6 ? 6 : 8;
     e |= prepare_v<3, 2, 8, 8>(4096);
     e |= prepare_v<3, 4, 4, 4>(4096);
     e |= prepare_v<4, 2, 8, 8>(4096);
     e |= prepare_v<4, 4, 4, 4>(4096);
     if (const char *v = getenv("HG_GEMV_B34")) g_b34 = atoi(v);
+    if (const char *v = getenv("HG_GEMV_PDL")) g_pdl = atoi(v) != 0;
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     e |= prepare_b<2>();
     e |= prepare_b<3>();
@@ -647,6 +685,22 @@ int gemv_prepare() {
     e |= prepare_b<8>();
     if (gemv_tc_prepare() != 0) g_tc_ok = false;  // no TMA encoder: SIMT only
     return e;
+}
+
+// Measurement: per-CTA globaltimer stamps of every later SIMT GEMV launch (entry, first stage
+// full in consumer warp 0, consumer warp 0 done, producer done) into mapped host memory.
+unsigned long long *g_stamps_dev = nullptr;
+unsigned long long *gemv_stamps_enable(bool on) {
+    if (!on) {
+        g_stamps = nullptr;
+        return g_stamps_host;
+    }
+    if (!g_stamps_host) {
+        if (cudaHostAlloc((void **)&g_stamps_host, 4096 * 4 * 8, cudaHostAllocMapped) != cudaSuccess) return nullptr;
+        if (cudaHostGetDevicePointer((void **)&g_stamps_dev, g_stamps_host, 0) != cudaSuccess) return nullptr;
+    }
+    g_stamps = g_stamps_dev;
+    return g_stamps_host;
 }
 
 int launch_read_bw(const void *p, int64_t bytes, float *sink, void *stream) {

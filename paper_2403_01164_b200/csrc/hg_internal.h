@@ -67,7 +67,10 @@ struct StreamLaunch {
     volatile uint32_t *trace = nullptr;  // debug trace words (mapped host) or NULL
     uint32_t trace_id = 0;
 };
+// SIMT GEMV per-row-group part counters (P > 1) after the 4 words of gbar
+constexpr int kGroupCounters = 1024;
 int launch_gemv_stream(const StreamLaunch &L, void *stream);
+unsigned long long *gemv_stamps_enable(bool on);
 
 // ---------------------------------------------------------------- glue_sm100.cu
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,

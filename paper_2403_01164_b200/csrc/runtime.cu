@@ -159,7 +159,7 @@ struct hg_ctx {
     int64_t next_seq = 0;
     int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
     bool tags = false;      // cfg.handshake == 1 and stream memory operations available
-    uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4]
+    uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4 + kGroupCounters]
     uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr, *gbar = nullptr;
     std::vector<ChunkReq> future;
     size_t fpos = 0;
@@ -1274,8 +1274,8 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
     c->tags = cfg.handshake != 0 && load_memops();
-    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8) * 4));
-    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8) * 4));
+    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
+    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
     c->arrived = c->tagmem;
     c->consumed = c->tagmem + c->nslots;
     c->slot_cnt = c->tagmem + 2 * c->nslots;
@@ -1433,7 +1433,7 @@ HG_API hg_status hg_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t
 }
 
 HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, const void *W_dev,
-                                const float *bias, float *y, void *stream) {
+                                const float *bias, float *y, int64_t seq0, void *stream) {
     if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
     if (c->error) return set_error(HG_ESTATE, "context is in an error state");
     if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
@@ -1448,6 +1448,7 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     if (gemv_use_tc(B)) return set_error(HG_EUNSUPPORTED, "replay covers the SIMT streaming GEMV (batch < %d)",
                                          c->cfg.gemv_tc_min_batch);
     if (p->n_chunks > c->nslots) return set_error(HG_EINVAL, "plan has more chunks than ring slots");
+    if (seq0 < 0) return set_error(HG_EINVAL, "seq0 < 0");
     const int64_t n = p->n_res + p->n_str;
     if (gemv_ws_floats(n, p->K, B) > c->ws_floats) return set_error(HG_EINVAL, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1461,7 +1462,7 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     S.ring = c->ring;
     S.slot_bytes = c->slot_bytes;
     S.nslots = c->nslots;
-    S.seq0 = 0;
+    S.seq0 = seq0;
     S.n_chunks = p->n_str > 0 ? p->n_chunks : 0;
     S.chunk_rows = p->chunk_rows;
     S.n_str = p->n_str;
@@ -1475,6 +1476,17 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     S.timeout_s = c->cfg.timeout_s;
     HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));
     HG_CK(c, cudaEventRecord(c->ev_done, s));
+    return HG_OK;
+}
+
+HG_API hg_status hg_debug_gemv_stamps(uint64_t **out) {
+    if (!out) {
+        gemv_stamps_enable(false);
+        return HG_OK;
+    }
+    unsigned long long *p = gemv_stamps_enable(true);
+    if (!p) return set_error(HG_ECUDA, "cannot allocate mapped stamp memory");
+    *out = (uint64_t *)p;
     return HG_OK;
 }
 

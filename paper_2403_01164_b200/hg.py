@@ -141,10 +141,11 @@ _sig = {
     "hg_layer": (_i32, [_vp, _P(OptLayer), _vp, _i32, _P(LayerTrace), _vp]),
     "hg_stack": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _vp]),
     "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
-    "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp]),
+    "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _i64, _vp]),
     "hg_schedule": (_i32, [_P(Module), _i32, _i64, _i64, _i32, _P(_i64), _P(_i64)]),
     "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "hg_host_isa": (ctypes.c_char_p, []),
+    "hg_debug_gemv_stamps": (_i32, [_P(ctypes.POINTER(ctypes.c_uint64))]),
     "hg_dist_unique_id": (_i32, [_vp]),
     "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
     "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -189,6 +190,18 @@ def hg_abi_version() -> int:
 
 def hg_host_isa() -> str:
     return _lib.hg_host_isa().decode()
+
+
+def hg_debug_gemv_stamps(n_ctas: int, on: bool = True):
+    """Measurement only: enable (on) or disable per-CTA globaltimer stamps in every later SIMT
+    GEMV launch; returns a numpy uint64 view [n_ctas, 4] of the library's mapped stamp array."""
+    import numpy as np
+    if not on:
+        _check(_lib.hg_debug_gemv_stamps(None))
+        return None
+    p = ctypes.POINTER(ctypes.c_uint64)()
+    _check(_lib.hg_debug_gemv_stamps(ctypes.byref(p)))
+    return np.ctypeslib.as_array(p, shape=(4096, 4))[:n_ctas]
 
 
 def hg_config_default() -> Config:
@@ -294,9 +307,9 @@ class Context:
         arr = (OptLayer * len(layers))(*layers)
         _check(_lib.hg_stack(self._h, arr, len(layers), _ptr(h), batch, _stream(stream)))
 
-    def hg_gemv_replay(self, plan, x, W_dev, bias, y, stream=None):
+    def hg_gemv_replay(self, plan, x, W_dev, bias, y, stream=None, seq0=0):
         _check(_lib.hg_gemv_replay(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(bias), _ptr(y),
-                                   _stream(stream)))
+                                   seq0, _stream(stream)))
 
     def hg_gemv(self, x, batch, n, K, W, bias, y, ldy=None, stream=None):
         _check(_lib.hg_gemv(self._h, _ptr(x), batch, n, K, _ptr(W), _ptr(bias), _ptr(y),

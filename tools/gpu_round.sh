@@ -37,8 +37,9 @@ if has full; then
     > $out/full_bench.log 2>&1
   echo "full rc=$?"
   python tools/ncu_summary.py full $out/prof_gemv_step.ncu-rep > $out/full_summary_step.md 2>&1
-  REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_stream \
+  ALPHA=0.24 REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k regex:gemv_stream \
     -o $out/prof_gemv_replay python tools/prof_replay.py > $out/full_replay.log 2>&1
   python tools/ncu_summary.py full $out/prof_gemv_replay.ncu-rep > $out/full_summary_replay.md 2>&1
+  python tools/ncu_summary.py traffic $out/prof_gemv_replay.ncu-rep 0.24 > $out/ncu_gemv_replay_traffic.json 2>&1
   head -40 $out/full_summary_replay.md
 fi

@@ -2,6 +2,8 @@
 
   python tools/ncu_summary.py launches <launches.csv>          per-kernel share of device time
   python tools/ncu_summary.py full <prof.ncu-rep>               key counters of a --set full capture
+  python tools/ncu_summary.py traffic <prof.ncu-rep> <alpha> [B] per-launch DRAM traffic JSON of a
+      tools/prof_replay.py capture (REPS=1: launches qkv, o, fc1, fc2) beside the algorithmic bytes
 """
 import csv
 import io
@@ -60,6 +62,38 @@ def full(path):
     return "\n".join(out)
 
 
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0,
+          "msecond": 1e3, "%": 1.0}
+
+
+def traffic(path, alpha, B=1):
+    """JSON for bench.ncu_traffic(): dram read/write bytes per launch of the replay capture."""
+    import json
+    import os
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2403_01164_b200 import hg
+    txt = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rdr = list(csv.reader(io.StringIO(txt)))
+    hdr, units = rdr[0], rdr[1]
+    H, F = 7168, 28672
+    shapes = [("qkv", 3 * H, H), ("o", H, H), ("fc1", F, H), ("fc2", H, F)]
+    per = {}
+    for (name, N, K), row in zip(shapes, rdr[2:]):
+        d, u = dict(zip(hdr, row)), dict(zip(hdr, units))
+        val = lambda k: float(d[k].replace(",", "")) * _SCALE.get(u.get(k, ""), 1.0)  # noqa: E731
+        p = hg.hg_plan(hg.make_rates(1, 1, 1), N, K, B, 0, hg.FIXED, alpha, 128, 32 << 20)
+        per[name] = {"duration_us": round(val("gpu__time_duration.sum"), 3),
+                     "dram_read_MB": val("dram__bytes_read.sum") / 1e6,
+                     "dram_write_MB": val("dram__bytes_write.sum") / 1e6,
+                     "dram_pct_peak": val("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                     "algorithmic_MB": 2 * K * (p.n_res + p.n_str) / 1e6}
+    return json.dumps({"source": f"ncu --set full of tools/prof_replay.py (hg_gemv_replay, alpha={alpha}, B={B}, "
+                                 "32 MiB chunks)", "per_launch": per}, indent=1)
+
+
 if __name__ == "__main__":
     mode, path = sys.argv[1], sys.argv[2]
-    print(launches(path) if mode == "launches" else full(path))
+    if mode == "traffic":
+        print(traffic(path, float(sys.argv[3]), int(sys.argv[4]) if len(sys.argv) > 4 else 1))
+    else:
+        print(launches(path) if mode == "launches" else full(path))

@@ -29,7 +29,7 @@ def main():
             flush.zero_()
             e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
             e0.record(s)
-            ctx.hg_gemv_replay(p, x, None, None, y, stream=s)
+            ctx.hg_gemv_replay(p, x, None, None, y, stream=s, seq0=0)
             e1.record(s)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3)
