@@ -541,7 +541,7 @@ int prepare_b() {
 int g_cps1 = 1;
 unsigned long long *g_stamps = nullptr;  // device view of mapped host stamps (measurement only)
 unsigned long long *g_stamps_host = nullptr;
-int g_b1s = 8;  // A/B (HG_GEMV_B1S): B = 1 stage count 8 (one CTA per SM) or 6 (~100 KB: two fit, PDL overlap)
+int g_b1s = 8;  // A/B (HG_GEMV_B1S): B = 1 stage count 8 (one CTA per SM), 7 or 6 (<= 115 KB: two fit, PDL overlap)
 int g_b34 = 0;  // A/B (HG_GEMV_B34): B = 3, 4 kernel shape 0 = Cfg (R2,S10,W10), 1 = (R2,S8,W8), 2 = (R4,S4,W4)
 
 }  // namespace
@@ -626,7 +626,11 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
     switch (L.batch) {
-        case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : g_b1s == 6 ? launch_v<1, 1, 6, 6>(a, st) : launch_b<1>(a, st);
+        case 1:
+            return cps > 1 ? launch_v<1, 1, 4, 4>(a, st)
+                 : g_b1s == 6 ? launch_v<1, 1, 6, 6>(a, st)
+                 : g_b1s == 7 ? launch_v<1, 1, 7, 7>(a, st)
+                              : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
         case 3:
             return g_b34 == 1 ? launch_v<3, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<3, 4, 4, 4>(a, st) : launch_b<3>(a, st);
@@ -668,7 +672,8 @@ int gemv_prepare() {
     e |= prepare_b<1>();
     e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
     e |= prepare_v<1, 1, 6, 6>(Cfg<1>::PART);
-    if (const char *v = getenv("HG_GEMV_B1S")) g_b1s = atoi(v) == 6 ? 6 : 8;
+    e |= prepare_v<1, 1, 7, 7>(Cfg<1>::PART);
+    if (const char *v = getenv("HG_GEMV_B1S")) g_b1s = (atoi(v) == 6 || atoi(v) == 7) ? atoi(v) : 8;
     e |= prepare_v<3, 2, 8, 8>(4096);
     e |= prepare_v<3, 4, 4, 4>(4096);
     e |= prepare_v<4, 2, 8, 8>(4096);

@@ -306,3 +306,33 @@ def test_pageable_measure_reports_pin_rate():
                     staging_bytes=64 << 20) as c:
         r = c.hg_measure(_pageable(W), N, K, 1)
         assert np.isfinite(r.v_pin) and r.v_pin > 0 and r.v_link > 0 and r.v_cpu > 0
+
+
+@pytest.mark.parametrize("B,K", [(1, 28672), (3, 12288), (1, 7168)])
+def test_back_to_back_gemv_pdl_ordering(ctx, B, K):
+    """Back-to-back GEMV launches (programmatic dependent launch) where a torch kernel rewrites x
+    right before each one: every launch must see its own x (griddepcontrol.wait before the x copy)
+    and, for P > 1, the per-row-group part counters must reset between launches.  Each result is
+    bit-identical to the same GEMV launched alone."""
+    N = 640
+    xs = [gen.linear_inputs(40 + i, 0, "fc2", B, N, K)[0] for i in range(4)]
+    _, W, b = gen.linear_inputs(40, 0, "fc2", B, N, K)
+    Wd, bd = dev(W), dev_f32(b)
+    alone = []
+    for x in xs:
+        y = torch.empty((B, N), device="cuda")
+        ctx.hg_gemv(dev(x), B, N, K, Wd, bd, y)
+        torch.cuda.synchronize()
+        alone.append(y.cpu().numpy())
+        assert oracle.within_tol(alone[-1], oracle.linear(x, W, b))[0]
+    src = [dev(x) for x in xs]
+    xbuf = torch.empty_like(src[0])
+    ys = [torch.empty((B, N), device="cuda") for _ in range(24)]
+    torch.cuda.synchronize()
+    torch.cuda._sleep(2_000_000)  # queue everything behind a spin so launches run back to back
+    for i, y in enumerate(ys):
+        torch.bitwise_or(src[i % 4], 0, out=xbuf)  # a kernel (not a memcpy) writing x right before the GEMV
+        ctx.hg_gemv(xbuf, B, N, K, Wd, bd, y, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    for i, y in enumerate(ys):
+        assert np.array_equal(y.cpu().numpy().view(np.uint32), alone[i % 4].view(np.uint32)), i
