@@ -188,7 +188,7 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
         try:
             for q in seqs[:3]:
                 ctx.hg_gemv_replay(p, x, Wd, None, y, stream=s, seq0=q)
-        except Exception as e:  # tcgen05 batches: no replay entry point
+        except Exception as e:  # noqa: BLE001
             return {"unavailable": str(e)}
         torch.cuda.synchronize()
         # back to back, GPU held by a spin kernel while the host enqueues
@@ -222,8 +222,12 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     if tot_time <= 0:
         return None
     gbps = tot_bytes / tot_time / 1e9
-    traffic, traffic_detail = ncu_traffic()
-    return {"bound": "hbm", "kernel": "gemv_stream_kernel (persistent per-linear GEMV, TMA bulk staged)",
+    tcmin = ctx.config.gemv_tc_min_batch
+    tc = tcmin > 0 and B >= tcmin
+    traffic, traffic_detail = ncu_traffic() if B == 1 else (None, None)
+    kernel = ("gemv_tc_stream_kernel (tcgen05 M=128 N=16, TMA 2-D tiles; one persistent launch per linear)" if tc
+              else "gemv_stream_kernel (persistent per-linear GEMV, TMA bulk staged)")
+    return {"bound": "hbm", "kernel": kernel,
             "achieved": round(gbps, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4),
             "traffic": traffic, "traffic_detail": traffic_detail,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy BW)" if "hbm_gbs" in pk else "fallback 6650 GB/s",

@@ -135,7 +135,7 @@ typedef struct {
     int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
     double timeout_s;    /* bound on every host wait (default 60 s)                      */
-    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 5; 0 = never) */
+    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 2; 0 = never) */
     int32_t handshake;   /* streamed-chunk synchronisation: 1 = device tags (default): the copy
                             stream writes an arrival tag per chunk (cuStreamWriteValue32) and waits
                             on the slot's consumed tag (cuStreamWaitValue32), one persistent GEMV
@@ -362,8 +362,9 @@ HG_API hg_status hg_gemv(hg_ctx *ctx, const void *x_dev, int batch, int64_t n, i
  * step's launch configuration.  Rotating seq0 across calls walks the whole ring (the bench uses
  * it so that back-to-back replays read more than L2 holds).  Streamed outputs are computed from
  * whatever the ring holds (timing only); resident outputs are exact.  y [batch, N] fp32 device.
- * Batches on the tcgen05 path, seq0 < 0 and plans with more chunks than ring slots return
- * HG_EUNSUPPORTED / HG_EINVAL. */
+ * On the tcgen05 path (batch >= gemv_tc_min_batch) the step launches the resident block and then
+ * one GEMV per chunk, and so does the replay.  seq0 < 0 and plans with more chunks than ring
+ * slots return HG_EINVAL. */
 HG_API hg_status hg_gemv_replay(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
                                 const void *W_dev, const float *bias_dev, float *y_dev, int64_t seq0,
                                 void *stream);

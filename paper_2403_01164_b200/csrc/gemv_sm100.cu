@@ -549,7 +549,7 @@ int g_b34 = 0;  // A/B (HG_GEMV_B34): B = 3, 4 kernel shape 0 = Cfg (R2,S10,W10)
 // Batches >= the calling context's gemv_tc_min_batch run the tcgen05 kernel
 // (gemv_tc_sm100.cu); 0 disables it.  Set per API call by the runtime (one
 // context per host thread), so it is thread-local.
-static thread_local int g_tc_min_batch = 5;
+static thread_local int g_tc_min_batch = 2;
 static bool g_tc_ok = true;  // false when the TMA encoder / tcgen05 setup is unavailable
 
 void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }

@@ -1,9 +1,11 @@
-// gemv_tc_sm100.cu -- tcgen05 tensor-core GEMV for batch 5..8.
+// gemv_tc_sm100.cu -- tcgen05 tensor-core GEMV for batch 2..8.
 //
 // Same contract as gemv_sm100.cu: y[b, j] = sum_k x[b,k] W[j,k] (+bias[j]) with
-// fp32 accumulation.  At batch >= 5 the SIMT kernel spends ~B FMAs per weight
-// and the FMA pipe, not HBM, becomes the limit, so here the contraction runs on
-// the 5th-generation tensor cores while the kernel stays an HBM stream:
+// fp32 accumulation.  From batch 2 the SIMT kernel is instruction-issue bound (per weight it
+// converts bf16 -> fp32 and issues B FMAs, and x's conversion grows with B), measured at 0.43 of
+// the copy peak at B = 2 and 0.37 at B = 4 against 0.58 / 0.55 here (profiles/r01/gemv_batches.md).
+// Here the conversion and the multiply-adds run on the 5th-generation tensor cores and the kernel
+// stays an HBM stream (the batch is padded to N = 16 inside the MMA, the weights are read once):
 //
 //   D[128 rows of W, 16] (TMEM, fp32) += A[128 x 16] (W tile, smem) . B[16 x 16] (x^T, smem)
 //
@@ -17,14 +19,18 @@
 // * warps 2-5 drain the accumulator with tcgen05.ld (32x32b.x16) and write
 //   y (+bias), or the split-K partial.  Two accumulators (TMEM columns 0-15,
 //   16-31) let the epilogue of one work unit overlap the MMAs of the next.
-// * persistent CTAs walk work units (row tile, k-slice); the k-slices and the
-//   deterministic last-arriver reduction are the same scheme as the SIMT kernel
-//   (slice geometry depends on K only, so every launch reduces identically).
+// * persistent CTAs walk work units (row tile, k-slice); the k-slice geometry depends on K only
+//   and partial sums are added by the last arriver in slice order, so every launch reduces every
+//   row identically (split invariance).
+// * gemv_tc_kernel: one buffer per launch (the resident GEMV alone, and the per-chunk fallback);
+//   gemv_tc_stream_kernel: ONE launch per linear over the resident block and every streamed chunk,
+//   gated by the chunk arrival tags, PDL-launched (see below).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -302,6 +308,258 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kStages + 4) + 16;
+constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16; }
+// persistent form: 6 stages (two CTAs per SM) when there are enough units for 2 per SM, else 11
+// stages (one CTA per SM, ~200 KB in flight) so that a small linear still fills its SMs' queues
+constexpr int kStagesWide = 6, kStagesDeep = 11;
+
+// ---------------------------------------------------------------- persistent per-linear form
+// One launch per linear covering the resident block and every streamed chunk (the SIMT kernel's
+// structure, SURVEY 8(a) a3+a4), so small chunks do not each pay a launch and a sub-wave grid.
+// Sources: [resident block] then chunk 0, 1, ... in arrival order; each has its own tensor map (a
+// kernel parameter) over exactly its rows (rows past a source are zero-filled by TMA, never read
+// from a neighbour).  Work unit u = (global tile t = u / S, k-slice s = u % S): a CTA walks its
+// units in increasing order, so it meets the sources in arrival order and waits for a chunk's
+// arrival tag before its first TMA from that chunk.  When every unit of a chunk has finished its
+// MMAs (all TMA reads of the slot done), the last one writes the slot's `consumed` tag.
+constexpr int kMaxSrc = 17;  // resident + up to 16 chunks per launch (else the per-chunk path)
+
+struct TcArgs {
+    CUtensorMap map_x;
+    CUtensorMap maps[kMaxSrc];
+    int64_t rows[kMaxSrc], g0[kMaxSrc], tile0[kMaxSrc + 1];
+    int32_t slot[kMaxSrc];
+    uint32_t tag[kMaxSrc];
+    int n_src;
+    int S;
+    int64_t ks, K, n_total;
+    const float *bias;
+    float *y;
+    int64_t ldy;
+    float *ws;
+    int *counters;
+    const uint32_t *arrived;  // null: every source present (resident / replay)
+    uint32_t *consumed, *slot_cnt, *err;
+    unsigned long long timeout_ns;
+};
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int B, int ST>
+__global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t sW = base;
+    const uint32_t sX = base + ST * kWBytes;
+    const uint32_t bars = sX + ST * kXBytes;
+    uint32_t *tmem_slot = (uint32_t *)(gbase + (bars - base) + 8 * (2 * ST + 4));
+    int *last_flag = (int *)(tmem_slot + 1);
+    auto full = [&](int s) { return bars + 8 * s; };
+    auto empty = [&](int s) { return bars + 8 * (ST + s); };
+    auto tfull = [&](int q) { return bars + 8 * (2 * ST + q); };
+    auto tempty = [&](int q) { return bars + 8 * (2 * ST + 2 + q); };
+
+    // PDL: the next kernel may be scheduled once every CTA of this one runs; x (read by the
+    // producer with every stage) is the only input of the previous kernel, so only the producer
+    // waits (griddepcontrol.wait) before its first TMA.
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; ++s) {
+            mbar_init(full(s), 1);
+            mbar_init(empty(s), 1);
+        }
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(tfull(q), 1);
+            mbar_init(tempty(q), 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.map_x) : "memory");
+        for (int i = 0; i < a.n_src; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[i]) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    const int S = a.S;
+    const int64_t n_units = a.tile0[a.n_src] * S;
+    auto src_of = [&](int64_t t) {
+        int i = 0;
+        while (t >= a.tile0[i + 1]) ++i;
+        return i;
+    };
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            int stage = 0;
+            uint32_t phase = 0;
+            int ready = -1;  // highest source index known to have arrived
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int64_t t = u / S;
+                const int s = (int)(u - t * S);
+                const int i = src_of(t);
+                if (a.arrived && a.slot[i] >= 0 && i > ready) {
+                    const unsigned long long t0 = gtimer();
+                    while ((int32_t)(ld_acquire_u32(a.arrived + a.slot[i]) - a.tag[i]) < 0) {
+                        __nanosleep(64);
+                        if (gtimer() - t0 > a.timeout_ns) {
+                            atomicOr(a.err, 1u);
+                            break;
+                        }
+                    }
+                    ready = i;
+                }
+                const int32_t row0 = (int32_t)((t - a.tile0[i]) * kTileM);
+                const int64_t k0 = (int64_t)s * a.ks;
+                const int64_t k1 = k0 + a.ks < a.K ? k0 + a.ks : a.K;
+                for (int64_t k = k0; k < k1; k += kTileK) {
+                    mbar_wait(empty(stage), phase ^ 1);
+                    mbar_expect_tx(full(stage), kWBytes + kXBytes);
+                    tma_load_2d(sW + stage * kWBytes, &a.maps[i], full(stage), (int32_t)k, row0);
+                    tma_load_2d(sX + stage * kXBytes, &a.map_x, full(stage), (int32_t)k, 0);
+                    if (++stage == ST) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer
+            int stage = 0;
+            uint32_t phase = 0;
+            int it = 0;
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+                mbar_wait(tempty(acc), aphase ^ 1);
+                tc_fence_after();
+                const int64_t t = u / S;
+                const int s = (int)(u - t * S);
+                const int64_t k0 = (int64_t)s * a.ks;
+                const int64_t k1 = k0 + a.ks < a.K ? k0 + a.ks : a.K;
+                const uint32_t d = tmem + (uint32_t)(acc * kUmmaN);
+                uint32_t accum = 0;
+                for (int64_t k = k0; k < k1; k += kTileK) {
+                    mbar_wait(full(stage), phase);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < kTileK / kUmmaK; ++kk) {
+                        const uint64_t da = sw128_desc(sW + stage * kWBytes + kk * kUmmaK * 2);
+                        const uint64_t db = sw128_desc(sX + stage * kXBytes + kk * kUmmaK * 2);
+                        umma(d, da, db, accum);
+                        accum = 1;
+                    }
+                    umma_commit(empty(stage));
+                    if (++stage == ST) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(tfull(acc));
+            }
+        }
+    } else {  // ---------------- epilogue warps 2..5
+        const int quarter = warp & 3;
+        const int et = (warp - 2) * 32 + lane;
+        int it = 0;
+        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+            const int64_t t = u / S;
+            const int s = (int)(u - t * S);
+            const int i = src_of(t);
+            mbar_wait(tfull(acc), aphase);
+            tc_fence_after();
+            uint32_t r[16];
+            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kUmmaN);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                "%14,%15}, [%16];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                  "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+                  "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            mbar_arrive(tempty(acc));
+            // every TMA read of this unit has landed (its MMAs completed): count it for the slot
+            if (a.arrived && a.slot[i] >= 0 && et == 0) {
+                const uint32_t units_i = (uint32_t)((a.tile0[i + 1] - a.tile0[i]) * S);
+                const uint32_t old = atomicAdd(&a.slot_cnt[a.slot[i]], 1u);
+                if (old == units_i - 1) {
+                    atomicExch(&a.slot_cnt[a.slot[i]], 0u);
+                    __threadfence();
+                    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.consumed + a.slot[i]), "r"(a.tag[i])
+                                 : "memory");
+                }
+            }
+            const int64_t lrow = (t - a.tile0[i]) * kTileM + quarter * 32 + lane;
+            const bool valid = lrow < a.rows[i];
+            const int64_t g = a.g0[i] + lrow;
+            if (S == 1) {
+                if (valid) {
+                    const float bb = a.bias ? a.bias[g] : 0.f;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = __uint_as_float(r[b]) + bb;
+                }
+                continue;
+            }
+            if (valid) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * B + b) * a.n_total + g] = __uint_as_float(r[b]);
+            }
+            __threadfence();
+            named_barrier(1, 128);
+            if (et == 0) *last_flag = (atomicAdd(&a.counters[t], 1) == S - 1);
+            named_barrier(1, 128);
+            if (*last_flag) {
+                __threadfence();
+                if (valid) {
+                    const float bb = a.bias ? a.bias[g] : 0.f;
+#pragma unroll
+                    for (int b = 0; b < B; ++b) {
+                        float sum = 0.f;
+                        for (int q0 = 0; q0 < S; q0 += 8) {  // 8 loads in flight, summed in order
+                            float part[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q0 + q < S) part[q] = __ldcg(&a.ws[((int64_t)(q0 + q) * B + b) * a.n_total + g]);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                if (q0 + q < S) sum += part[q];
+                        }
+                        a.y[b * a.ldy + g] = sum + bb;
+                    }
+                }
+                if (et == 0) a.counters[t] = 0;
+            }
+            named_barrier(1, 128);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+}
 
 // ---------------------------------------------------------------- host side
 typedef CUresult (*encode_fn_t)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -353,17 +611,48 @@ int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float 
     return (int)cudaGetLastError();
 }
 
+int g_tc_deep = 0;  // A/B (HG_TC_DEEP=1: 11-stage one-per-SM form below 2 units per SM; measured slower)
+
+template <int B>
+int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    const bool deep = g_tc_deep && units < 2 * sms;
+    int grid = deep ? sms : 2 * sms;
+    if (units < grid) grid = (int)units;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem_for(deep ? kStagesDeep : kStagesWide);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep>, a)
+                         : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide>, a);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
 template <int B>
 int prepare_tc_b() {
-    return (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)kSmemBytes);
+    int e = (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)kSmemBytes);
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_for(kStagesWide));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_for(kStagesDeep));
+    return e;
 }
 
 }  // namespace
 
+int64_t g_slice_max = kSliceMaxTc;  // A/B (HG_TC_SLICE): max k per work unit, multiple of kTileK
+
 GemvGeom gemv_tc_geom(int64_t K) {
     GemvGeom g;
-    const int64_t s0 = (K + kSliceMaxTc - 1) / kSliceMaxTc;
+    const int64_t s0 = (K + g_slice_max - 1) / g_slice_max;
     int64_t ks = (K + s0 - 1) / s0;
     ks = (ks + kTileK - 1) / kTileK * kTileK;
     g.ks = ks;
@@ -376,7 +665,16 @@ int gemv_tc_prepare() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (const char *v = getenv("HG_TC_DEEP")) g_tc_deep = atoi(v);
+    if (const char *v = getenv("HG_TC_SLICE")) {
+        const int64_t sl = atoll(v) / kTileK * kTileK;
+        if (sl >= kTileK) g_slice_max = sl;
+    }
     int e = 0;
+    e |= prepare_tc_b<1>();
+    e |= prepare_tc_b<2>();
+    e |= prepare_tc_b<3>();
+    e |= prepare_tc_b<4>();
     e |= prepare_tc_b<5>();
     e |= prepare_tc_b<6>();
     e |= prepare_tc_b<7>();
@@ -390,11 +688,98 @@ int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n
     if (n <= 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     switch (batch) {
+        case 1: return launch_tc_b<1>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 2: return launch_tc_b<2>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 3: return launch_tc_b<3>(x, K, W, n, bias, y, ldy, ws, counters, st);
+        case 4: return launch_tc_b<4>(x, K, W, n, bias, y, ldy, ws, counters, st);
         case 5: return launch_tc_b<5>(x, K, W, n, bias, y, ldy, ws, counters, st);
         case 6: return launch_tc_b<6>(x, K, W, n, bias, y, ldy, ws, counters, st);
         case 7: return launch_tc_b<7>(x, K, W, n, bias, y, ldy, ws, counters, st);
         case 8: return launch_tc_b<8>(x, K, W, n, bias, y, ldy, ws, counters, st);
         default: return (int)cudaErrorInvalidValue;
+    }
+}
+
+bool gemv_tc_stream_ok(int64_t n_res, int64_t n_chunks) {
+    return (n_res > 0 ? 1 : 0) + n_chunks <= kMaxSrc;
+}
+
+int64_t gemv_tc_stream_tiles(int64_t n_res, int64_t n_str, int64_t chunk_rows, int64_t n_chunks) {
+    int64_t t = (n_res + kTileM - 1) / kTileM;
+    for (int64_t i = 0; i < n_chunks; ++i) {
+        const int64_t r0 = i * chunk_rows;
+        const int64_t rows = chunk_rows < n_str - r0 ? chunk_rows : n_str - r0;
+        t += (rows + kTileM - 1) / kTileM;
+    }
+    return t;
+}
+
+int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
+    const int B = L.batch;
+    if (B < 1 || B > 8) return (int)cudaErrorInvalidValue;
+    const int64_t n_chunks = L.n_str > 0 ? L.n_chunks : 0;
+    if (!gemv_tc_stream_ok(L.n_res, n_chunks)) return (int)cudaErrorInvalidValue;
+    static TcArgs a;  // ~2.5 KB: not on the stack; the launch copies it (one context per host thread)
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    std::memset(&a, 0, sizeof(a));
+    const int64_t K = L.K;
+    if (!make_map(&a.map_x, L.x, K, B, kTileK, kUmmaN)) return (int)cudaErrorInvalidValue;
+    int ns = 0;
+    a.tile0[0] = 0;
+    if (L.n_res > 0) {
+        if (!make_map(&a.maps[ns], L.W_res, K, L.n_res, kTileK, kTileM)) return (int)cudaErrorInvalidValue;
+        a.rows[ns] = L.n_res;
+        a.g0[ns] = 0;
+        a.slot[ns] = -1;
+        a.tag[ns] = 0;
+        a.tile0[ns + 1] = a.tile0[ns] + (L.n_res + kTileM - 1) / kTileM;
+        ++ns;
+    }
+    for (int64_t i = 0; i < n_chunks; ++i) {
+        const int64_t seq = L.seq0 + i;
+        const int64_t slot = seq % (L.nslots > 0 ? L.nslots : 1);
+        const int64_t r0 = i * L.chunk_rows;
+        const int64_t rows = L.chunk_rows < L.n_str - r0 ? L.chunk_rows : L.n_str - r0;
+        if (!make_map(&a.maps[ns], L.ring + slot * L.slot_bytes, K, rows, kTileK, kTileM))
+            return (int)cudaErrorInvalidValue;
+        a.rows[ns] = rows;
+        a.g0[ns] = L.n_res + r0;
+        a.slot[ns] = L.arrived ? (int32_t)slot : -1;
+        a.tag[ns] = (uint32_t)(seq + 1);
+        a.tile0[ns + 1] = a.tile0[ns] + (rows + kTileM - 1) / kTileM;
+        ++ns;
+    }
+    a.n_src = ns;
+    if (ns == 0) return 0;
+    const GemvGeom g = gemv_tc_geom(K);
+    a.S = g.s;
+    a.ks = g.ks;
+    a.K = K;
+    a.n_total = L.n_res + L.n_str;
+    a.bias = L.bias;
+    a.y = L.y;
+    a.ldy = L.ldy;
+    a.ws = L.ws;
+    a.counters = counters;
+    a.arrived = L.arrived;
+    a.consumed = L.consumed;
+    a.slot_cnt = L.slot_cnt;
+    a.err = L.err;
+    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
+    if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
+    if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
+    const int64_t units = a.tile0[ns] * a.S;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (B) {
+        case 1: return launch_tc_stream_b<1>(a, units, st);
+        case 2: return launch_tc_stream_b<2>(a, units, st);
+        case 3: return launch_tc_stream_b<3>(a, units, st);
+        case 4: return launch_tc_stream_b<4>(a, units, st);
+        case 5: return launch_tc_stream_b<5>(a, units, st);
+        case 6: return launch_tc_stream_b<6>(a, units, st);
+        case 7: return launch_tc_stream_b<7>(a, units, st);
+        default: return launch_tc_stream_b<8>(a, units, st);
     }
 }
 

@@ -159,4 +159,8 @@ GemvGeom gemv_tc_geom(int64_t K);
 int gemv_tc_prepare();
 int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
                    float *y, int64_t ldy, float *ws, int *counters, void *stream);
+// persistent per-linear tcgen05 GEMV (resident block + every streamed chunk, arrival tags)
+bool gemv_tc_stream_ok(int64_t n_res, int64_t n_chunks);
+int64_t gemv_tc_stream_tiles(int64_t n_res, int64_t n_str, int64_t chunk_rows, int64_t n_chunks);
+int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream);
 }  // namespace hg

@@ -159,6 +159,7 @@ struct hg_ctx {
     int64_t next_seq = 0;
     int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
     bool tags = false;      // cfg.handshake == 1 and stream memory operations available
+    bool tc_stream = true;  // tcgen05 batches: one persistent launch per linear (HG_TC_STREAM=0: per chunk)
     uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4 + kGroupCounters]
     uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr, *gbar = nullptr;
     std::vector<ChunkReq> future;
@@ -594,7 +595,12 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const int B = (int)p.batch;
     const int64_t K = p.K;
     const bool direct = c->cfg.stream_mode == 1 && !gemv_use_tc(B);
-    if ((c->tags || direct) && !gemv_use_tc(B)) {
+    // tcgen05 batches take the persistent per-linear launch too when the linear's sources fit
+    // its parameter block (resident + <= 16 chunks) and no chunk reuses a slot of the same launch
+    const bool tc = gemv_use_tc(B);
+    const bool tc_stream = tc && c->tags && c->tc_stream &&
+                           gemv_tc_stream_ok(p.n_res, p.n_str > 0 ? p.n_chunks : 0) && p.n_chunks <= c->nslots;
+    if ((c->tags || direct) && (!tc || tc_stream)) {
         // a3 + a4 in ONE persistent launch: resident rows, then each chunk as its arrival tag lands
         // (stream_mode 1: the streamed rows are read by the kernel itself over the link, zero-copy)
         std::vector<ChunkReq> mine;
@@ -644,11 +650,18 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         if (S.trace) {
             c->trace_lin.push_back({S.trace_id, (int64_t)seq0, (int64_t)S.n_chunks, p.n_res, p.n_str, p.K});
         }
+        if (tc_stream &&
+            gemv_tc_stream_tiles(p.n_res, p.n_str, p.chunk_rows, S.n_chunks) > c->n_counters)
+            return set_error(HG_EINVAL, "tcgen05 GEMV: %lld rows need more tile counters than the context has",
+                             (long long)n);
         if (n > 0) {
             size_t i0 = 0, i1 = 0;
             cudaEvent_t e0 = nullptr;
             if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
-            HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv stream launch"));
+            if (tc_stream)
+                HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 stream launch"));
+            else
+                HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv stream launch"));
             c->st.gpu_launches++;
             for (int64_t i = 0; i < S.n_chunks; ++i)  // the slots are free once this GEMV is done
                 HG_CK(c, cudaEventRecord(c->ev_free[(seq0 + i) % c->nslots], s));
@@ -1170,7 +1183,7 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     cfg->collect_stats = 0;
     cfg->wrap_prefetch = 0;
     cfg->timeout_s = 60.0;
-    cfg->gemv_tc_min_batch = 5;
+    cfg->gemv_tc_min_batch = 2;  // measured: SIMT is issue-bound from B = 2 (profiles/r01/gemv_batches.md)
     if (const char *v = getenv("HG_GEMV_TC_MIN_BATCH")) cfg->gemv_tc_min_batch = atoi(v);
     cfg->handshake = 1;
     if (const char *v = getenv("HG_HANDSHAKE")) cfg->handshake = atoi(v);
@@ -1269,11 +1282,14 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
             c->n_counters = std::max(c->n_counters, gemv_counters(cfg.max_n, cfg.max_k, b) + 1);
         }
     gemv_set_tc_min_batch(cfg.gemv_tc_min_batch);
+    // the persistent tcgen05 launch has up to one partial tile per chunk on top
+    c->n_counters = std::max(c->n_counters, (cfg.max_n + 127) / 128 + (int64_t)c->nslots + 2);
     CREATE_CK(cudaMalloc((void **)&c->ws, (size_t)c->ws_floats * 4));
     CREATE_CK(cudaMalloc((void **)&c->counters, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMemset(c->counters, 0, (size_t)c->n_counters * 4));
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
     c->tags = cfg.handshake != 0 && load_memops();
+    if (const char *v = getenv("HG_TC_STREAM")) c->tc_stream = atoi(v) != 0;
     CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
     CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
     c->arrived = c->tagmem;
@@ -1445,10 +1461,24 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     if (bias) HG_TRY(check_ptr(c, bias, true, "bias"));
     const int B = (int)p->batch;
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
-    if (gemv_use_tc(B)) return set_error(HG_EUNSUPPORTED, "replay covers the SIMT streaming GEMV (batch < %d)",
-                                         c->cfg.gemv_tc_min_batch);
     if (p->n_chunks > c->nslots) return set_error(HG_EINVAL, "plan has more chunks than ring slots");
     if (seq0 < 0) return set_error(HG_EINVAL, "seq0 < 0");
+    if (gemv_use_tc(B) && !(c->tc_stream && gemv_tc_stream_ok(p->n_res, p->n_str > 0 ? p->n_chunks : 0))) {
+        // tcgen05 batches without the persistent launch: the step launches the resident block,
+        // then one GEMV per chunk (each gated by stream memops, skipped here)
+        cudaStream_t s = (cudaStream_t)stream;
+        HG_TRY(stream_guard(c, s));
+        if (p->n_res > 0) HG_TRY(gemv(c, x, B, p->K, W_dev, p->n_res, bias, y, p->N, s));
+        for (int64_t i = 0; p->n_str > 0 && i < p->n_chunks; ++i) {
+            const int64_t r0 = i * p->chunk_rows;
+            const int64_t rows = std::min(p->chunk_rows, p->n_str - r0);
+            const int64_t g0 = p->n_res + r0;
+            HG_TRY(gemv(c, x, B, p->K, c->ring + ((seq0 + i) % c->nslots) * c->slot_bytes, rows,
+                        bias ? bias + g0 : nullptr, y + g0, p->N, s));
+        }
+        HG_CK(c, cudaEventRecord(c->ev_done, s));
+        return HG_OK;
+    }
     const int64_t n = p->n_res + p->n_str;
     if (gemv_ws_floats(n, p->K, B) > c->ws_floats) return set_error(HG_EINVAL, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
@@ -1474,7 +1504,13 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     S.gbar = c->gbar;
     S.err = c->err;
     S.timeout_s = c->cfg.timeout_s;
-    HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));
+    if (gemv_use_tc(B)) {
+        if (gemv_tc_stream_tiles(p->n_res, p->n_str, p->chunk_rows, S.n_chunks) > c->n_counters)
+            return set_error(HG_EINVAL, "tcgen05 GEMV: too many tiles for the context's counters");
+        HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 replay"));
+    } else {
+        HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));
+    }
     HG_CK(c, cudaEventRecord(c->ev_done, s));
     return HG_OK;
 }

@@ -131,6 +131,20 @@ def test_split_invariance_gpu_bit_exact(ctx):
     assert np.array_equal(_gemv(ctx, x, W, b, 3), ref)
 
 
+@pytest.mark.parametrize("B", [5, 8])
+def test_split_invariance_tcgen05_bit_exact(ctx, B):
+    """tcgen05 batches: the persistent per-linear launch (resident block + up to 16 chunks, each
+    its own tensor map) and the plain resident GEMV give identical bits for every partition with
+    n_cpu = 0 (rows never depend on the tile they share)."""
+    x, W, b = gen.linear_inputs(14, 0, "fc1", B, 2048, 7168)
+    ref = _linear(ctx, x, W, b, B, 2048, 0.0)  # fully resident
+    assert oracle.within_tol(ref, oracle.linear(x, W, b))[0]
+    for n_res in (0, 128, 1024, 1920):
+        y = _linear(ctx, x, W, b, B, n_res, 1.0)  # the rest streamed: 128-row chunks
+        assert np.array_equal(y, ref), n_res
+    assert np.array_equal(_gemv(ctx, x, W, b, B), ref)
+
+
 def test_cpu_rows_equal_host_lane(ctx):
     x, W, b = gen.linear_inputs(5, 0, "fc1", 2, 1024, 512)
     y = _linear(ctx, x, W, b, 2, 0, 0.0)  # everything on the CPU lane
