@@ -630,6 +630,8 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
             return cps > 1 ? launch_v<1, 1, 4, 4>(a, st)
                  : g_b1s == 6 ? launch_v<1, 1, 6, 6>(a, st)
                  : g_b1s == 7 ? launch_v<1, 1, 7, 7>(a, st)
+                 : g_b1s == 10 ? launch_v<1, 1, 10, 10>(a, st)
+                 : g_b1s == 12 ? launch_v<1, 1, 12, 12>(a, st)
                               : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
         case 3:
@@ -673,7 +675,12 @@ int gemv_prepare() {
     e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
     e |= prepare_v<1, 1, 6, 6>(Cfg<1>::PART);
     e |= prepare_v<1, 1, 7, 7>(Cfg<1>::PART);
-    if (const char *v = getenv("HG_GEMV_B1S")) g_b1s = (atoi(v) == 6 || atoi(v) == 7) ? atoi(v) : 8;
+    e |= prepare_v<1, 1, 10, 10>(Cfg<1>::PART);
+    e |= prepare_v<1, 1, 12, 12>(Cfg<1>::PART);
+    if (const char *v = getenv("HG_GEMV_B1S")) {
+        const int b1s = atoi(v);
+        g_b1s = (b1s == 6 || b1s == 7 || b1s == 10 || b1s == 12) ? b1s : 8;
+    }
     e |= prepare_v<3, 2, 8, 8>(4096);
     e |= prepare_v<3, 4, 4, 4>(4096);
     e |= prepare_v<4, 2, 8, 8>(4096);
