@@ -397,6 +397,17 @@ def run_point(st, args, budget_gb=0.0):
                  "cpu_GBps_by_kind": {k: round(v_kind[k] / 1e9, 2) for k in NAMES},
                  "resident_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if nr == n),
                  "partial_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if 0 < nr < n)}
+    if args.resident > 0 and budget_gb <= 0:
+        # C2 (BJ:8): a fixed fraction r of every linear's rows resident in HBM,
+        # n_res = G * floor(r * (N / G) + 1/2)
+        for l in range(args.layers):
+            for name in NAMES:
+                n = SHAPES[name][0] // world
+                nr = 128 * math.floor(args.resident * (n // 128) + 0.5)
+                if nr > 0:
+                    n_res_map[(l, name)] = nr
+                    W_dev_map[(l, name)] = st["host"][l][name][:nr].cuda()
+        torch.cuda.synchronize()
     layers, plans, all_plans = build_layers(st, args, mode, af, n_res_map, W_dev_map)
     h_dev.copy_(h_host)
 
@@ -625,6 +636,8 @@ def main():
     ap.add_argument("--abench-gamma", type=float, default=0.06)
     ap.add_argument("--pageable", action="store_true",
                     help="NEXT(1): host weights not page-locked; streamed chunks go through the pin lane")
+    ap.add_argument("--resident", type=float, default=0.0,
+                    help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
     args = ap.parse_args()
