@@ -422,17 +422,29 @@ def run_point(st, args, budget_gb=0.0):
             t = torch.tensor([alpha_seed], dtype=torch.float64, device="cuda")
             dist.broadcast(t, 0)
             alpha_seed = float(t.item())
+        def agreed(r):
+            # every rank must run the same number of alpha-benchmark rounds over the same window (each
+            # round runs the stack, whose all-gathers need every rank): take rank 0's decision
+            if world == 1:
+                return r.alpha_bar, bool(r.clamped)
+            t = torch.tensor([r.alpha_bar, 1.0 if r.clamped else 0.0], dtype=torch.float64, device="cuda")
+            dist.broadcast(t, 0)
+            return float(t[0].item()), bool(t[1].item() > 0.5)
+
         res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_seed, gamma=args.abench_gamma, lam=0.02, degree=2,
                                  reps=1, stream=s)
+        alpha_bar, clamped = agreed(res)
         rounds = 1
         # no balance point inside the window: re-centre it on the clamped edge (at most 3 more rounds)
-        while res.clamped and rounds < 4 and 0.0 < res.alpha_bar < 1.0:
-            res = ctx.hg_alpha_bench(layers, h_dev, B, res.alpha_bar, gamma=args.abench_gamma, lam=0.02,
+        while clamped and rounds < 4 and 0.0 < alpha_bar < 1.0:
+            res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_bar, gamma=args.abench_gamma, lam=0.02,
                                      degree=2, reps=1, stream=s)
+            alpha_bar, clamped = agreed(res)
             rounds += 1
         abench = res.as_dict()
         abench["rounds"] = rounds
-        layers, plans, all_plans = build_layers(st, args, hg.FIXED, res.alpha_bar, n_res_map, W_dev_map)
+        abench["alpha_used"] = alpha_bar
+        layers, plans, all_plans = build_layers(st, args, hg.FIXED, alpha_bar, n_res_map, W_dev_map)
         h_dev.copy_(h_host)
 
     def barrier():
