@@ -340,6 +340,12 @@ def cpu_rate_per_kind(st):
     return st["v_kind"]
 
 
+def resident_rows(r, n, G=128):
+    """Rows of an n-row linear kept in HBM for a resident fraction r: G * floor(r * (n / G) + 1/2)
+    (the same rule the oracle's partition follows)."""
+    return G * math.floor(r * (n // G) + 0.5)
+
+
 def build_layers(st, args, mode, af, n_res_map, W_dev_map):
     hg = st["hg"]
     ctx, world, B = st["ctx"], st["world"], st["B"]
@@ -402,8 +408,7 @@ def run_point(st, args, budget_gb=0.0):
         # n_res = G * floor(r * (N / G) + 1/2)
         for l in range(args.layers):
             for name in NAMES:
-                n = SHAPES[name][0] // world
-                nr = 128 * math.floor(args.resident * (n // 128) + 0.5)
+                nr = resident_rows(args.resident, SHAPES[name][0] // world)
                 if nr > 0:
                     n_res_map[(l, name)] = nr
                     W_dev_map[(l, name)] = st["host"][l][name][:nr].cuda()
