@@ -403,7 +403,7 @@ def run_point(st, args, budget_gb=0.0):
                  "cpu_GBps_by_kind": {k: round(v_kind[k] / 1e9, 2) for k in NAMES},
                  "resident_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if nr == n),
                  "partial_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if 0 < nr < n)}
-    if args.resident > 0 and budget_gb <= 0:
+    if getattr(args, "resident", 0.0) > 0 and budget_gb <= 0:
         # C2 (BJ:8): a fixed fraction r of every linear's rows resident in HBM,
         # n_res = G * floor(r * (N / G) + 1/2)
         for l in range(args.layers):

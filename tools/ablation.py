@@ -52,7 +52,7 @@ def main():
     bench.set_model(a.model)
     args = argparse.Namespace(steps=a.steps, warmup=max(3, a.warmup), batch=1, layers=bench.LAYERS, alpha=None,
                               chunk_mb=32, ring_mb=4096, threads=0, breakdown=True, abench=True,
-                              abench_gamma=0.06, hbm_budget_gb=0.0, pageable=False)
+                              abench_gamma=0.06, hbm_budget_gb=0.0, pageable=False, resident=0.0)
     st = bench.prepare(args)
     hg = st["hg"]
     base_ctx = st["ctx"]
