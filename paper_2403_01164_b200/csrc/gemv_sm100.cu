@@ -702,6 +702,7 @@ int gemv_prepare() {
 // Measurement: per-CTA globaltimer stamps of every later SIMT GEMV launch (entry, first stage
 // full in consumer warp 0, consumer warp 0 done, producer done) into mapped host memory.
 unsigned long long *g_stamps_dev = nullptr;
+unsigned long long *gemv_stamps_dev() { return g_stamps; }
 unsigned long long *gemv_stamps_enable(bool on) {
     if (!on) {
         g_stamps = nullptr;

@@ -341,6 +341,7 @@ struct TcArgs {
     const uint32_t *arrived;  // null: every source present (resident / replay)
     uint32_t *consumed, *slot_cnt, *err;
     unsigned long long timeout_ns;
+    unsigned long long *stamps;  // measurement: [CTA][4] globaltimer (entry, first MMA stage, epilogue done, exit)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -374,6 +375,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     // producer with every stage) is the only input of the previous kernel, so only the producer
     // waits (griddepcontrol.wait) before its first TMA.
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 0] = gtimer();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -385,18 +387,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             mbar_init(tempty(q), 128);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.map_x) : "memory");
-        for (int i = 0; i < a.n_src; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[i]) : "memory");
     }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    __syncthreads();  // barriers initialised: the producer starts at once; TMEM is allocated meanwhile
+    uint32_t tmem = 0;
+    if (warp >= 1) {  // MMA warp allocates; warps 1-5 meet on named barrier 2 (the producer never waits)
+        if (warp == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot))
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
+        named_barrier(2, kThreads - 32);
+        tc_fence_after();
+        tmem = *tmem_slot;
     }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
 
     const int S = a.S;
     const int64_t n_units = a.tile0[a.n_src] * S;
@@ -407,15 +411,28 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     };
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            asm volatile("griddepcontrol.wait;" ::: "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.map_x) : "memory");
+            for (int i = 0; i < a.n_src; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[i]) : "memory");
             int stage = 0;
             uint32_t phase = 0;
             int ready = -1;  // highest source index known to have arrived
+            // W does not depend on the previous kernel, x does: the first ST stages get their W tile at
+            // once and their x tile after griddepcontrol.wait (each stage's barrier expects both)
+            bool dep = false;
+            int pend = 0, pst[ST];
+            int32_t pk[ST];
+            auto flush_x = [&]() {
+                asm volatile("griddepcontrol.wait;" ::: "memory");
+                for (int q = 0; q < pend; ++q) tma_load_2d(sX + pst[q] * kXBytes, &a.map_x, full(pst[q]), pk[q], 0);
+                pend = 0;
+                dep = true;
+            };
             for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const int64_t t = u / S;
                 const int s = (int)(u - t * S);
                 const int i = src_of(t);
                 if (a.arrived && a.slot[i] >= 0 && i > ready) {
+                    if (!dep) flush_x();
                     const unsigned long long t0 = gtimer();
                     while ((int32_t)(ld_acquire_u32(a.arrived + a.slot[i]) - a.tag[i]) < 0) {
                         __nanosleep(64);
@@ -433,13 +450,20 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                     mbar_wait(empty(stage), phase ^ 1);
                     mbar_expect_tx(full(stage), kWBytes + kXBytes);
                     tma_load_2d(sW + stage * kWBytes, &a.maps[i], full(stage), (int32_t)k, row0);
-                    tma_load_2d(sX + stage * kXBytes, &a.map_x, full(stage), (int32_t)k, 0);
+                    if (dep) {
+                        tma_load_2d(sX + stage * kXBytes, &a.map_x, full(stage), (int32_t)k, 0);
+                    } else {
+                        pst[pend] = stage;
+                        pk[pend] = (int32_t)k;
+                        if (++pend == ST) flush_x();  // before any stage could be waited on again
+                    }
                     if (++stage == ST) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
             }
+            if (!dep) flush_x();
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
@@ -460,6 +484,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 for (int64_t k = k0; k < k1; k += kTileK) {
                     mbar_wait(full(stage), phase);
                     tc_fence_after();
+                    if (a.stamps && it == 0 && k == k0) a.stamps[blockIdx.x * 4 + 1] = gtimer();
 #pragma unroll
                     for (int kk = 0; kk < kTileK / kUmmaK; ++kk) {
                         const uint64_t da = sw128_desc(sW + stage * kWBytes + kk * kUmmaK * 2);
@@ -554,11 +579,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             named_barrier(1, 128);
         }
     }
+    if (a.stamps && warp == 2 && lane == 0) a.stamps[blockIdx.x * 4 + 2] = gtimer();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 3] = gtimer();
 }
 
 // ---------------------------------------------------------------- host side
@@ -767,6 +794,7 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.slot_cnt = L.slot_cnt;
     a.err = L.err;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
+    a.stamps = gemv_stamps_dev();
     if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     const int64_t units = a.tile0[ns] * a.S;

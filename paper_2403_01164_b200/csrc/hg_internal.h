@@ -71,6 +71,7 @@ struct StreamLaunch {
 constexpr int kGroupCounters = 1024;
 int launch_gemv_stream(const StreamLaunch &L, void *stream);
 unsigned long long *gemv_stamps_enable(bool on);
+unsigned long long *gemv_stamps_dev();  // NULL unless hg_debug_gemv_stamps enabled them
 
 // ---------------------------------------------------------------- glue_sm100.cu
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,
