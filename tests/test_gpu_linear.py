@@ -145,6 +145,19 @@ def test_split_invariance_tcgen05_bit_exact(ctx, B):
     assert np.array_equal(_gemv(ctx, x, W, b, B), ref)
 
 
+@pytest.mark.parametrize("B", [2, 4, 8])
+@pytest.mark.parametrize("K", [64, 200, 1032])
+def test_tcgen05_persistent_few_stages(ctx, B, K):
+    """Persistent tcgen05 launch with fewer k-stages per CTA than ring stages (K = 64: one stage)
+    and a K that is not a multiple of the 64-wide tile (zero-filled tail): the x tiles deferred
+    behind griddepcontrol.wait are still issued; resident + streamed rows match the oracle."""
+    x, W, b = gen.linear_inputs(19, 0, "o", B, 1536, K)
+    for n_res, alpha in ((0, 1.0), (128, 1.0), (512, 0.5)):
+        y = _linear(ctx, x, W, b, B, n_res, alpha)
+        ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+        assert ok, (n_res, alpha, worst)
+
+
 def test_cpu_rows_equal_host_lane(ctx):
     x, W, b = gen.linear_inputs(5, 0, "fc1", 2, 1024, 512)
     y = _linear(ctx, x, W, b, 2, 0, 0.0)  # everything on the CPU lane

@@ -43,3 +43,7 @@ if has full; then
   python tools/ncu_summary.py traffic $out/prof_gemv_replay.ncu-rep 0.24 > $out/ncu_gemv_replay_traffic.json 2>&1
   head -40 $out/full_summary_replay.md
 fi
+if has batches; then
+  for b in 1 2 4 8; do B=$b timeout 120 python tools/replay_roofline.py >> $out/replay.jsonl 2>&1; done; cat $out/replay.jsonl
+  for b in 8; do timeout 900 python bench.py --batch $b --no-cpu-baseline > $out/bench_b$b.json 2> $out/bench_b$b.err; echo "b$b rc=$?"; done
+fi
