@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kStages + 4) + 16;
-constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16; }
+constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16 + 16 * 8 + 16 * 4; }
 // persistent form: 6 stages (two CTAs per SM) when there are enough units for 2 per SM, else 11
 // stages (one CTA per SM, ~200 KB in flight) so that a small linear still fills its SMs' queues
 constexpr int kStagesWide = 6, kStagesDeep = 11;
@@ -342,6 +342,7 @@ struct TcArgs {
     uint32_t *consumed, *slot_cnt, *err;
     unsigned long long timeout_ns;
     unsigned long long *stamps;  // measurement: [CTA][4] globaltimer (entry, first MMA stage, epilogue done, exit)
+    uint32_t *work;              // DYN: [ticket, exit count] of this launch (zero at launch, reset at exit)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -355,7 +356,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-template <int B, int ST>
+template <int B, int ST, bool DYN>
 __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -370,6 +371,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     auto empty = [&](int s) { return bars + 8 * (ST + s); };
     auto tfull = [&](int q) { return bars + 8 * (2 * ST + q); };
     auto tempty = [&](int q) { return bars + 8 * (2 * ST + 2 + q); };
+    // DYN: work units handed out by a global ticket counter; the producer passes each unit id to
+    // the MMA and epilogue warps through a 16-entry smem queue (at most ST + 3 units are in flight
+    // between producer and epilogue, so a slot is never lapped)
+    const uint32_t uqbar0 = bars + 8 * (2 * ST + 4) + 16;
+    int32_t *uq = (int32_t *)(gbase + (bars - base) + 8 * (2 * ST + 4) + 16 + 16 * 8);
+    auto uqbar = [&](int q) { return uqbar0 + 8 * q; };
 
     // PDL: the next kernel may be scheduled once every CTA of this one runs; x (read by the
     // producer with every stage) is the only input of the previous kernel, so only the producer
@@ -386,6 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             mbar_init(tfull(q), 1);
             mbar_init(tempty(q), 128);
         }
+        if (DYN)
+            for (int q = 0; q < 16; ++q) mbar_init(uqbar(q), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();  // barriers initialised: the producer starts at once; TMEM is allocated meanwhile
@@ -427,7 +436,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 pend = 0;
                 dep = true;
             };
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+            int qi = 0;
+            for (int64_t u = DYN ? -1 : blockIdx.x;; u += gridDim.x) {
+                if (DYN) {
+                    const uint32_t tk = atomicAdd(a.work, 1u);
+                    u = tk < (uint64_t)n_units ? (int64_t)tk : -1;
+                    uq[qi & 15] = (int32_t)u;
+                    mbar_arrive(uqbar(qi & 15));
+                    ++qi;
+                    if (u < 0) break;
+                } else if (u >= n_units) {
+                    break;
+                }
                 const int64_t t = u / S;
                 const int s = (int)(u - t * S);
                 const int i = src_of(t);
@@ -470,7 +490,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+            for (int64_t u = blockIdx.x;; u += gridDim.x, ++it) {
+                if (DYN) {
+                    mbar_wait(uqbar(it & 15), (uint32_t)((it >> 4) & 1));
+                    u = uq[it & 15];
+                    if (u < 0) break;
+                } else if (u >= n_units) {
+                    break;
+                }
                 const int acc = it & 1;
                 const uint32_t aphase = (uint32_t)((it >> 1) & 1);
                 mbar_wait(tempty(acc), aphase ^ 1);
@@ -505,7 +532,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
         const int quarter = warp & 3;
         const int et = (warp - 2) * 32 + lane;
         int it = 0;
-        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        for (int64_t u = blockIdx.x;; u += gridDim.x, ++it) {
+            if (DYN) {
+                mbar_wait(uqbar(it & 15), (uint32_t)((it >> 4) & 1));
+                u = uq[it & 15];
+                if (u < 0) break;
+            } else if (u >= n_units) {
+                break;
+            }
             const int acc = it & 1;
             const uint32_t aphase = (uint32_t)((it >> 1) & 1);
             const int64_t t = u / S;
@@ -562,13 +596,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
 #pragma unroll
                     for (int b = 0; b < B; ++b) {
                         float sum = 0.f;
-                        for (int q0 = 0; q0 < S; q0 += 8) {  // 8 loads in flight, summed in order
-                            float part[8];
+                        for (int q0 = 0; q0 < S; q0 += 16) {  // 16 loads in flight, summed in order
+                            float part[16];
 #pragma unroll
-                            for (int q = 0; q < 8; ++q)
+                            for (int q = 0; q < 16; ++q)
                                 if (q0 + q < S) part[q] = __ldcg(&a.ws[((int64_t)(q0 + q) * B + b) * a.n_total + g]);
 #pragma unroll
-                            for (int q = 0; q < 8; ++q)
+                            for (int q = 0; q < 16; ++q)
                                 if (q0 + q < S) sum += part[q];
                         }
                         a.y[b * a.ldy + g] = sum + bb;
@@ -586,6 +620,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
     if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 3] = gtimer();
+    if (DYN && threadIdx.x == 0) {  // the last CTA out resets this launch's ticket slot
+        __threadfence();
+        if (atomicAdd(a.work + 1, 1u) == gridDim.x - 1) {
+            atomicExch(a.work, 0u);
+            atomicExch(a.work + 1, 0u);
+        }
+    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -638,6 +679,7 @@ int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float 
     return (int)cudaGetLastError();
 }
 
+int g_tc_dyn = 0;   // A/B (HG_TC_DYN=1: work units from a ticket counter; measured slower, profiles/r01/gemv_batches.md)
 int g_tc_deep = 0;  // A/B (HG_TC_DEEP=1: 11-stage one-per-SM form below 2 units per SM; measured slower)
 
 template <int B>
@@ -656,8 +698,11 @@ int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cudaError_t e = deep ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep>, a)
-                         : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide>, a);
+    const bool dyn = a.work != nullptr;
+    cudaError_t e = deep ? (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, true>, a)
+                                : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, false>, a))
+                         : (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, true>, a)
+                                : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, false>, a));
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
@@ -666,10 +711,14 @@ template <int B>
 int prepare_tc_b() {
     int e = (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes);
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_for(kStagesWide));
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem_for(kStagesDeep));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesDeep));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep, true>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesDeep));
     return e;
 }
 
@@ -693,6 +742,7 @@ int gemv_tc_prepare() {
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (const char *v = getenv("HG_TC_DEEP")) g_tc_deep = atoi(v);
+    if (const char *v = getenv("HG_TC_DYN")) g_tc_dyn = atoi(v);
     if (const char *v = getenv("HG_TC_SLICE")) {
         const int64_t sl = atoll(v) / kTileK * kTileK;
         if (sl >= kTileK) g_slice_max = sl;
@@ -795,6 +845,7 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.err = L.err;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
     a.stamps = gemv_stamps_dev();
+    a.work = g_tc_dyn ? L.work : nullptr;
     if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     const int64_t units = a.tile0[ns] * a.S;

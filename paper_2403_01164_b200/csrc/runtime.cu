@@ -160,6 +160,8 @@ struct hg_ctx {
     int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
     bool tags = false;      // cfg.handshake == 1 and stream memory operations available
     bool tc_stream = true;  // tcgen05 batches: one persistent launch per linear (HG_TC_STREAM=0: per chunk)
+    uint32_t *work = nullptr;  // device: [kWorkSlots][ticket, exit] for the tcgen05 launches' work queues
+    uint64_t work_seq = 0;     // launches so far (slot = seq mod kWorkSlots; a slot is zero again at exit)
     uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4 + kGroupCounters]
     uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr, *gbar = nullptr;
     std::vector<ChunkReq> future;
@@ -658,8 +660,10 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
             size_t i0 = 0, i1 = 0;
             cudaEvent_t e0 = nullptr;
             if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
-            if (tc_stream)
+            if (tc_stream) {
+                S.work = c->work + 2 * (c->work_seq++ % kWorkSlots);
                 HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 stream launch"));
+            }
             else
                 HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv stream launch"));
             c->st.gpu_launches++;
@@ -1290,8 +1294,9 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
     c->tags = cfg.handshake != 0 && load_memops();
     if (const char *v = getenv("HG_TC_STREAM")) c->tc_stream = atoi(v) != 0;
-    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
-    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
+    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters + 2 * kWorkSlots) * 4));
+    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters + 2 * kWorkSlots) * 4));
+    c->work = c->tagmem + 3 * c->nslots + 8 + kGroupCounters;
     c->arrived = c->tagmem;
     c->consumed = c->tagmem + c->nslots;
     c->slot_cnt = c->tagmem + 2 * c->nslots;
@@ -1507,6 +1512,7 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     if (gemv_use_tc(B)) {
         if (gemv_tc_stream_tiles(p->n_res, p->n_str, p->chunk_rows, S.n_chunks) > c->n_counters)
             return set_error(HG_EINVAL, "tcgen05 GEMV: too many tiles for the context's counters");
+        S.work = c->work + 2 * (c->work_seq++ % kWorkSlots);
         HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 replay"));
     } else {
         HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));
