@@ -554,10 +554,17 @@ static bool g_tc_ok = true;  // false when the TMA encoder / tcgen05 setup is un
 
 void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }
 
-bool gemv_use_tc(int batch) { return g_tc_ok && g_tc_min_batch > 0 && batch >= g_tc_min_batch; }
+// Long rows (K > g_tc_long_k) take the tcgen05 kernel at every batch: the SIMT kernel splits them
+// into K-parts whose reduction and row-group imbalance cost more than the tensor-core kernel's
+// k-slices (measured: OPT-30B fc2, K = 28672, 24.1 vs 19.0 us per launch at B = 1).  The choice
+// depends on (batch, K) only, so every partition of a linear runs the same kernel.
+static int64_t g_tc_long_k = 8192;
+bool gemv_use_tc(int batch, int64_t K) {
+    return g_tc_ok && g_tc_min_batch > 0 && (batch >= g_tc_min_batch || (g_tc_long_k > 0 && K > g_tc_long_k));
+}
 
 GemvGeom gemv_geom(int64_t K, int batch) {
-    if (gemv_use_tc(batch)) return gemv_tc_geom(K);
+    if (gemv_use_tc(batch, K)) return gemv_tc_geom(K);
     GemvGeom g;
     const int64_t pm = part_max(batch);
     const int64_t P = (K + pm - 1) / pm;
@@ -570,7 +577,7 @@ GemvGeom gemv_geom(int64_t K, int batch) {
 }
 
 int64_t gemv_ws_floats(int64_t n, int64_t K, int batch) {
-    if (gemv_use_tc(batch)) {
+    if (gemv_use_tc(batch, K)) {
         const GemvGeom g = gemv_tc_geom(K);
         return g.s > 1 ? (int64_t)g.s * batch * n : 0;
     }
@@ -579,7 +586,7 @@ int64_t gemv_ws_floats(int64_t n, int64_t K, int batch) {
 }
 
 int64_t gemv_counters(int64_t n, int64_t K, int batch) {
-    if (gemv_use_tc(batch)) {
+    if (gemv_use_tc(batch, K)) {
         const GemvGeom g = gemv_tc_geom(K);
         return (n + g.rows_per_cta - 1) / g.rows_per_cta;
     }
@@ -649,7 +656,7 @@ int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, c
                 float *y, int64_t ldy, float *ws, int *counters, uint32_t *gbar, uint32_t *err,
                 void *stream) {
     if (n <= 0) return 0;
-    if (gemv_use_tc(batch)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
+    if (gemv_use_tc(batch, K)) return launch_gemv_tc(x, batch, K, W, n, bias, y, ldy, ws, counters, stream);
     StreamLaunch L{};
     L.x = x;
     L.batch = batch;
@@ -687,6 +694,7 @@ int gemv_prepare() {
     e |= prepare_v<4, 4, 4, 4>(4096);
     if (const char *v = getenv("HG_GEMV_B34")) g_b34 = atoi(v);
     if (const char *v = getenv("HG_GEMV_PDL")) g_pdl = atoi(v) != 0;
+    if (const char *v = getenv("HG_TC_LONG_K")) g_tc_long_k = atoll(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     e |= prepare_b<2>();
     e |= prepare_b<3>();

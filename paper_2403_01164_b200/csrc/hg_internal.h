@@ -36,7 +36,7 @@ int64_t gemv_counters(int64_t n, int64_t K, int batch);
 int launch_gemv(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
                 float *y, int64_t ldy, float *ws, int *counters, uint32_t *gbar, uint32_t *err,
                 void *stream);
-bool gemv_use_tc(int batch);
+bool gemv_use_tc(int batch, int64_t K);
 
 // One persistent SIMT launch over the GPU lanes of a linear: resident rows [0, n_res) of W_res,
 // then streamed chunk c (rows [n_res + c*chunk_rows, ...)) in ring slot (seq0 + c) % nslots.

@@ -596,10 +596,10 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const hg_plan_t &p = L.plan;
     const int B = (int)p.batch;
     const int64_t K = p.K;
-    const bool direct = c->cfg.stream_mode == 1 && !gemv_use_tc(B);
+    const bool direct = c->cfg.stream_mode == 1 && !gemv_use_tc(B, K);
     // tcgen05 batches take the persistent per-linear launch too when the linear's sources fit
     // its parameter block (resident + <= 16 chunks) and no chunk reuses a slot of the same launch
-    const bool tc = gemv_use_tc(B);
+    const bool tc = gemv_use_tc(B, K);
     const bool tc_stream = tc && c->tags && c->tc_stream &&
                            gemv_tc_stream_ok(p.n_res, p.n_str > 0 ? p.n_chunks : 0) && p.n_chunks <= c->nslots;
     if ((c->tags || direct) && (!tc || tc_stream)) {
@@ -1468,7 +1468,7 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     if (p->n_chunks > c->nslots) return set_error(HG_EINVAL, "plan has more chunks than ring slots");
     if (seq0 < 0) return set_error(HG_EINVAL, "seq0 < 0");
-    if (gemv_use_tc(B) && !(c->tc_stream && gemv_tc_stream_ok(p->n_res, p->n_str > 0 ? p->n_chunks : 0))) {
+    if (gemv_use_tc(B, p->K) && !(c->tc_stream && gemv_tc_stream_ok(p->n_res, p->n_str > 0 ? p->n_chunks : 0))) {
         // tcgen05 batches without the persistent launch: the step launches the resident block,
         // then one GEMV per chunk (each gated by stream memops, skipped here)
         cudaStream_t s = (cudaStream_t)stream;
@@ -1509,7 +1509,7 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     S.gbar = c->gbar;
     S.err = c->err;
     S.timeout_s = c->cfg.timeout_s;
-    if (gemv_use_tc(B)) {
+    if (gemv_use_tc(B, p->K)) {
         if (gemv_tc_stream_tiles(p->n_res, p->n_str, p->chunk_rows, S.n_chunks) > c->n_counters)
             return set_error(HG_EINVAL, "tcgen05 GEMV: too many tiles for the context's counters");
         S.work = c->work + 2 * (c->work_seq++ % kWorkSlots);
