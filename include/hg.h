@@ -135,7 +135,8 @@ typedef struct {
     int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
     double timeout_s;    /* bound on every host wait (default 60 s)                      */
-    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 2; 0 = never) */
+    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 2; 0 = never); below it,
+                                  rows with K > 8192 also do (HG_TC_LONG_K=0 turns that off) */
     int32_t handshake;   /* streamed-chunk synchronisation: 1 = device tags (default): the copy
                             stream writes an arrival tag per chunk (cuStreamWriteValue32) and waits
                             on the slot's consumed tag (cuStreamWaitValue32), one persistent GEMV
