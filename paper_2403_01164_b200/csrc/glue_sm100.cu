@@ -9,6 +9,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include <cstdint>
 
 #include "hg_internal.h"
@@ -18,6 +20,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr float kLnEps = 1e-5f;
+
+// Programmatic dependent launch: every glue kernel is launched with PDL, lets the next kernel (the
+// GEMV, whose W stream does not depend on it) launch at once, and waits for the previous kernel's
+// results before touching memory.
+__device__ __forceinline__ void pdl_enter() {
+    if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
 
 __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162float(v); }
 
@@ -67,6 +77,7 @@ __device__ void layernorm_row(Get get, int64_t H, const float *g, const float *b
 __global__ void layernorm_kernel(const __nv_bfloat16 *__restrict__ h, int64_t H,
                                  const float *__restrict__ g, const float *__restrict__ b,
                                  __nv_bfloat16 *__restrict__ out) {
+    pdl_enter();
     __shared__ float red[32];
     const __nv_bfloat16 *row = h + blockIdx.x * H;
     layernorm_row([&](int64_t i) { return bf(row[i]); }, H, g, b, out + blockIdx.x * H, red);
@@ -77,6 +88,7 @@ __global__ void residual_ln_kernel(const __nv_bfloat16 *__restrict__ h, const fl
                                    int64_t H, __nv_bfloat16 *__restrict__ h1,
                                    const float *__restrict__ g, const float *__restrict__ b,
                                    __nv_bfloat16 *__restrict__ a2) {
+    pdl_enter();
     __shared__ float red[32];
     const int64_t off = blockIdx.x * H;
     for (int64_t i = threadIdx.x; i < H; i += kThreads)
@@ -90,6 +102,7 @@ __global__ void residual_ln_kernel(const __nv_bfloat16 *__restrict__ h, const fl
 __global__ void join_kernel(float *__restrict__ y, int64_t ldy, int64_t col0, int64_t ncols,
                             int batch, const float *__restrict__ ycpu, int64_t ldsrc,
                             const float *__restrict__ bias) {
+    pdl_enter();
     const int64_t total = (int64_t)batch * ncols;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -101,6 +114,7 @@ __global__ void join_kernel(float *__restrict__ y, int64_t ldy, int64_t col0, in
 
 __global__ void slice_bf16_kernel(const float *__restrict__ y, int64_t ldy, int64_t col0,
                                   int64_t ncols, int batch, __nv_bfloat16 *__restrict__ out) {
+    pdl_enter();
     const int64_t total = (int64_t)batch * ncols;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -111,6 +125,7 @@ __global__ void slice_bf16_kernel(const float *__restrict__ y, int64_t ldy, int6
 
 __global__ void relu_bf16_kernel(const float *__restrict__ y, int64_t total,
                                  __nv_bfloat16 *__restrict__ out) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = __float2bfloat16_rn(y[i] > 0.f ? y[i] : 0.f);  // +0 for -0 and NaN (host mirror)
@@ -118,6 +133,7 @@ __global__ void relu_bf16_kernel(const float *__restrict__ y, int64_t total,
 
 __global__ void residual_kernel(const __nv_bfloat16 *__restrict__ h1, const float *__restrict__ y,
                                 int64_t total, __nv_bfloat16 *__restrict__ out) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x)
         out[i] = __float2bfloat16_rn(__fadd_rn(bf(h1[i]), y[i]));
@@ -126,6 +142,7 @@ __global__ void residual_kernel(const __nv_bfloat16 *__restrict__ h1, const floa
 // y[b, p*n_local + j] = gbuf[p][b][j]
 __global__ void gather_permute_kernel(const float *__restrict__ gbuf, int P, int batch,
                                       int64_t n_local, float *__restrict__ y) {
+    pdl_enter();
     const int64_t total = (int64_t)P * batch * n_local;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -142,54 +159,61 @@ inline unsigned grid_for(int64_t total) {
     return (unsigned)(g < 1 ? 1 : g);
 }
 
+template <typename... Exp, typename... Act>
+int pdl_launch(void (*kernel)(Exp...), unsigned grid, void *stream, Act &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
 }  // namespace
 
 int launch_join(float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch, const float *ycpu,
                 int64_t ldsrc, const float *bias, void *stream) {
     if (ncols <= 0) return 0;
-    join_kernel<<<grid_for(batch * ncols), kThreads, 0, (cudaStream_t)stream>>>(y, ldy, col0, ncols,
-                                                                               batch, ycpu, ldsrc, bias);
-    return (int)cudaGetLastError();
+    return pdl_launch(join_kernel, grid_for(batch * ncols), stream, y, ldy, col0, ncols, batch, ycpu, ldsrc, bias);
 }
 
 int launch_layernorm(const void *h, int64_t H, int batch, const float *g, const float *b, void *out,
                      void *stream) {
-    layernorm_kernel<<<batch, kThreads, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16 *)h, H, g, b, (__nv_bfloat16 *)out);
-    return (int)cudaGetLastError();
+    return pdl_launch(layernorm_kernel, (unsigned)batch, stream, (const __nv_bfloat16 *)h, H, g, b,
+                      (__nv_bfloat16 *)out);
 }
 
 int launch_slice_to_bf16(const float *y, int64_t ldy, int64_t col0, int64_t ncols, int batch,
                          void *out, void *stream) {
-    slice_bf16_kernel<<<grid_for(batch * ncols), kThreads, 0, (cudaStream_t)stream>>>(
-        y, ldy, col0, ncols, batch, (__nv_bfloat16 *)out);
-    return (int)cudaGetLastError();
+    return pdl_launch(slice_bf16_kernel, grid_for(batch * ncols), stream, y, ldy, col0, ncols, batch,
+                      (__nv_bfloat16 *)out);
 }
 
 int launch_residual_ln(const void *h, const float *y, int64_t H, int batch, void *h1,
                        const float *g, const float *b, void *a2, void *stream) {
-    residual_ln_kernel<<<batch, kThreads, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16 *)h, y, H, (__nv_bfloat16 *)h1, g, b, (__nv_bfloat16 *)a2);
-    return (int)cudaGetLastError();
+    return pdl_launch(residual_ln_kernel, (unsigned)batch, stream, (const __nv_bfloat16 *)h, y, H,
+                      (__nv_bfloat16 *)h1, g, b, (__nv_bfloat16 *)a2);
 }
 
 int launch_relu_bf16(const float *y, int64_t n, int batch, void *out, void *stream) {
-    relu_bf16_kernel<<<grid_for(batch * n), kThreads, 0, (cudaStream_t)stream>>>(
-        y, batch * n, (__nv_bfloat16 *)out);
-    return (int)cudaGetLastError();
+    return pdl_launch(relu_bf16_kernel, grid_for(batch * n), stream, y, batch * n, (__nv_bfloat16 *)out);
 }
 
 int launch_residual(const void *h1, const float *y, int64_t H, int batch, void *out, void *stream) {
-    residual_kernel<<<grid_for(batch * H), kThreads, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16 *)h1, y, batch * H, (__nv_bfloat16 *)out);
-    return (int)cudaGetLastError();
+    return pdl_launch(residual_kernel, grid_for(batch * H), stream, (const __nv_bfloat16 *)h1, y, batch * H,
+                      (__nv_bfloat16 *)out);
 }
 
 int launch_gather_permute(const float *gbuf, int P, int batch, int64_t n_local, float *y,
                           void *stream) {
-    gather_permute_kernel<<<grid_for((int64_t)P * batch * n_local), kThreads, 0,
-                            (cudaStream_t)stream>>>(gbuf, P, batch, n_local, y);
-    return (int)cudaGetLastError();
+    return pdl_launch(gather_permute_kernel, grid_for((int64_t)P * batch * n_local), stream, gbuf, P, batch,
+                      n_local, y);
 }
 
 }  // namespace hg
