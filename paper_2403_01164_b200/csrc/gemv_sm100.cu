@@ -538,7 +538,7 @@ int prepare_b() {
 
 // CTAs per SM for B = 1 (A/B switch HG_GEMV_CPS): 1 = Cfg<1> (8 stages, 8 consumer warps);
 // 2 or 3 = smaller CTAs (4 stages, 4 consumer warps, ~70 KB smem) sharing each SM.
-int g_cps1 = 1;
+int g_cps1 = 3;  // measured: 3 small CTAs per SM (4 stages each) +1% over one 8-stage CTA back to back (profiles/r01/gemv_latency.md)
 unsigned long long *g_stamps = nullptr;  // device view of mapped host stamps (measurement only)
 unsigned long long *g_stamps_host = nullptr;
 int g_b1s = 8;  // A/B (HG_GEMV_B1S): B = 1 stage count 8 (one CTA per SM), 7 or 6 (<= 115 KB: two fit, PDL overlap)
