@@ -583,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             }
             if (valid) {
 #pragma unroll
-                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * B + b) * a.n_total + g] = __uint_as_float(r[b]);
+                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * a.n_total + g) * B + b] = __uint_as_float(r[b]);
             }
             __threadfence();
             named_barrier(1, 128);
@@ -593,20 +593,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 __threadfence();
                 if (valid) {
                     const float bb = a.bias ? a.bias[g] : 0.f;
+                    // partials are [slice][row][b]: each round loads 4 slices x B values (all independent)
+                    // and adds them per b in slice order -- the same order as the one-buffer kernel
+                    float sum[B];
 #pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        float sum = 0.f;
-                        for (int q0 = 0; q0 < S; q0 += 16) {  // 16 loads in flight, summed in order
-                            float part[16];
+                    for (int b = 0; b < B; ++b) sum[b] = 0.f;
+                    for (int q0 = 0; q0 < S; q0 += 4) {
+                        float part[4][B];
 #pragma unroll
-                            for (int q = 0; q < 16; ++q)
-                                if (q0 + q < S) part[q] = __ldcg(&a.ws[((int64_t)(q0 + q) * B + b) * a.n_total + g]);
+                        for (int q = 0; q < 4; ++q)
 #pragma unroll
-                            for (int q = 0; q < 16; ++q)
-                                if (q0 + q < S) sum += part[q];
-                        }
-                        a.y[b * a.ldy + g] = sum + bb;
+                            for (int b = 0; b < B; ++b)
+                                if (q0 + q < S) part[q][b] = __ldcg(&a.ws[((int64_t)(q0 + q) * a.n_total + g) * B + b]);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+#pragma unroll
+                            for (int b = 0; b < B; ++b)
+                                if (q0 + q < S) sum[b] += part[q][b];
                     }
+#pragma unroll
+                    for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = sum[b] + bb;
                 }
                 if (et == 0) a.counters[t] = 0;
             }
