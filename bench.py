@@ -273,7 +273,12 @@ def prepare(args):
     ncores = os.cpu_count() or 1
     per = max(1, ncores // world)
     pin_threads = 4 if args.pageable else 0  # the pin lane's memcpy threads get their own cores
-    threads = args.threads or max(1, per - pin_threads)
+    # leave cores for the API thread (it enqueues the GPU lanes and joins the CPU rows) and the CUDA
+    # driver's threads: with all 16 cores of the GPU box in the pool, a preempted worker stalls the
+    # lane now and then (measured: 14 threads 283.6 / 285.8 ms/token, 16 threads 283.0 / 329.7 / 298.0,
+    # the slow runs with the link at ~46 GB/s -- profiles/r01/threads.md)
+    reserve = 2 if per >= 12 else (1 if per >= 4 else 0)
+    threads = args.threads or max(1, per - pin_threads - reserve)
     ctx = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
                      chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
                      max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
