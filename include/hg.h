@@ -130,7 +130,8 @@ typedef struct {
     int64_t ring_bytes;  /* device staging ring for streamed chunks (default 1 GiB)      */
     int64_t max_k;       /* largest K the context will see (default 65536)               */
     int64_t max_n;       /* largest N (default 131072)                                   */
-    int32_t cpu_threads; /* host GEMV threads incl. the caller (0 = all online cores)    */
+    int32_t cpu_threads; /* host GEMV threads incl. the caller (0 = online cores minus 2 with >= 12
+                            cores, minus 1 with 4-11: room for the CUDA driver's threads)         */
     int32_t cpu_first;   /* first core to pin pool threads to (-1 = no pinning)          */
     int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */

@@ -1221,7 +1221,10 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     c->cfg = cfg;
     c->device = device;
     std::memset(&c->st, 0, sizeof c->st);
-    int nthr = cfg.cpu_threads > 0 ? cfg.cpu_threads : (int)sysconf(_SC_NPROCESSORS_ONLN);
+    // auto: leave cores to the CUDA driver's threads (and whatever else the process runs) -- with
+    // every core in the pool a preempted worker stalls the lane now and then (profiles/r01/threads.md)
+    const int ncpu = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    int nthr = cfg.cpu_threads > 0 ? cfg.cpu_threads : ncpu - (ncpu >= 12 ? 2 : ncpu >= 4 ? 1 : 0);
     c->pool = pool_create(nthr, cfg.cpu_first);
     c->host_fn = host_rows_select(nullptr);
     {
