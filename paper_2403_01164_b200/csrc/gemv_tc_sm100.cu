@@ -311,7 +311,7 @@ constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kS
 constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16 + 16 * 8 + 16 * 4; }
 // persistent form: 6 stages (two CTAs per SM) when there are enough units for 2 per SM, else 11
 // stages (one CTA per SM, ~200 KB in flight) so that a small linear still fills its SMs' queues
-constexpr int kStagesWide = 6, kStagesDeep = 11;
+constexpr int kStagesWide = 6, kStagesDeep = 11, kStagesNarrow = 4;  // narrow: three CTAs per SM (A/B)
 
 // ---------------------------------------------------------------- persistent per-linear form
 // One launch per linear covering the resident block and every streamed chunk (the SIMT kernel's
@@ -686,18 +686,20 @@ int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float 
 }
 
 int g_tc_dyn = 0;   // A/B (HG_TC_DYN=1: work units from a ticket counter; measured slower, profiles/r01/gemv_batches.md)
+int g_tc_narrow = 0;  // A/B (HG_TC_CPS=3: 4-stage CTAs, three per SM)
 int g_tc_deep = 0;  // A/B (HG_TC_DEEP=1: 11-stage one-per-SM form below 2 units per SM; measured slower)
 
 template <int B>
 int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
     const bool deep = g_tc_deep && units < 2 * sms;
-    int grid = deep ? sms : 2 * sms;
+    const bool narrow = !deep && g_tc_narrow && a.work == nullptr;
+    int grid = deep ? sms : narrow ? 3 * sms : 2 * sms;
     if (units < grid) grid = (int)units;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem_for(deep ? kStagesDeep : kStagesWide);
+    cfg.dynamicSmemBytes = smem_for(deep ? kStagesDeep : narrow ? kStagesNarrow : kStagesWide);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -705,7 +707,8 @@ int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     const bool dyn = a.work != nullptr;
-    cudaError_t e = deep ? (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, true>, a)
+    cudaError_t e = narrow ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesNarrow, false>, a)
+                  : deep ? (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, true>, a)
                                 : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, false>, a))
                          : (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, true>, a)
                                 : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, false>, a));
@@ -725,6 +728,8 @@ int prepare_tc_b() {
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
     e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep, true>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesDeep));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesNarrow, false>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesNarrow));
     return e;
 }
 
@@ -749,6 +754,7 @@ int gemv_tc_prepare() {
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     if (const char *v = getenv("HG_TC_DEEP")) g_tc_deep = atoi(v);
     if (const char *v = getenv("HG_TC_DYN")) g_tc_dyn = atoi(v);
+    if (const char *v = getenv("HG_TC_CPS")) g_tc_narrow = atoi(v) == 3;
     if (const char *v = getenv("HG_TC_SLICE")) {
         const int64_t sl = atoll(v) / kTileK * kTileK;
         if (sl >= kTileK) g_slice_max = sl;
