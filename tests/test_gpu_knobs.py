@@ -40,6 +40,7 @@ print("BAD" if bad else "OK", bad)
     {"HG_GEMV_PDL": "0"},
     {"HG_TC_STREAM": "0"},
     {"HG_TC_DEEP": "1"},
+    {"HG_TC_CPS": "3"},
     {"HG_GEMV_CPS": "1"},
     {"HG_GEMV_CPS": "1", "HG_GEMV_B1S": "6"},
     {"HG_GEMV_TC_MIN_BATCH": "0"},
