@@ -305,6 +305,27 @@ def plan(rates: dict, N: int, K: int, batch: int, n_res: int, mode: int, alpha_f
     }
 
 
+def strategy_period(strategy: str, t_cpu: float, t_pin: float, t_trans: float, t_gpu: float,
+                    t_act: float = 0.0) -> float:
+    """Steady-state period of one heterogeneous module under the strategies of Fig. 5.
+
+    naive (Fig. 5a): activation to the CPU (t_act), CPU computation, and an asynchronous
+        weight transfer beside it (t_trans at the rate of un-pinned memory; no pin lane):
+        max(t_act + t_cpu, t_trans + t_gpu).
+    pinned_blocking (Fig. 5b): "pinning the relevant CPU memory first ... the pinning memory
+        blocks both communication and CPU computation": t_pin + max(t_cpu, t_trans + t_gpu).
+    hybrid (Fig. 5c, Eq. (9)): CPU computation, pinning and transfer concurrent:
+        max(t_cpu, max(t_pin, t_trans) + t_gpu).
+    """
+    if strategy == "naive":
+        return max(t_act + t_cpu, t_trans + t_gpu)
+    if strategy == "pinned_blocking":
+        return t_pin + max(t_cpu, t_trans + t_gpu)
+    if strategy == "hybrid":
+        return max(t_cpu, max(t_pin, t_trans) + t_gpu)
+    raise ValueError("strategy must be naive, pinned_blocking or hybrid")
+
+
 # ----------------------------------------------------------------------------
 # c2.7 Alpha benchmark refinement (P:252-266, Sec. 4.4; DESIGN.md readings R9, R10)
 #   "we adjust its value within a small range of [alpha - gamma, alpha + gamma] in

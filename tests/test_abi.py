@@ -152,3 +152,15 @@ def test_struct_mirrors_match_the_c_layout():
     for i, m in enumerate(mirrors):
         assert lib.hg_struct_size(i) == ctypes.sizeof(m), (m.__name__, lib.hg_struct_size(i), ctypes.sizeof(m))
     assert lib.hg_struct_size(99) == 0
+
+
+def test_hg_plan_hand_worked_time_fields():
+    """hg_plan reproduces the hand-worked time fields of tests/test_oracle_plan.py (S:447-448
+    schedule; the chunked t_pred / streamed-doubling t_hbm case)."""
+    p = hg.hg_plan(hg.Rates(512.0, 20480.0, 1024.0, math.inf, 1.0, 1.0, 1.0, 0.0), 256, 8, 1, 0, hg.FIXED, 0.5, 128, 1)
+    assert p.t_cpu == 4.0 and p.t_link == 2.0 and abs(p.t_eq4 - 4.0) <= 1e-12
+    p = hg.hg_plan(hg.Rates(32768.0, 491520.0, 98304.0, math.inf, 212992.0, 196608.0, 65536.0, 0.0),
+                   1152, 64, 1, 128, hg.FIXED, 0.75, 128, 49152)
+    assert (p.n_res, p.n_str, p.n_cpu, p.chunk_rows, p.n_chunks) == (128, 768, 256, 384, 2)
+    assert abs(p.t_pred - 1.1) <= 1e-12 and abs(p.t_eq4 - 1.2) <= 1e-12
+    assert p.t_hbm == 1.0 and p.t_roof == 1.0

@@ -211,3 +211,75 @@ def test_plan_fields():
     pa = oracle.plan(rates, N, K, 1, 0, oracle.ASYNC, 0.0, 128, 8 << 20)
     pt = oracle.plan(rates, N, K, 1, 0, oracle.TPRIME, 0.0, 128, 8 << 20)
     assert pa["alpha_req"] == pt["alpha_req"]
+
+
+# ---------------------------------------------------------------------------------------------
+# Hand-worked pins of plan()'s time fields.  Every number below is worked by
+# hand in the comments, not recomputed with the oracle's formula.
+# ---------------------------------------------------------------------------------------------
+def _rates(**kw):
+    r = dict(v_cpu=1.0, v_gpu=1.0, v_link=1.0, v_pin=math.inf, b_hbm=1.0, b_link=1.0, b_cpu=1.0)
+    r.update(kw)
+    return r
+
+
+def test_plan_t_eq4_spec_hand_schedule():
+    """S:447-448 hand schedule with the pin lane free (weights pre-pinned, reading R7): one module,
+    t_cpu = 4, t_trans = 2, t_gpu = 0.1 -> period max(4, 2 + 0.1) = 4; with t_cpu = 2 -> 2.1.
+    Realised as N = 256 rows of K = 8 (16 B per row), G = 128, alpha = 0.5 -> 128 streamed rows and
+    128 CPU rows = 2048 B each: v_cpu = 2048/4 = 512 B/s, v_link = 2048/2 = 1024 B/s,
+    v_gpu = 2048/0.1 = 20480 B/s."""
+    p = oracle.plan(_rates(v_cpu=512.0, v_link=1024.0, v_gpu=20480.0), 256, 8, 1, 0, oracle.FIXED, 0.5, 128, 1)
+    assert (p["n_str"], p["n_cpu"]) == (128, 128)
+    assert p["t_cpu"] == 4.0 and p["t_link"] == 2.0
+    assert abs(p["t_eq4"] - 4.0) <= 1e-12
+    p = oracle.plan(_rates(v_cpu=1024.0, v_link=1024.0, v_gpu=20480.0), 256, 8, 1, 0, oracle.FIXED, 0.5, 128, 1)
+    assert abs(p["t_eq4"] - 2.1) <= 1e-12
+
+
+def test_plan_t_pred_and_t_hbm_hand_worked():
+    """N = 1152 rows of K = 64 (row = 128 B), n_res = 128, alpha = 0.75, G = 128:
+    m = (1152-128)/128 = 8, g_str = floor(0.75*8 + 0.5) = 6 -> n_str = 768, n_cpu = 256.
+    chunk_bytes = 49152 -> C = 128*max(1, floor(49152/(128*64*2))) = 128*3 = 384 rows -> chunks
+    [128, 512) and [512, 896): 2 chunks, the last of 384 rows.
+    Rates: v_link = 98304 -> t_link = 768*128/98304 = 1.0; v_gpu = 491520 -> GEMV of the last chunk
+    t_tail = 384*128/491520 = 0.1, GEMV of all GPU rows t_gpu = 896*128/491520 = 0.2333...;
+    v_cpu = 32768 -> t_cpu = 256*128/32768 = 1.0.
+    t_pred (pipelined) = max(1.0, 1.0 + 0.1, 0.2333) = 1.1.
+    t_eq4 (serial, Eq. (4): streamed GEMV after the whole transfer) = max(1.0, 1.0 + 768*128/491520 = 1.2) = 1.2.
+    t_hbm: resident 128*128 = 16384 B read once + streamed 768*128 = 98304 B written by the copy engine
+    and read by the SMs = 196608 B -> 212992 B; b_hbm = 212992 -> t_hbm = 1.0 (without the doubling it
+    would be 114688/212992 = 0.538).  t_roof = max(1.0, 98304/196608 = 0.5, 32768/65536 = 0.5) = 1.0."""
+    r = _rates(v_cpu=32768.0, v_link=98304.0, v_gpu=491520.0, b_hbm=212992.0, b_link=196608.0, b_cpu=65536.0)
+    p = oracle.plan(r, 1152, 64, 1, 128, oracle.FIXED, 0.75, 128, 49152)
+    assert (p["n_res"], p["n_str"], p["n_cpu"], p["chunk_rows"], p["n_chunks"]) == (128, 768, 256, 384, 2)
+    assert abs(p["t_pred"] - 1.1) <= 1e-12
+    assert abs(p["t_eq4"] - 1.2) <= 1e-12
+    assert abs(p["t_gpu"] - 896 * 128 / 491520) <= 1e-15 and abs(p["t_gpu"] - 0.23333333333333334) <= 1e-12
+    assert p["t_hbm"] == 1.0 and p["t_roof"] == 1.0
+
+
+def test_strategy_periods_spec_and_paper():
+    """Fig. 5 strategies, steady-state period per module.  S:448: pinned-blocking
+    3.1 vs hybrid 2.1 at t_cpu=2, t_pin=1, t_trans=2, t_gpu=0.1; hybrid 4 at t_cpu=4.  At
+    t_cpu=4 the pinned-blocking period is 1 + max(4, 2.1) = 5 under P:225 ("the pinning memory
+    blocks both communication and CPU computation"), not S:447's max(4, 3.1) = 4 (reading R27)."""
+    per = oracle.strategy_period
+    assert per("hybrid", 4, 1, 2, 0.1) == 4
+    assert abs(per("hybrid", 2, 1, 2, 0.1) - 2.1) <= 1e-12
+    assert abs(per("pinned_blocking", 2, 1, 2, 0.1) - 3.1) <= 1e-12
+    assert per("pinned_blocking", 4, 1, 2, 0.1) == 5
+    # naive (Fig. 5a): no pin lane, the transfer runs at the pageable rate (t_trans given as such)
+    # beside the CPU lane, plus the activation hop on the CPU side
+    assert abs(per("naive", 2, 0, 3, 0.1, t_act=0.05) - 3.1) <= 1e-12
+    assert abs(per("naive", 4, 0, 3, 0.1, t_act=0.05) - 4.05) <= 1e-12
+    # v_pin = inf (t_pin = 0): hybrid == pinned-blocking (S: compare_strategies, "pin free")
+    assert per("hybrid", 3, 0, 2, 0.5) == per("pinned_blocking", 3, 0, 2, 0.5) == 3
+    # ranking at equal lane times: hybrid <= pinned-blocking
+    import random
+    rnd = random.Random(5)
+    for _ in range(1000):
+        t = [rnd.uniform(0, 5) for _ in range(4)]
+        assert per("hybrid", *t) <= per("pinned_blocking", *t)
+    with pytest.raises(ValueError):
+        per("other", 1, 1, 1, 1)
