@@ -257,19 +257,9 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------- our arm
-def prepare(args):
-    """Process-wide setup: context, this rank's pinned weights, measured rates."""
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    from harness import gen
+def make_context(args, rank, world, local, **extra):
+    """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores."""
     from paper_2403_01164_b200 import hg
-
-    rank, world, local = env_rank()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ncores = os.cpu_count() or 1
     per = max(1, ncores // world)
     pin_threads = 4 if args.pageable else 0  # the pin lane's memcpy threads get their own cores
@@ -279,18 +269,19 @@ def prepare(args):
     # the slow runs with the link at ~46 GB/s -- profiles/r01/threads.md)
     reserve = 2 if per >= 12 else (1 if per >= 4 else 0)
     threads = args.threads or max(1, per - pin_threads - reserve)
-    ctx = hg.Context(local, cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
-                     chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
-                     max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
-                     pageable=int(args.pageable), pin_threads=max(1, pin_threads))
-    if world > 1:
-        uid = hg.hg_dist_unique_id() if rank == 0 else None
-        obj = [uid]
-        dist.broadcast_object_list(obj, src=0)
-        ctx.hg_dist_init(world, rank, obj[0])
-    B = args.batch
+    cfg = dict(cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
+               chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
+               max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
+               pageable=int(args.pageable), pin_threads=max(1, pin_threads))
+    cfg.update(extra)
+    return hg.Context(local, **cfg), threads
 
-    # ---- weights: this rank's row shard of every linear, pinned host ----
+
+def make_weights(args, rank, world):
+    """This rank's row shard of every linear: W in host memory (pinned unless --pageable), bias on
+    the device and its host copy (the CPU lane adds its rows' bias in the mirrored glue)."""
+    import torch
+    from harness import gen
     t_setup = time.perf_counter()
     host, biases, biases_h = [], [], []
     for l in range(args.layers):
@@ -304,20 +295,47 @@ def prepare(args):
             b = gen.bf16_bits_to_f32(gen.uniform_bf16(SEED, gen.tensor_id(l, name, "bias"), r1 - r0,
                                                       gen.BIAS_SCALE, offset=r0))
             hl[name] = Wt
-            bh[name] = torch.from_numpy(b)  # host copy: the CPU lane adds its rows' bias (mirrored glue)
+            bh[name] = torch.from_numpy(b)
             bl[name] = bh[name].cuda()
         host.append(hl)
         biases.append(bl)
         biases_h.append(bh)
-    t_setup = time.perf_counter() - t_setup
+    return host, biases, biases_h, time.perf_counter() - t_setup
+
+
+def initial_h(B):
+    """The decode step's input activation h [B, H] (bf16 bits)."""
+    from harness import gen
+    return gen.uniform_bf16(SEED + 1, 999, B * H, 1.0).reshape(B, H)
+
+
+def prepare(args, weights=None, **ctx_extra):
+    """Process-wide setup: context, this rank's host weights, measured rates."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_01164_b200 import hg
+
+    rank, world, local = env_rank()
+    torch.cuda.set_device(local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctx, threads = make_context(args, rank, world, local, **ctx_extra)
+    if world > 1:
+        uid = hg.hg_dist_unique_id() if rank == 0 else None
+        obj = [uid]
+        dist.broadcast_object_list(obj, src=0)
+        ctx.hg_dist_init(world, rank, obj[0])
+    B = args.batch
+    host, biases, biases_h, t_setup = weights or make_weights(args, rank, world)
 
     # ---- a1: measured rates (Fig. 1's "parameter size divided by processing time", P:46) ----
     fc1 = host[0]["fc1"]
     rates = ctx.hg_measure(fc1, fc1.shape[0], H, B, under_load=True)
 
-    h0 = gen.uniform_bf16(SEED + 1, 999, B * H, 1.0).reshape(B, H)
     h_host = torch.empty((B, H), dtype=torch.int16, pin_memory=True)
-    h_host.numpy()[...] = h0.view(np.int16)
+    h_host.numpy()[...] = initial_h(B).view(np.int16)
     return {"torch": torch, "dist": dist, "hg": hg, "rank": rank, "world": world, "local": local,
             "threads": threads, "ctx": ctx, "B": B, "host": host, "biases": biases, "biases_h": biases_h,
             "rates": rates, "t_setup": t_setup, "h_host": h_host, "h_dev": h_host.cuda(),
@@ -529,6 +547,12 @@ def run_point(st, args, budget_gb=0.0):
         roof = gemv_roofline(ctx, plans, args.layers, B, torch, pk,
                              W_dev={name: W_dev_map.get((0, name)) for name in NAMES})
 
+    # ---- parity leg, part 1: one more step of the timed path (same context, plans and layers) with
+    # layers 0 and L-1 traced; the oracle side runs in the cpu_baseline leg (main_arm) ----
+    trace = None
+    if rank == 0 and world == 1 and args.parity and not args.no_cpu_baseline:
+        trace = trace_layers(st, layers, sorted({0, args.layers - 1}))
+
     times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
@@ -615,22 +639,111 @@ def run_point(st, args, budget_gb=0.0):
         "clocks": ck,
         "wall_ms_per_step": round(wall / args.steps * 1e3, 3),
         "setup_s": round(st["t_setup"], 1),
+        "_trace": trace,
     }
     del W_dev_map, layers
     torch.cuda.empty_cache()
     return line
 
 
+def trace_layers(st, layers, which):
+    """Run one step through hg_stack_trace (the timed path, mirrored glue included) with `which`
+    layers traced; returns {layer: {name: host ndarray}} plus the step's input h of layer 0."""
+    import numpy as np
+    torch, hg, ctx, B, s = st["torch"], st["hg"], st["ctx"], st["B"], st["stream"]
+    bufs = {}
+    for l in which:
+        tr = {k: torch.zeros(B, n, dtype=torch.int16, device="cuda") for k, n in
+              (("a", H), ("v", H), ("h1", H), ("a2", H), ("u", F))}
+        tr.update({k: torch.zeros(B, n, device="cuda") for k, n in
+                   (("y_qkv", 3 * H), ("y_o", H), ("y_fc1", F), ("y_fc2", H))})
+        bufs[l] = tr
+    h_in = st["h_host"].numpy().view(np.uint16).copy()
+    st["h_dev"].copy_(st["h_host"])
+    torch.cuda.synchronize()
+    ctx.hg_reset_stats()
+    ctx.hg_stack_trace(layers, st["h_dev"], B, {l: hg.layer_trace(**tr) for l, tr in bufs.items()}, stream=s)
+    torch.cuda.synchronize()
+    stats = ctx.hg_stats()
+    out = {l: {k: (v.cpu().numpy().view(np.uint16) if v.dtype == torch.int16 else v.cpu().numpy())
+               for k, v in tr.items()} for l, tr in bufs.items()}
+    return {"layers": out, "h_in": h_in, "mirror_linears": int(stats.mirror_linears),
+            "h_out": st["h_dev"].cpu().numpy().view(np.uint16).copy()}
+
+
+LIN_IO = (("qkv", "a", "y_qkv"), ("o", "v", "y_o"), ("fc1", "a2", "y_fc1"), ("fc2", "u", "y_fc2"))
+
+
+def cpu_baseline_and_parity(st, trace, reps=2, sample_rows=256):
+    """The cpu_baseline leg: the fp64 oracle timed on layer 0's four linears on the host cores.
+    With a trace of the timed path it is fed the GPU's own bf16 inputs to those linears
+    (teacher-forced) and its outputs are compared with the GPU's, element by
+    element (BJ:5 tolerance); the last layer is compared on `sample_rows` seeded rows per linear
+    (oracle.linear_rows), and layer 0's glue against the oracle's LN / V / residual / ReLU."""
+    import numpy as np
+    import oracle
+    from harness import gen
+    B, nthr = st["B"], os.cpu_count() or 1
+    W = lambda l, n: st["host"][l][n].numpy().view(np.uint16)
+    bias = lambda l, n: st["biases_h"][l][n].numpy()
+    if trace is None:  # no trace: generated inputs (timing only)
+        xs = {n: gen.linear_inputs(SEED, 0, n, B, *SHAPES[n])[0] for n in NAMES}
+    else:
+        T0 = trace["layers"][0]
+        xs = {n: T0[xin] for n, xin, _ in LIN_IO}
+    ts, ys = [], {}
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        for n in NAMES:
+            ys[n] = oracle.linear(xs[n], W(0, n), bias(0, n), nthreads=nthr)
+        ts.append(time.perf_counter() - t0)
+    cb = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr, "kind": "oracle",
+          "sample": "layer 0's four linears (%.3f GB), fp64 naive C loops on all host cores, best of %d, "
+                    "scaled x%d to a token%s" % (STACK_BYTES / LAYERS / 1e9, reps, LAYERS,
+                                                 "; inputs = the timed path's traced activations" if trace else "")}
+    if trace is None:
+        return cb, None
+    worst, ok, checked, per = 0.0, True, 0, {}
+    for n, _, yk in LIN_IO:
+        good, w = oracle.within_tol(T0[yk], ys[n])
+        per["L0." + n] = round(w, 6)
+        ok &= good
+        worst = max(worst, w)
+        checked += T0[yk].size
+    rng = np.random.default_rng(SEED)
+    for l, T in trace["layers"].items():
+        if l == 0:
+            continue
+        for n, xin, yk in LIN_IO:
+            rows = np.sort(rng.choice(SHAPES[n][0], size=min(sample_rows, SHAPES[n][0]), replace=False))
+            ref = oracle.linear_rows(T[xin], W(l, n), rows, bias(l, n), nthreads=nthr)
+            good, w = oracle.within_tol(T[yk][:, rows], ref)
+            per["L%d.%s" % (l, n)] = round(w, 6)
+            ok &= good
+            worst = max(worst, w)
+            checked += ref.size
+    chk = lambda got, ref: oracle.within_tol(oracle.bf16_to_f64(got), oracle.bf16_to_f64(ref))
+    glue = [chk(T0["a"], oracle.layernorm(trace["h_in"])), chk(T0["v"], oracle.attention_pos0(T0["y_qkv"], H)),
+            chk(T0["h1"], oracle.residual(trace["h_in"], T0["y_o"])), chk(T0["a2"], oracle.layernorm(T0["h1"])),
+            chk(T0["u"], oracle.relu_bf16(T0["y_fc1"]))]
+    glue_ok = all(g for g, _ in glue)
+    parity = {"ok": bool(ok and glue_ok), "worst": round(worst, 6), "glue_ok": glue_ok,
+              "glue_worst": round(max(w for _, w in glue), 6),
+              "tolerance": "|y - y_ref| <= 1e-2 max(1, |y_ref|) elementwise (BJ:5); worst = max err/bound",
+              "checked_outputs": int(checked), "per_linear": per, "mirror_linears": trace["mirror_linears"],
+              "what": "one extra step of the timed path (same context/plans, hg_stack_trace); layer 0 all "
+                      "outputs + glue, layer %d on %d seeded rows per linear, teacher-forced fp64 oracle"
+                      % (max(trace["layers"]), sample_rows)}
+    return cb, parity
+
+
 def main_arm(args):
     st = prepare(args)
     line = run_point(st, args, args.hbm_budget_gb)
     rank, world = st["rank"], st["world"]
+    trace = line.pop("_trace", None)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        ts, nthr = oracle_layer_sample(reps=2, batch=st["B"])
-        line["cpu_baseline"] = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr,
-                                "kind": "oracle",
-                                "sample": "layer 0's four linears (%.3f GB), fp64 naive C loops on all host "
-                                          "cores, best of 2, scaled x%d to a token" % (STACK_BYTES / LAYERS / 1e9, LAYERS)}
+        line["cpu_baseline"], line["parity"] = cpu_baseline_and_parity(st, trace)
     if rank == 0:
         print(json.dumps(line), flush=True)
     st["ctx"].close()
@@ -639,7 +752,7 @@ def main_arm(args):
     return 0
 
 
-def main():
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=8)
@@ -663,12 +776,19 @@ def main():
                     help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
-    args = ap.parse_args()
+    ap.add_argument("--no-parity", dest="parity", action="store_false",
+                    help="skip the parity leg (one traced step checked against the oracle)")
+    args = ap.parse_args(argv)
     set_model(args.model)
     if args.layers is None:
         args.layers = LAYERS
     if args.warmup < 3:
         args.warmup = 3
+    return args
+
+
+def main():
+    args = parse_args()
     if args.impl == "reference":
         return run_reference(args)
     return main_arm(args)

@@ -36,9 +36,10 @@
  *   16-byte aligned and K % 8 == 0 (HG_EALIGN); N % G == 0, n_res % G == 0,
  *   0 <= alpha <= 1 (not NaN), 1 <= batch <= HG_MAX_BATCH (HG_EINVAL).
  * Synchronisation: hg_linear / hg_layer / hg_stack are host-blocking for the
- *   CPU slice (they return after the CPU rows are computed and their
- *   host->device copy is enqueued) and stream-ordered for the GPU side: y (or h)
- *   is complete when `stream` passes the call.
+ *   CPU slice (they return after the CPU rows are computed into a mapped pinned
+ *   buffer and the join kernel that reads them in place -- zero-copy, no
+ *   host->device memcpy -- is enqueued) and stream-ordered for the GPU side: y
+ *   (or h) is complete when `stream` passes the call.
  * Errors: no C++ exception crosses the ABI.  A CUDA/NCCL failure mid-call
  *   returns HG_ECUDA / HG_ENCCL and puts the context in an error state (later
  *   calls return HG_ESTATE until hg_destroy).  Host waits are bounded
@@ -259,7 +260,7 @@ HG_API hg_status hg_plan(const hg_rates *rates, int64_t N, int64_t K, int batch,
  * For a pageable W_host (hg_config.pageable) v_pin is the pin lane's rate into its staging ring and
  * the link is probed from staging; otherwise v_pin = +inf (weights pinned once, reading R7).
  * Fills v_cpu, v_gpu, v_link, b_link (large-chunk copy), b_host (flags bit 0), b_cpu (host read rate
- * of the pool threads), b_hbm (device read rate); v_pin = +inf. */
+ * of the pool threads), b_hbm (device read rate), and v_pin as above (+inf for page-locked W_host). */
 HG_API hg_status hg_measure(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch,
                             int flags, hg_rates *out);
 
@@ -350,6 +351,15 @@ HG_API hg_status hg_layer(hg_ctx *ctx, const hg_opt_layer *layer, void *h_dev, i
 HG_API hg_status hg_stack(hg_ctx *ctx, const hg_opt_layer *layers, int n_layers, void *h_dev,
                           int batch, void *stream);
 
+/* hg_stack with per-layer intermediates copied out (teacher-forced parity of the exact path the
+ * bench times).  traces: NULL or an array of n_layers hg_layer_trace whose NULL
+ * members are skipped.  The copies are stream-ordered device-to-device copies issued after the
+ * glue kernel (linear inputs a, v, h1, a2, u) and after the join (linear outputs y_*) of the
+ * traced layer, on whichever path the stack takes (mirrored glue included); they do not change
+ * the partition, the pipeline or any result bit. */
+HG_API hg_status hg_stack_trace(hg_ctx *ctx, const hg_opt_layer *layers, int n_layers, void *h_dev,
+                                int batch, hg_layer_trace *traces, void *stream);
+
 /* ---------------------------------------------------------------- lanes alone */
 /* Device GEMV alone (the resident/streamed kernel): y[b*ldy + j] = x[b,:].W[j,:] (+bias[j]),
  * j < n.  All device pointers.  Same kernel and reduction order hg_linear uses. */
@@ -364,9 +374,10 @@ HG_API hg_status hg_gemv(hg_ctx *ctx, const void *x_dev, int batch, int64_t n, i
  * step's launch configuration.  Rotating seq0 across calls walks the whole ring (the bench uses
  * it so that back-to-back replays read more than L2 holds).  Streamed outputs are computed from
  * whatever the ring holds (timing only); resident outputs are exact.  y [batch, N] fp32 device.
- * On the tcgen05 path (batch >= gemv_tc_min_batch) the step launches the resident block and then
- * one GEMV per chunk, and so does the replay.  seq0 < 0 and plans with more chunks than ring
- * slots return HG_EINVAL. */
+ * On the tcgen05 path (batch >= gemv_tc_min_batch, or K > 8192) the step and the replay are one
+ * persistent launch per linear as well (up to 16 streamed chunks; a linear with more chunks falls
+ * back to the resident block plus one launch per chunk, in the step and in the replay alike).
+ * seq0 < 0 and plans with more chunks than ring slots return HG_EINVAL. */
 HG_API hg_status hg_gemv_replay(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
                                 const void *W_dev, const float *bias_dev, float *y_dev, int64_t seq0,
                                 void *stream);

@@ -160,10 +160,9 @@ struct hg_ctx {
     int64_t prebound = 0;   // upcoming future chunks already bound to an enqueued GEMV (tags mode)
     bool tags = false;      // cfg.handshake == 1 and stream memory operations available
     bool tc_stream = true;  // tcgen05 batches: one persistent launch per linear (HG_TC_STREAM=0: per chunk)
-    uint32_t *work = nullptr;  // device: [kWorkSlots][ticket, exit] for the tcgen05 launches' work queues
-    uint64_t work_seq = 0;     // launches so far (slot = seq mod kWorkSlots; a slot is zero again at exit)
     uint32_t *tagmem = nullptr;  // device: arrived[nslots] consumed[nslots] slot_cnt[nslots] err[4] gbar[4 + kGroupCounters]
     uint32_t *arrived = nullptr, *consumed = nullptr, *slot_cnt = nullptr, *err = nullptr, *gbar = nullptr;
+    volatile uint32_t *err_host = nullptr;  // mapped pinned [4]: host view of `err` (read without a sync)
     std::vector<ChunkReq> future;
     size_t fpos = 0;
     bool fwrap = false;
@@ -320,11 +319,11 @@ void dbg_trace_report(hg_ctx *c) {
                     (long long)(t.seq0 % c->nslots));
 }
 
-// A tag wait inside a kernel that timed out leaves err != 0 (read at synchronising calls).
+// A tag wait inside a kernel that timed out leaves err != 0 (mapped host word; also polled by
+// begin_call / end_call).
 hg_status check_device_error(hg_ctx *c) {
-    if (!c->err) return HG_OK;
-    uint32_t e = 0;
-    HG_CK(c, cudaMemcpy(&e, c->err, 4, cudaMemcpyDeviceToHost));
+    if (!c->err_host) return HG_OK;
+    const uint32_t e = c->err_host[0];
     if (e) {
         c->error = true;
         return set_error(HG_ETIMEOUT, "a GEMV waited longer than %.1f s for a streamed chunk", c->cfg.timeout_s);
@@ -629,10 +628,10 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
         S.chunk_rows = p.chunk_rows;
         S.n_str = direct ? 0 : p.n_str;
         const void *wdir = nullptr;
-        if (direct && p.n_str > 0) {  // the device address of the pinned host rows (UVA mapping)
+        if (direct && p.n_str > 0) {  // the device address of the pinned host rows (UVA mapping; checked
+                                      // by validate_lin / validate_layer before anything was enqueued)
             cudaPointerAttributes at;
             HG_CK(c, cudaPointerGetAttributes(&at, L.W_host));
-            if (!at.devicePointer) return set_error(HG_ENOTPINNED, "W_host is not mapped into the device address space");
             wdir = at.devicePointer;
         }
         S.W_dir = wdir;
@@ -661,7 +660,6 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
             cudaEvent_t e0 = nullptr;
             if (c->cfg.collect_stats && (e0 = tev_get(c, &i0))) HG_CK(c, cudaEventRecord(e0, s));
             if (tc_stream) {
-                S.work = c->work + 2 * (c->work_seq++ % kWorkSlots);
                 HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 stream launch"));
             }
             else
@@ -785,6 +783,18 @@ hg_status validate_plan(hg_ctx *c, const hg_plan_t &p) {
     return HG_OK;
 }
 
+// stream_mode 1 (zero-copy streaming) reads the streamed rows through the host pointer's device
+// mapping: checked with the other arguments, before anything is enqueued.
+hg_status check_mapped(hg_ctx *c, const hg_plan_t &p, const void *W_host) {
+    if (c->cfg.stream_mode != 1 || p.n_str <= 0 || gemv_use_tc((int)p.batch, p.K)) return HG_OK;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, W_host) != cudaSuccess || !at.devicePointer) {
+        cudaGetLastError();
+        return set_error(HG_ENOTPINNED, "stream_mode 1: W_host is not mapped into the device address space");
+    }
+    return HG_OK;
+}
+
 hg_status validate_lin(hg_ctx *c, const hg_plan_t &p, const void *x, const void *W_dev,
                        const void *W_host, const float *bias, const float *y) {
     HG_TRY(validate_plan(c, p));
@@ -797,6 +807,7 @@ hg_status validate_lin(hg_ctx *c, const hg_plan_t &p, const void *x, const void 
     if (p.n_res < p.N) {
         HG_TRY(check_ptr(c, W_host, false, "W_host"));
         if (!aligned(W_host, 16)) return set_error(HG_EALIGN, "W_host not 16-byte aligned");
+        HG_TRY(check_mapped(c, p, W_host));
     }
     if (bias) {
         HG_TRY(check_ptr(c, bias, true, "bias"));
@@ -807,9 +818,25 @@ hg_status validate_lin(hg_ctx *c, const hg_plan_t &p, const void *x, const void 
     return HG_OK;
 }
 
+// Asynchronous failures found without synchronising: a GEMV's bounded wait for a streamed chunk
+// (the kernel sets the mapped err word) or the pin lane's bounded wait for a staging slot.  Both
+// leave the results of the call in flight undefined, so the context enters its error state.
+hg_status check_async_errors(hg_ctx *c) {
+    if (c->err_host && c->err_host[0]) {
+        c->error = true;
+        return set_error(HG_ETIMEOUT, "a GEMV waited longer than %.1f s for a streamed chunk", c->cfg.timeout_s);
+    }
+    if (c->pin && pinlane_error(c->pin)) {
+        c->error = true;
+        return set_error(HG_ETIMEOUT, "the pin lane waited longer than %.1f s for a staging slot", c->cfg.timeout_s);
+    }
+    return HG_OK;
+}
+
 hg_status begin_call(hg_ctx *c, cudaStream_t s) {
     if (c->error) return set_error(HG_ESTATE, "context is in an error state");
     if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    HG_TRY(check_async_errors(c));
     HG_CK(c, cudaSetDevice(c->device));
     gemv_set_tc_min_batch(c->cfg.gemv_tc_min_batch);
     HG_TRY(stream_guard(c, s));
@@ -823,6 +850,7 @@ hg_status begin_call(hg_ctx *c, cudaStream_t s) {
 }
 
 hg_status end_call(hg_ctx *c, cudaStream_t s) {
+    HG_TRY(check_async_errors(c));
     HG_CK(c, cudaEventRecord(c->ev_call1, s));
     HG_CK(c, cudaEventRecord(c->ev_done, s));
     c->call_timed = true;
@@ -879,14 +907,18 @@ hg_status validate_layer(hg_ctx *c, const hg_opt_layer &l, int B) {
                              (long long)Ks[i], B);
         HG_TRY(validate_plan(c, d.plan));
         if (d.plan.n_res > 0) HG_TRY(check_ptr(c, d.W_dev, true, "layer W_dev"));
-        if (d.plan.n_res < d.plan.N) HG_TRY(check_ptr(c, d.W_host, false, "layer W_host"));
+        if (d.plan.n_res < d.plan.N) {
+            HG_TRY(check_ptr(c, d.W_host, false, "layer W_host"));
+            HG_TRY(check_mapped(c, d.plan, d.W_host));
+        }
         if (d.bias) HG_TRY(check_ptr(c, d.bias, true, "layer bias"));
     }
     return HG_OK;
 }
 
-void trace_copy(hg_ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s) {
-    if (dst) cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s);
+hg_status trace_copy(hg_ctx *c, void *dst, const void *src, size_t bytes, cudaStream_t s) {
+    if (dst) HG_CK(c, cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, s));
+    return HG_OK;
 }
 
 hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_trace *tr,
@@ -897,38 +929,38 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
     HG_TRY(ensure(c, &c->h1, &c->h1_elems, (int64_t)B * H * 2));
     // a = LN1(h)
     HG_TRY(kerr(c, launch_layernorm(h, H, B, l.ln1_g, l.ln1_b, c->act, s), "ln1"));
-    if (tr) trace_copy(c, tr->a, c->act, (size_t)B * H * 2, s);
+    if (tr) HG_TRY(trace_copy(c, tr->a, c->act, (size_t)B * H * 2, s));
     // qkv
     HG_TRY(layer_linear(c, l.lin[0], c->act, c->yscr, 3 * H, s));
-    if (tr && tr->y_qkv) trace_copy(c, tr->y_qkv, c->yscr, (size_t)B * 3 * H * 4, s);
+    if (tr && tr->y_qkv) HG_TRY(trace_copy(c, tr->y_qkv, c->yscr, (size_t)B * 3 * H * 4, s));
     // attention at decode position 0: context = v
     HG_TRY(kerr(c, launch_slice_to_bf16(c->yscr, 3 * H, 2 * H, H, B, c->act, s), "v"));
-    if (tr) trace_copy(c, tr->v, c->act, (size_t)B * H * 2, s);
+    if (tr) HG_TRY(trace_copy(c, tr->v, c->act, (size_t)B * H * 2, s));
     // o
     HG_TRY(layer_linear(c, l.lin[1], c->act, c->yscr, H, s));
-    if (tr) trace_copy(c, tr->y_o, c->yscr, (size_t)B * H * 4, s);
+    if (tr) HG_TRY(trace_copy(c, tr->y_o, c->yscr, (size_t)B * H * 4, s));
     // h1 = h + o ; a2 = LN2(h1)
     HG_TRY(kerr(c, launch_residual_ln(h, c->yscr, H, B, c->h1, l.ln2_g, l.ln2_b, c->act, s), "res+ln2"));
     if (tr) {
-        trace_copy(c, tr->h1, c->h1, (size_t)B * H * 2, s);
-        trace_copy(c, tr->a2, c->act, (size_t)B * H * 2, s);
+        HG_TRY(trace_copy(c, tr->h1, c->h1, (size_t)B * H * 2, s));
+        HG_TRY(trace_copy(c, tr->a2, c->act, (size_t)B * H * 2, s));
     }
     // fc1 + ReLU
     HG_TRY(layer_linear(c, l.lin[2], c->act, c->yscr, F, s));
-    if (tr) trace_copy(c, tr->y_fc1, c->yscr, (size_t)B * F * 4, s);
+    if (tr) HG_TRY(trace_copy(c, tr->y_fc1, c->yscr, (size_t)B * F * 4, s));
     HG_TRY(kerr(c, launch_relu_bf16(c->yscr, F, B, c->act, s), "relu"));
-    if (tr) trace_copy(c, tr->u, c->act, (size_t)B * F * 2, s);
+    if (tr) HG_TRY(trace_copy(c, tr->u, c->act, (size_t)B * F * 2, s));
     // fc2 + residual
     HG_TRY(layer_linear(c, l.lin[3], c->act, c->yscr, H, s));
-    if (tr) trace_copy(c, tr->y_fc2, c->yscr, (size_t)B * H * 4, s);
+    if (tr) HG_TRY(trace_copy(c, tr->y_fc2, c->yscr, (size_t)B * H * 4, s));
     HG_TRY(kerr(c, launch_residual(c->h1, c->yscr, H, B, h, s), "residual"));
     c->st.gpu_launches += 5;
     return HG_OK;
 }
 
 // ---------------------------------------------------------------- mirrored glue (reading R24)
-bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n, hg_layer_trace *tr) {
-    if (!c->cfg.mirror_glue || tr || dist_nranks(c->dist) != 1 || !hglue_supported()) return false;
+bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n) {
+    if (!c->cfg.mirror_glue || dist_nranks(c->dist) != 1 || !hglue_supported()) return false;
     bool any_cpu = false;  // without CPU rows nobody needs the glue on the host
     for (int l = 0; l < n; ++l)
         for (int i = 0; i < 4; ++i) any_cpu |= layers[l].lin[i].plan.n_cpu > 0;
@@ -1006,7 +1038,8 @@ hg_status ensure_mirror(hg_ctx *c) {
 // rows needs its input -- from each linear's full y (its CPU rows were written there by the CPU
 // lane itself, its GPU rows arrive D2H while the CPU lane is busy).  So neither a D2H of x nor the
 // zero-copy join sits on the CPU lane's critical path, and fully resident linears run back to back.
-hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *h, int B, cudaStream_t s) {
+hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *h, int B, hg_layer_trace *trs,
+                           cudaStream_t s) {
     constexpr int R = hg_ctx::kMirrorRing;
     const int64_t H = layers[0].hidden;
     int64_t maxF = 0;
@@ -1076,6 +1109,12 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             HG_TRY(kerr(c, launch_relu_bf16(yprev_d, F, B, c->act, s), "relu"));
         }
         c->st.gpu_launches++;
+        hg_layer_trace *tr = trs ? &trs[l] : nullptr;
+        if (tr) {  // the linear's input as the GPU computed it (stream-ordered device copies)
+            void *xin = i == 0 ? tr->a : i == 1 ? tr->v : i == 2 ? tr->a2 : tr->u;
+            HG_TRY(trace_copy(c, xin, c->act, (size_t)B * K * 2, s));
+            if (i == 2) HG_TRY(trace_copy(c, tr->h1, c->h1, (size_t)B * H * 2, s));
+        }
         HG_TRY(dbg_sync(c, s, "glue", k));
         // ---- this slot's previous occupant (k - R): its D2H must be done before y is overwritten,
         // and the host must have consumed its host copy before the new D2H / CPU rows land there
@@ -1134,6 +1173,10 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
                                        d.bias_host ? nullptr : d.bias, s), "join"));
             c->st.gpu_launches++;
             HG_TRY(dbg_sync(c, s, "join", k));
+        }
+        if (tr) {  // the linear's full output y (GPU rows + joined CPU rows)
+            float *yt = i == 0 ? tr->y_qkv : i == 1 ? tr->y_o : i == 2 ? tr->y_fc1 : tr->y_fc2;
+            HG_TRY(trace_copy(c, yt, yd, (size_t)B * N * 4, s));
         }
         HG_CK(c, cudaEventRecord(c->ev_use[slot], s));
         c->st.n_linears++;
@@ -1217,6 +1260,8 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     if (cfg.granule < 1 || cfg.chunk_bytes < 1 || cfg.max_k < 8 || cfg.max_n < 1 ||
         !(cfg.timeout_s > 0))
         return set_error(HG_EINVAL, "bad config");
+    if (cfg.pageable && cfg.stream_mode == 1)  // zero-copy reads need page-locked, mapped rows
+        return set_error(HG_EINVAL, "pageable weights cannot be streamed zero-copy (stream_mode 1)");
     hg_ctx *c = new hg_ctx;
     c->cfg = cfg;
     c->device = device;
@@ -1297,14 +1342,19 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     CREATE_CK(cudaMalloc((void **)&c->sink, 256));
     c->tags = cfg.handshake != 0 && load_memops();
     if (const char *v = getenv("HG_TC_STREAM")) c->tc_stream = atoi(v) != 0;
-    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters + 2 * kWorkSlots) * 4));
-    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters + 2 * kWorkSlots) * 4));
-    c->work = c->tagmem + 3 * c->nslots + 8 + kGroupCounters;
+    CREATE_CK(cudaMalloc((void **)&c->tagmem, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
+    CREATE_CK(cudaMemset(c->tagmem, 0, (size_t)(3 * c->nslots + 8 + kGroupCounters) * 4));
     c->arrived = c->tagmem;
     c->consumed = c->tagmem + c->nslots;
     c->slot_cnt = c->tagmem + 2 * c->nslots;
-    c->err = c->tagmem + 3 * c->nslots;
-    c->gbar = c->err + 4;
+    c->gbar = c->tagmem + 3 * c->nslots + 4;
+    {  // the kernels' timeout word lives in mapped host memory: begin_call/end_call poll it for free
+        uint32_t *eh = nullptr;
+        CREATE_CK(cudaHostAlloc((void **)&eh, 64, cudaHostAllocMapped));
+        std::memset(eh, 0, 64);
+        c->err_host = eh;
+        CREATE_CK(cudaHostGetDevicePointer((void **)&c->err, eh, 0));
+    }
     CREATE_CK(cudaDeviceSynchronize());
 #undef CREATE_CK
     *out = c;
@@ -1338,6 +1388,7 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
                         (void *)c->gbuf, (void *)c->tagmem})
             if (p) cudaFree(p);
         if (c->x_host) cudaFreeHost(c->x_host);
+        if (c->err_host) cudaFreeHost((void *)c->err_host);
         for (float *p : c->ycpu_host)
             if (p) cudaFreeHost(p);
     }
@@ -1405,13 +1456,13 @@ HG_API hg_status hg_layer(hg_ctx *c, const hg_opt_layer *l, void *h, int batch,
     std::vector<ChunkReq> list;
     for (int i = 0; i < 4; ++i) push_chunks(list, l->lin[i].plan, l->lin[i].W_host);
     set_future(c, std::move(list), false);
-    if (can_mirror(c, l, 1, trace)) HG_TRY(run_stack_mirror(c, l, 1, h, batch, s));
+    if (can_mirror(c, l, 1)) HG_TRY(run_stack_mirror(c, l, 1, h, batch, trace, s));
     else HG_TRY(run_layer(c, *l, h, batch, trace, s));
     return end_call(c, s);
 }
 
-HG_API hg_status hg_stack(hg_ctx *c, const hg_opt_layer *layers, int n_layers, void *h, int batch,
-                          void *stream) {
+HG_API hg_status hg_stack_trace(hg_ctx *c, const hg_opt_layer *layers, int n_layers, void *h, int batch,
+                                hg_layer_trace *traces, void *stream) {
     if (!c || !layers || n_layers < 1) return set_error(HG_EINVAL, "bad arguments");
     if (c->error) return set_error(HG_ESTATE, "context is in an error state");
     if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
@@ -1424,14 +1475,19 @@ HG_API hg_status hg_stack(hg_ctx *c, const hg_opt_layer *layers, int n_layers, v
     for (int l = 0; l < n_layers; ++l)
         for (int i = 0; i < 4; ++i) push_chunks(list, layers[l].lin[i].plan, layers[l].lin[i].W_host);
     set_future(c, std::move(list), c->cfg.wrap_prefetch != 0);
-    if (can_mirror(c, layers, n_layers, nullptr)) {
+    if (can_mirror(c, layers, n_layers)) {
         for (int l = 1; l < n_layers; ++l)
             if (layers[l].hidden != layers[0].hidden) return set_error(HG_EINVAL, "layers differ in hidden size");
-        HG_TRY(run_stack_mirror(c, layers, n_layers, h, batch, s));
+        HG_TRY(run_stack_mirror(c, layers, n_layers, h, batch, traces, s));
     } else {
-        for (int l = 0; l < n_layers; ++l) HG_TRY(run_layer(c, layers[l], h, batch, nullptr, s));
+        for (int l = 0; l < n_layers; ++l) HG_TRY(run_layer(c, layers[l], h, batch, traces ? &traces[l] : nullptr, s));
     }
     return end_call(c, s);
+}
+
+HG_API hg_status hg_stack(hg_ctx *c, const hg_opt_layer *layers, int n_layers, void *h, int batch,
+                          void *stream) {
+    return hg_stack_trace(c, layers, n_layers, h, batch, nullptr, stream);
 }
 
 HG_API hg_status hg_gemv(hg_ctx *c, const void *x, int batch, int64_t n, int64_t K, const void *W,
@@ -1515,7 +1571,6 @@ HG_API hg_status hg_gemv_replay(hg_ctx *c, const hg_plan_t *p, const void *x, co
     if (gemv_use_tc(B, p->K)) {
         if (gemv_tc_stream_tiles(p->n_res, p->n_str, p->chunk_rows, S.n_chunks) > c->n_counters)
             return set_error(HG_EINVAL, "tcgen05 GEMV: too many tiles for the context's counters");
-        S.work = c->work + 2 * (c->work_seq++ % kWorkSlots);
         HG_TRY(kerr(c, launch_gemv_tc_stream(S, c->counters, s), "gemv tcgen05 replay"));
     } else {
         HG_TRY(kerr(c, launch_gemv_stream(S, s), "gemv replay"));

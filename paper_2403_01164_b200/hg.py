@@ -140,6 +140,7 @@ _sig = {
     "hg_linear_planned": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
     "hg_layer": (_i32, [_vp, _P(OptLayer), _vp, _i32, _P(LayerTrace), _vp]),
     "hg_stack": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _vp]),
+    "hg_stack_trace": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _P(LayerTrace), _vp]),
     "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
     "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _i64, _vp]),
     "hg_schedule": (_i32, [_P(Module), _i32, _i64, _i64, _i32, _P(_i64), _P(_i64)]),
@@ -306,6 +307,14 @@ class Context:
     def hg_stack(self, layers, h, batch, stream=None):
         arr = (OptLayer * len(layers))(*layers)
         _check(_lib.hg_stack(self._h, arr, len(layers), _ptr(h), batch, _stream(stream)))
+
+    def hg_stack_trace(self, layers, h, batch, traces, stream=None):
+        """traces: {layer index: LayerTrace}; other layers are not traced."""
+        arr = (OptLayer * len(layers))(*layers)
+        tarr = (LayerTrace * len(layers))()
+        for l, t in traces.items():
+            tarr[l] = t
+        _check(_lib.hg_stack_trace(self._h, arr, len(layers), _ptr(h), batch, tarr, _stream(stream)))
 
     def hg_gemv_replay(self, plan, x, W_dev, bias, y, stream=None, seq0=0):
         _check(_lib.hg_gemv_replay(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(bias), _ptr(y),
