@@ -39,6 +39,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
                 flush();
                 __nanosleep(64);
                 if (globaltimer() - t0 > a.timeout_ns) {
-                    atomicOr(a.err, 1u);
+                    *(volatile uint32_t *)a.err = 1u;  // mapped host word: a plain store (no PCIe atomic)
                     return;
                 }
             }
@@ -541,8 +542,6 @@ int prepare_b() {
 int g_cps1 = 3;  // measured: 3 small CTAs per SM (4 stages each) +1% over one 8-stage CTA back to back (profiles/r01/gemv_latency.md)
 unsigned long long *g_stamps = nullptr;  // device view of mapped host stamps (measurement only)
 unsigned long long *g_stamps_host = nullptr;
-int g_b1s = 8;  // A/B (HG_GEMV_B1S): B = 1 stage count 8 (one CTA per SM), 7 or 6 (<= 115 KB: two fit, PDL overlap)
-int g_b34 = 0;  // A/B (HG_GEMV_B34): B = 3, 4 kernel shape 0 = Cfg (R2,S10,W10), 1 = (R2,S8,W8), 2 = (R4,S4,W4)
 
 }  // namespace
 
@@ -602,7 +601,21 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.K = L.K;
     a.len = g.ks;
     a.P = g.s;
-    const int cps = (L.batch == 1) ? g_cps1 : 1;
+    int cps = (L.batch == 1) ? g_cps1 : 1;
+    if (cps > 1) {  // as many small CTAs per SM as fit in shared memory at this part length
+        static thread_local int64_t occ_len = -1;
+        static thread_local int occ = 0;
+        if (occ_len != a.len) {
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_stream_kernel<1, 1, 4, 4>,
+                                                              threads_for<4>(), smem_bytes_for<1, 1, 4>(a.len)) !=
+                cudaSuccess) {
+                (void)cudaGetLastError();
+                occ = 1;
+            }
+            occ_len = a.len;
+        }
+        cps = std::max(1, std::min(cps, occ));
+    }
     a.gp = cps * g_sms / a.P;
     if (a.gp < 1) return (int)cudaErrorInvalidValue;
     a.W_res = (const uint8_t *)L.W_res;
@@ -633,18 +646,10 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
     switch (L.batch) {
-        case 1:
-            return cps > 1 ? launch_v<1, 1, 4, 4>(a, st)
-                 : g_b1s == 6 ? launch_v<1, 1, 6, 6>(a, st)
-                 : g_b1s == 7 ? launch_v<1, 1, 7, 7>(a, st)
-                 : g_b1s == 10 ? launch_v<1, 1, 10, 10>(a, st)
-                 : g_b1s == 12 ? launch_v<1, 1, 12, 12>(a, st)
-                              : launch_b<1>(a, st);
+        case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
-        case 3:
-            return g_b34 == 1 ? launch_v<3, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<3, 4, 4, 4>(a, st) : launch_b<3>(a, st);
-        case 4:
-            return g_b34 == 1 ? launch_v<4, 2, 8, 8>(a, st) : g_b34 == 2 ? launch_v<4, 4, 4, 4>(a, st) : launch_b<4>(a, st);
+        case 3: return launch_b<3>(a, st);
+        case 4: return launch_b<4>(a, st);
         case 5: return launch_b<5>(a, st);
         case 6: return launch_b<6>(a, st);
         case 7: return launch_b<7>(a, st);
@@ -680,19 +685,6 @@ int gemv_prepare() {
     int e = 0;
     e |= prepare_b<1>();
     e |= prepare_v<1, 1, 4, 4>(Cfg<1>::PART);
-    e |= prepare_v<1, 1, 6, 6>(Cfg<1>::PART);
-    e |= prepare_v<1, 1, 7, 7>(Cfg<1>::PART);
-    e |= prepare_v<1, 1, 10, 10>(Cfg<1>::PART);
-    e |= prepare_v<1, 1, 12, 12>(Cfg<1>::PART);
-    if (const char *v = getenv("HG_GEMV_B1S")) {
-        const int b1s = atoi(v);
-        g_b1s = (b1s == 6 || b1s == 7 || b1s == 10 || b1s == 12) ? b1s : 8;
-    }
-    e |= prepare_v<3, 2, 8, 8>(4096);
-    e |= prepare_v<3, 4, 4, 4>(4096);
-    e |= prepare_v<4, 2, 8, 8>(4096);
-    e |= prepare_v<4, 4, 4, 4>(4096);
-    if (const char *v = getenv("HG_GEMV_B34")) g_b34 = atoi(v);
     if (const char *v = getenv("HG_GEMV_PDL")) g_pdl = atoi(v) != 0;
     if (const char *v = getenv("HG_TC_LONG_K")) g_tc_long_k = atoll(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;

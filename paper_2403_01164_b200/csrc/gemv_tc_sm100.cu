@@ -308,10 +308,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kStages + 4) + 16;
-constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16 + 16 * 8 + 16 * 4; }
-// persistent form: 6 stages (two CTAs per SM) when there are enough units for 2 per SM, else 11
-// stages (one CTA per SM, ~200 KB in flight) so that a small linear still fills its SMs' queues
-constexpr int kStagesWide = 6, kStagesDeep = 11, kStagesNarrow = 4;  // narrow: three CTAs per SM (A/B)
+constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16; }
+// persistent form: 6-stage CTAs, two per SM (measured against 11 stages x one per SM and 4 stages x
+// three per SM: both slower, profiles/r01/gemv_batches.md)
+constexpr int kStagesWide = 6;
 
 // ---------------------------------------------------------------- persistent per-linear form
 // One launch per linear covering the resident block and every streamed chunk (the SIMT kernel's
@@ -342,7 +342,6 @@ struct TcArgs {
     uint32_t *consumed, *slot_cnt, *err;
     unsigned long long timeout_ns;
     unsigned long long *stamps;  // measurement: [CTA][4] globaltimer (entry, first MMA stage, epilogue done, exit)
-    uint32_t *work;              // DYN: [ticket, exit count] of this launch (zero at launch, reset at exit)
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -356,7 +355,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
     return t;
 }
 
-template <int B, int ST, bool DYN>
+template <int B, int ST>
 __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -371,12 +370,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     auto empty = [&](int s) { return bars + 8 * (ST + s); };
     auto tfull = [&](int q) { return bars + 8 * (2 * ST + q); };
     auto tempty = [&](int q) { return bars + 8 * (2 * ST + 2 + q); };
-    // DYN: work units handed out by a global ticket counter; the producer passes each unit id to
-    // the MMA and epilogue warps through a 16-entry smem queue (at most ST + 3 units are in flight
-    // between producer and epilogue, so a slot is never lapped)
-    const uint32_t uqbar0 = bars + 8 * (2 * ST + 4) + 16;
-    int32_t *uq = (int32_t *)(gbase + (bars - base) + 8 * (2 * ST + 4) + 16 + 16 * 8);
-    auto uqbar = [&](int q) { return uqbar0 + 8 * q; };
 
     // PDL: the next kernel may be scheduled once every CTA of this one runs; x (read by the
     // producer with every stage) is the only input of the previous kernel, so only the producer
@@ -393,8 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             mbar_init(tfull(q), 1);
             mbar_init(tempty(q), 128);
         }
-        if (DYN)
-            for (int q = 0; q < 16; ++q) mbar_init(uqbar(q), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();  // barriers initialised: the producer starts at once; TMEM is allocated meanwhile
@@ -436,18 +427,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 pend = 0;
                 dep = true;
             };
-            int qi = 0;
-            for (int64_t u = DYN ? -1 : blockIdx.x;; u += gridDim.x) {
-                if (DYN) {
-                    const uint32_t tk = atomicAdd(a.work, 1u);
-                    u = tk < (uint64_t)n_units ? (int64_t)tk : -1;
-                    uq[qi & 15] = (int32_t)u;
-                    mbar_arrive(uqbar(qi & 15));
-                    ++qi;
-                    if (u < 0) break;
-                } else if (u >= n_units) {
-                    break;
-                }
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const int64_t t = u / S;
                 const int s = (int)(u - t * S);
                 const int i = src_of(t);
@@ -457,7 +437,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                     while ((int32_t)(ld_acquire_u32(a.arrived + a.slot[i]) - a.tag[i]) < 0) {
                         __nanosleep(64);
                         if (gtimer() - t0 > a.timeout_ns) {
-                            atomicOr(a.err, 1u);
+                            *(volatile uint32_t *)a.err = 1u;  // mapped host word: a plain store (no PCIe atomic)
                             break;
                         }
                     }
@@ -490,14 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int64_t u = blockIdx.x;; u += gridDim.x, ++it) {
-                if (DYN) {
-                    mbar_wait(uqbar(it & 15), (uint32_t)((it >> 4) & 1));
-                    u = uq[it & 15];
-                    if (u < 0) break;
-                } else if (u >= n_units) {
-                    break;
-                }
+            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
                 const int acc = it & 1;
                 const uint32_t aphase = (uint32_t)((it >> 1) & 1);
                 mbar_wait(tempty(acc), aphase ^ 1);
@@ -532,14 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
         const int quarter = warp & 3;
         const int et = (warp - 2) * 32 + lane;
         int it = 0;
-        for (int64_t u = blockIdx.x;; u += gridDim.x, ++it) {
-            if (DYN) {
-                mbar_wait(uqbar(it & 15), (uint32_t)((it >> 4) & 1));
-                u = uq[it & 15];
-                if (u < 0) break;
-            } else if (u >= n_units) {
-                break;
-            }
+        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t aphase = (uint32_t)((it >> 1) & 1);
             const int64_t t = u / S;
@@ -626,13 +592,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
     if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 3] = gtimer();
-    if (DYN && threadIdx.x == 0) {  // the last CTA out resets this launch's ticket slot
-        __threadfence();
-        if (atomicAdd(a.work + 1, 1u) == gridDim.x - 1) {
-            atomicExch(a.work, 0u);
-            atomicExch(a.work + 1, 0u);
-        }
-    }
 }
 
 // ---------------------------------------------------------------- host side
@@ -685,33 +644,22 @@ int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float 
     return (int)cudaGetLastError();
 }
 
-int g_tc_dyn = 0;   // A/B (HG_TC_DYN=1: work units from a ticket counter; measured slower, profiles/r01/gemv_batches.md)
-int g_tc_narrow = 0;  // A/B (HG_TC_CPS=3: 4-stage CTAs, three per SM)
-int g_tc_deep = 0;  // A/B (HG_TC_DEEP=1: 11-stage one-per-SM form below 2 units per SM; measured slower)
-
 template <int B>
 int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
-    const bool deep = g_tc_deep && units < 2 * sms;
-    const bool narrow = !deep && g_tc_narrow && a.work == nullptr;
-    int grid = deep ? sms : narrow ? 3 * sms : 2 * sms;
+    int grid = 2 * sms;
     if (units < grid) grid = (int)units;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem_for(deep ? kStagesDeep : narrow ? kStagesNarrow : kStagesWide);
+    cfg.dynamicSmemBytes = smem_for(kStagesWide);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const bool dyn = a.work != nullptr;
-    cudaError_t e = narrow ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesNarrow, false>, a)
-                  : deep ? (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, true>, a)
-                                : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesDeep, false>, a))
-                         : (dyn ? cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, true>, a)
-                                : cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide, false>, a));
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide>, a);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
@@ -720,16 +668,8 @@ template <int B>
 int prepare_tc_b() {
     int e = (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)kSmemBytes);
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide, false>,
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesDeep));
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesDeep, true>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesDeep));
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesNarrow, false>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesNarrow));
     return e;
 }
 
@@ -752,9 +692,6 @@ int gemv_tc_prepare() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char *v = getenv("HG_TC_DEEP")) g_tc_deep = atoi(v);
-    if (const char *v = getenv("HG_TC_DYN")) g_tc_dyn = atoi(v);
-    if (const char *v = getenv("HG_TC_CPS")) g_tc_narrow = atoi(v) == 3;
     if (const char *v = getenv("HG_TC_SLICE")) {
         const int64_t sl = atoll(v) / kTileK * kTileK;
         if (sl >= kTileK) g_slice_max = sl;
@@ -857,7 +794,6 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.err = L.err;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
     a.stamps = gemv_stamps_dev();
-    a.work = g_tc_dyn ? L.work : nullptr;
     if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     const int64_t units = a.tile0[ns] * a.S;

@@ -66,12 +66,9 @@ struct StreamLaunch {
     double timeout_s;
     volatile uint32_t *trace = nullptr;  // debug trace words (mapped host) or NULL
     uint32_t trace_id = 0;
-    uint32_t *work = nullptr;  // tcgen05 persistent launch: this launch's [ticket, exit] words (zeroed)
 };
 // SIMT GEMV per-row-group part counters (P > 1) after the 4 words of gbar
 constexpr int kGroupCounters = 1024;
-// tcgen05 persistent launches: work-queue slots (a slot is reused kWorkSlots launches later)
-constexpr int kWorkSlots = 64;
 int launch_gemv_stream(const StreamLaunch &L, void *stream);
 unsigned long long *gemv_stamps_enable(bool on);
 unsigned long long *gemv_stamps_dev();  // NULL unless hg_debug_gemv_stamps enabled them

@@ -7,8 +7,8 @@
 // 16*B*32 multiply-adds per instruction -- so the lane is memory-bound again.
 //
 // Rows are done 16 at a time (a tail of < 16 rows, or K % 32 != 0, goes to the AVX-512 path);
-// x is packed once per call into the pair-interleaved layout.  Each thread configures its tiles on
-// first use (LDTILECFG) and the process asks the kernel for AMX state once (arch_prctl).  fp32
+// x is packed once per job into the pair-interleaved layout.  Every call loads the tile configuration
+// (LDTILECFG) and releases it at the end; the process asks the kernel for AMX state once (arch_prctl).  fp32
 // accumulation of bf16 products like the other lanes; the order of the sums differs from the
 // AVX-512 path, which the CPU rows' tolerance comparison allows.
 #include <immintrin.h>
@@ -34,10 +34,13 @@ struct alignas(64) TileCfg {
     uint8_t rows[16] = {};
 };
 
-// tmm0: C [16 rows][B fp32]; tmm1: A = W [16 rows][32 bf16]; tmm2: B = x pairs [16][B][2 bf16]
+// tmm0: C [16 rows][B fp32]; tmm1: A = W [16 rows][32 bf16]; tmm2: B = x pairs [16][B][2 bf16].
+// Loaded at the start of every call and released at its end: the thread may be the API caller's,
+// where other code (e.g. a oneDNN bf16 kernel) can run AMX with its own configuration and
+// TILERELEASE it in between; a cached "already configured" flag would then run tile instructions
+// on an unconfigured (#UD) or foreign configuration.  LDTILECFG costs ~100 cycles against the
+// ~20 us a call's 16-row blocks take.
 void config_tiles(int B) {
-    static thread_local int configured = 0;
-    if (configured == B) return;
     TileCfg cfg;
     cfg.rows[0] = 16;
     cfg.colsb[0] = (uint16_t)(B * 4);
@@ -46,7 +49,6 @@ void config_tiles(int B) {
     cfg.rows[2] = 16;
     cfg.colsb[2] = (uint16_t)(B * 4);
     _tile_loadconfig(&cfg);
-    configured = B;
 }
 
 // x [B][K] bf16 -> xp[kb][r][b][2]: pair r of k-block kb for batch row b
@@ -112,6 +114,7 @@ void rows_amx(const uint16_t *x, int64_t K, const uint16_t *W, int64_t r0, int64
     const uint16_t *xp = packed_x(x, B, K);
     int64_t r = r0;
     for (; r + 16 <= r1; r += 16) rows16<B>(xp, K, W, r, bias, y, ldy);
+    _tile_release();
     if (r < r1) host_rows_avx512bf16(x, B, K, W, r, r1, bias, y, ldy);
 }
 

@@ -73,8 +73,11 @@ struct PinLane {
                 j = q.front();
                 q.pop_front();
             }
-            // the slot's previous occupant (tag - nslots) must have left for the device
-            if (j.tag > (uint32_t)nslots) {
+            // the slot's previous occupant (tag - nslots) must have left for the device.  After a
+            // timeout the lane is failed: it writes no staging slot any more (one may still be under
+            // DMA), but it still publishes every tag so the copy stream's device-side waits drain
+            // instead of hanging the GPU; the context reports HG_ETIMEOUT at its next call.
+            if (!error && j.tag > (uint32_t)nslots) {
                 const uint32_t need = j.tag - (uint32_t)nslots;
                 const auto t0 = std::chrono::steady_clock::now();
                 for (int spin = 0; (int32_t)(freed[j.slot] - need) < 0; ++spin) {
@@ -89,8 +92,10 @@ struct PinLane {
                 }
             }
             const auto t1 = std::chrono::steady_clock::now();
-            CopyPart cp{j.src, staging + (int64_t)j.slot * slot_bytes, j.bytes, threads};
-            pool_run(pool, copy_part, &cp);
+            if (!error) {
+                CopyPart cp{j.src, staging + (int64_t)j.slot * slot_bytes, j.bytes, threads};
+                pool_run(pool, copy_part, &cp);
+            }
             std::atomic_thread_fence(std::memory_order_release);
             pinned[j.slot] = j.tag;
             _mm_sfence();

@@ -35,14 +35,10 @@ print("BAD" if bad else "OK", bad)
 
 
 @pytest.mark.parametrize("env", [
-    {"HG_TC_DYN": "1"},
     {"HG_TC_LONG_K": "0"},
     {"HG_GEMV_PDL": "0"},
     {"HG_TC_STREAM": "0"},
-    {"HG_TC_DEEP": "1"},
-    {"HG_TC_CPS": "3"},
     {"HG_GEMV_CPS": "1"},
-    {"HG_GEMV_CPS": "1", "HG_GEMV_B1S": "6"},
     {"HG_GEMV_TC_MIN_BATCH": "0"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_keeps_parity(env):
