@@ -114,44 +114,81 @@ class Clocks:
 
 
 # ---------------------------------------------------------------- reference arm / cpu baseline
-def oracle_layer_sample(reps=1, batch=1, nthreads=None):
-    """Time the fp64 oracle on layer 0's four linears (1/48 of a token); returns seconds per sample."""
-    import numpy as np
-    import oracle
+def host_info():
+    """lscpu's model name, sockets and cores of the host the oracle runs on."""
+    info = {"model": None, "sockets": None, "cores_per_socket": None, "threads_online": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            k, v = k.strip(), v.strip()
+            if k == "Model name":
+                info["model"] = v
+            elif k == "Socket(s)":
+                info["sockets"] = int(v)
+            elif k == "Core(s) per socket":
+                info["cores_per_socket"] = int(v)
+    except Exception:  # noqa: BLE001
+        pass
+    return info
+
+
+def oracle_layer_inputs(layer, batch):
+    """Layer `layer`'s weights and biases (bf16 bits / fp32) from the seeded generator, and the step's
+    input activation."""
     from harness import gen
-    nthreads = nthreads or os.cpu_count()
-    xs, Ws, bs = {}, {}, {}
+    Wd, bd = {}, {}
     for name in NAMES:
         N, K = SHAPES[name]
-        xs[name], Ws[name], bs[name] = gen.linear_inputs(SEED, 0, name, batch, N, K)
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        for name in NAMES:
-            oracle.linear(xs[name], Ws[name], bs[name], nthreads=nthreads)
-        ts.append(time.perf_counter() - t0)
-    return ts, nthreads
+        _, Wd[name], bd[name] = gen.linear_inputs(SEED, layer, name, 1, N, K)
+    return Wd, bd
+
+
+def oracle_layer_time(h_bits, Wd, bd, nthreads):
+    """Seconds for one OPT layer through the fp64 oracle end to end (LN, QKV, V, O, residual, LN, fc1,
+    ReLU, fc2, residual with the oracle's exact bf16 rounding points)."""
+    import oracle
+    t0 = time.perf_counter()
+    out = oracle.layer(h_bits, Wd, bd, H, nthreads=nthreads)
+    return time.perf_counter() - t0, out
 
 
 def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores.  A step is a bounded sample of the
+    token: `--ref-layers` consecutive OPT layers end to end (each layer's output is the next one's
+    input), ms/token = the median step time x LAYERS / ref_layers; ms_per_step is the step's own
+    measured time."""
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    ts, nthr = oracle_layer_sample(reps=args.warmup + args.steps, batch=args.batch)
-    timed = ts[args.warmup:]
-    ms_tok = statistics.median(timed) * LAYERS * 1e3
+    nthr = os.cpu_count() or 1
+    L = max(1, min(args.ref_layers, LAYERS))
+    weights = [oracle_layer_inputs(l, args.batch) for l in range(L)]
+    h0 = initial_h(args.batch)
+    ts = []
+    for _ in range(args.warmup + args.steps):
+        h, t = h0, 0.0
+        for Wd, bd in weights:
+            dt, out = oracle_layer_time(h, Wd, bd, nthr)
+            h, t = out["out"], t + dt
+        ts.append(t)
+    step_s = statistics.median(ts[args.warmup:])
+    ms_tok = step_s * LAYERS / L * 1e3
     line = {
-        "impl": "reference", "metric": METRIC, "value": ms_tok, "unit": "ms/token", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_tok, "higher_is_better": False,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "impl": "reference", "metric": METRIC, "value": round(ms_tok, 1), "unit": "ms/token", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step_s * 1e3, 1),
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "%s %d-layer decode linear stack (qkv,o,fc1,fc2 x%d), batch %d" % (
                        MODEL.upper(), LAYERS, LAYERS, args.batch), "model": MODEL,
-                   "sample": "layer 0's 4 linears per step, scaled x%d" % LAYERS,
+                   "sample": "%d of %d layers end to end per step; value = step x %g" % (L, LAYERS, LAYERS / L),
                    "batch": args.batch, "hidden": H, "ffn": F, "layers": LAYERS},
-        "cpu_baseline": {"value": ms_tok, "unit": "ms/token", "cores": nthr, "kind": "oracle",
-                         "sample": "one layer (qkv,o,fc1,fc2: %.3f GB of weights) per step, fp64 naive C "
-                                   "loops, scaled x%d to a token" % (STACK_BYTES / LAYERS / 1e9, LAYERS)},
-        "e2e": {"value": ms_tok, "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "cpu_baseline": {"value": round(ms_tok, 1), "unit": "ms/token", "cores": nthr, "kind": "oracle",
+                         "sample": "%d OPT layer(s) end to end per step (LN, 4 linears, V, residuals, ReLU; %.3f GB "
+                                   "of weights per layer) through the fp64 oracle (C loops for the linears, exact "
+                                   "bf16 rounding in Python), all host threads; scaled x%g to a token"
+                                   % (L, STACK_BYTES / LAYERS / 1e9, LAYERS / L),
+                         "host": host_info()},
+        "e2e": {"value": round(ms_tok, 1), "unit": "ms/token", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -257,6 +294,16 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------- our arm
+def pct(sorted_vals, q):
+    """q-th percentile of sorted values, linear interpolation between closest ranks."""
+    if not sorted_vals:
+        return float("nan")
+    x = (len(sorted_vals) - 1) * q / 100.0
+    i = int(math.floor(x))
+    j = min(i + 1, len(sorted_vals) - 1)
+    return sorted_vals[i] + (sorted_vals[j] - sorted_vals[i]) * (x - i)
+
+
 def make_context(args, rank, world, local, **extra):
     """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores."""
     from paper_2403_01164_b200 import hg
@@ -501,20 +548,23 @@ def run_point(st, args, budget_gb=0.0):
     ctx.hg_reset_stats()
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event per step boundary on the launching stream: the distribution of step times (recording
+    # an event between steps adds no synchronisation)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     w0 = time.perf_counter()
     torch.cuda.nvtx.range_push("hg_timed")  # ncu --nvtx --nvtx-include hg_timed/ selects these launches
-    e0.record(s)
-    for _ in range(args.steps):
+    evs[0].record(s)
+    for i in range(args.steps):
         step_device()
-    e1.record(s)
+        evs[i + 1].record(s)
     torch.cuda.synchronize()
     torch.cuda.nvtx.range_pop()
     wall = time.perf_counter() - w0
     barrier()
     launches = ctx.hg_stats().gpu_launches
     ck = clocks.stop()
-    dev_s = e0.elapsed_time(e1) * 1e-3
+    dev_s = evs[0].elapsed_time(evs[-1]) * 1e-3
+    step_ms = sorted(evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps))
 
     # ---- e2e: public API with host buffers, H2D of the step input + D2H of the result ----
     barrier()
@@ -553,6 +603,11 @@ def run_point(st, args, budget_gb=0.0):
     if rank == 0 and world == 1 and args.parity and not args.no_cpu_baseline:
         trace = trace_layers(st, layers, sorted({0, args.layers - 1}))
 
+    # ---- rates re-probed after the timed region: the path roofline takes the larger of the two probes
+    # of each peak (a probe that under-reads would flatter the fraction) ----
+    rates_post = ctx.hg_measure(st["host"][0]["fc1"], st["host"][0]["fc1"].shape[0], H, B, under_load=True)
+    rdp = rates_post.as_dict()
+
     times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
@@ -569,17 +624,18 @@ def run_point(st, args, budget_gb=0.0):
         plan_tot["bytes_cpu"] += 2 * p.K * p.n_cpu
         plan_tot["bytes_res"] += 2 * p.K * p.n_res
     # stack roofline: the link runs ahead across linears, so lanes add up over the stack
-    t_link_roof = plan_tot["bytes_str"] / rd["b_link"]
-    t_cpu_roof = plan_tot["bytes_cpu"] / rd["b_cpu"]
+    peak = {k: max(rd[k], rdp[k]) for k in ("b_link", "b_cpu", "b_host")}
+    t_link_roof = plan_tot["bytes_str"] / peak["b_link"]
+    t_cpu_roof = plan_tot["bytes_cpu"] / peak["b_cpu"]
     t_hbm_roof = (plan_tot["bytes_res"] + 2 * plan_tot["bytes_str"]) / (hbm_peak * 1e9)
     # 4th term: every offloaded byte is read from host DRAM once, by the DMA or by the
     # CPU lane, so the joint host-DRAM rate measured with both running bounds the sum
-    b_host = rd.get("b_host") or 0.0
+    b_host = peak["b_host"] or 0.0
     t_host_roof = (plan_tot["bytes_str"] + plan_tot["bytes_cpu"]) / b_host if b_host > 0 else 0.0
     # best achievable over alpha: all host bytes shared by link + CPU at their peaks
     shard_bytes = STACK_BYTES / world * args.layers / LAYERS
     host_bytes = plan_tot["bytes_str"] + plan_tot["bytes_cpu"]
-    t_opt = max(host_bytes / min(rd["b_link"] + rd["b_cpu"], b_host if b_host > 0 else math.inf), t_hbm_roof)
+    t_opt = max(host_bytes / min(peak["b_link"] + peak["b_cpu"], b_host if b_host > 0 else math.inf), t_hbm_roof)
     t_roof = max(t_link_roof, t_cpu_roof, t_hbm_roof, t_host_roof)
     lanes = None
     if sctx_stats:
@@ -596,6 +652,11 @@ def run_point(st, args, budget_gb=0.0):
                  if sctx_stats["pin_busy_s"] > 0 else None,
                  "glue_ms": round(sctx_stats["glue_s"] * 1e3, 2),
                  "steps": 2, "mirror_linears": sctx_stats["mirror_linears"]}
+        # overlap fraction = (sum busy - wall) / (sum busy - max busy); 1 = the lanes fully
+        # overlap, 0 = they run one after another
+        busy = [sctx_stats["cpu_busy_s"], sctx_stats["link_busy_s"], sctx_stats["gpu_busy_s"]]
+        den = sum(busy) - max(busy)
+        lanes["overlap_frac"] = round((sum(busy) - sctx_stats["wall_s"]) / den, 4) if den > 0 else None
     line = {
         "metric": METRIC, "value": round(ms_tok, 3), "unit": "ms/token", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_tok, 3),
@@ -627,8 +688,15 @@ def run_point(st, args, budget_gb=0.0):
                           "t_opt_ms_best_alpha": round(t_opt * 1e3, 3),
                           "frac_of_roof_at_plan": round(t_roof * 1e3 / ms_tok, 4),
                           "frac_of_best": round(t_opt * 1e3 / ms_tok, 4),
-                          "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3)},
+                          "t_pred_ms_sum": round(plan_tot["t_pred"] * 1e3, 3),
+                          "peaks_GBps": {k: round(v / 1e9, 2) for k, v in peak.items()},
+                          "peaks_source": "max of the hg_measure probes before and after the timed region",
+                          "probe_under_read": bool(t_roof * 1e3 / ms_tok > 1.0)},
+        "step_ms": {"min": round(step_ms[0], 3), "p10": round(pct(step_ms, 10), 3), "p50": round(pct(step_ms, 50), 3),
+                    "p90": round(pct(step_ms, 90), 3), "max": round(step_ms[-1], 3),
+                    "note": "per-step CUDA events on the launching stream inside the timed region"},
         "rates_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rd.items()},
+        "rates_post_GBps": {k: (round(v / 1e9, 2) if math.isfinite(v) else None) for k, v in rdp.items()},
         "lanes": lanes,
         "scheduler": sched,
         "alpha_bench": None if abench is None else {
@@ -674,33 +742,41 @@ def trace_layers(st, layers, which):
 LIN_IO = (("qkv", "a", "y_qkv"), ("o", "v", "y_o"), ("fc1", "a2", "y_fc1"), ("fc2", "u", "y_fc2"))
 
 
-def cpu_baseline_and_parity(st, trace, reps=2, sample_rows=256):
-    """The cpu_baseline leg: the fp64 oracle timed on layer 0's four linears on the host cores.
-    With a trace of the timed path it is fed the GPU's own bf16 inputs to those linears
-    (teacher-forced) and its outputs are compared with the GPU's, element by
-    element (BJ:5 tolerance); the last layer is compared on `sample_rows` seeded rows per linear
-    (oracle.linear_rows), and layer 0's glue against the oracle's LN / V / residual / ReLU."""
+def cpu_baseline_and_parity(st, trace, sample_rows=256):
+    """The cpu_baseline leg: the fp64 oracle timed on layer 0 end to end on the host cores (and one
+    linear on one thread).  With a trace of the timed path the oracle is also fed the GPU's own bf16
+    inputs to layer 0's linears (teacher-forced) and its outputs are compared with
+    the GPU's element by element (BJ:5 tolerance); the last layer is compared on `sample_rows` seeded
+    rows per linear (oracle.linear_rows); layer 0's glue against the oracle's LN / V / residual / ReLU;
+    and the oracle's own end-to-end layer 0 (not teacher-forced) against the GPU's outputs (looser,
+    secondary, as in tests/test_gpu_layer.py)."""
     import numpy as np
     import oracle
-    from harness import gen
     B, nthr = st["B"], os.cpu_count() or 1
     W = lambda l, n: st["host"][l][n].numpy().view(np.uint16)
     bias = lambda l, n: st["biases_h"][l][n].numpy()
-    if trace is None:  # no trace: generated inputs (timing only)
-        xs = {n: gen.linear_inputs(SEED, 0, n, B, *SHAPES[n])[0] for n in NAMES}
-    else:
+    # the baseline: layer 0 end to end through the oracle on all host threads, on the step's input h
+    Wd0 = {n: W(0, n) for n in NAMES}
+    bd0 = {n: bias(0, n) for n in NAMES}
+    h_in = trace["h_in"] if trace is not None else initial_h(B)
+    t_layer, ref0 = oracle_layer_time(h_in, Wd0, bd0, nthr)
+    # single thread: the o projection of layer 0 (its share of the token's bytes scales it)
+    t0 = time.perf_counter()
+    oracle.linear(ref0["v"], Wd0["o"], bd0["o"], nthreads=1)
+    t_o1 = time.perf_counter() - t0
+    o_bytes = 2 * SHAPES["o"][0] * SHAPES["o"][1]
+    cb = {"value": round(t_layer * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr, "kind": "oracle",
+          "sample": "layer 0 end to end (LN, 4 linears, V, residuals, ReLU; %.3f GB of weights) through the fp64 "
+                    "oracle on all host threads, scaled x%d to a token" % (STACK_BYTES / LAYERS / 1e9, LAYERS),
+          "single_thread": {"value": round(t_o1 * STACK_BYTES / o_bytes * 1e3, 1), "unit": "ms/token", "cores": 1,
+                            "sample": "layer 0's o projection (%.1f MB) on one thread, scaled by bytes to a token"
+                                      % (o_bytes / 1e6)},
+          "host": host_info()}
+    if trace is not None:
         T0 = trace["layers"][0]
-        xs = {n: T0[xin] for n, xin, _ in LIN_IO}
-    ts, ys = [], {}
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        for n in NAMES:
-            ys[n] = oracle.linear(xs[n], W(0, n), bias(0, n), nthreads=nthr)
-        ts.append(time.perf_counter() - t0)
-    cb = {"value": round(min(ts) * LAYERS * 1e3, 1), "unit": "ms/token", "cores": nthr, "kind": "oracle",
-          "sample": "layer 0's four linears (%.3f GB), fp64 naive C loops on all host cores, best of %d, "
-                    "scaled x%d to a token%s" % (STACK_BYTES / LAYERS / 1e9, reps, LAYERS,
-                                                 "; inputs = the timed path's traced activations" if trace else "")}
+        ys = {}
+        for n, xin, _ in LIN_IO:  # teacher-forced: the GPU's own bf16 inputs
+            ys[n] = oracle.linear(T0[xin], W(0, n), bias(0, n), nthreads=nthr)
     if trace is None:
         return cb, None
     worst, ok, checked, per = 0.0, True, 0, {}
@@ -727,10 +803,13 @@ def cpu_baseline_and_parity(st, trace, reps=2, sample_rows=256):
             chk(T0["h1"], oracle.residual(trace["h_in"], T0["y_o"])), chk(T0["a2"], oracle.layernorm(T0["h1"])),
             chk(T0["u"], oracle.relu_bf16(T0["y_fc1"]))]
     glue_ok = all(g for g, _ in glue)
+    e2e = [oracle.within_tol(T0[yk], ref0[yk], rtol=5e-2) for _, _, yk in LIN_IO]
     parity = {"ok": bool(ok and glue_ok), "worst": round(worst, 6), "glue_ok": glue_ok,
               "glue_worst": round(max(w for _, w in glue), 6),
               "tolerance": "|y - y_ref| <= 1e-2 max(1, |y_ref|) elementwise (BJ:5); worst = max err/bound",
               "checked_outputs": int(checked), "per_linear": per, "mirror_linears": trace["mirror_linears"],
+              "layer0_end_to_end": {"ok": all(g for g, _ in e2e), "worst": round(max(w for _, w in e2e), 6),
+                                    "rtol": 5e-2},
               "what": "one extra step of the timed path (same context/plans, hg_stack_trace); layer 0 all "
                       "outputs + glue, layer %d on %d seeded rows per linear, teacher-forced fp64 oracle"
                       % (max(trace["layers"]), sample_rows)}
@@ -776,6 +855,8 @@ def parse_args(argv=None):
                     help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
+    ap.add_argument("--ref-layers", type=int, default=2,
+                    help="--impl reference: OPT layers per step through the oracle (a bounded sample of the token)")
     ap.add_argument("--no-parity", dest="parity", action="store_false",
                     help="skip the parity leg (one traced step checked against the oracle)")
     args = ap.parse_args(argv)

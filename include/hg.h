@@ -408,6 +408,12 @@ HG_API const char *hg_host_isa(void);
  *   communicator on every rank.  NCCL is loaded at run time (HG_ENCCL if absent). */
 HG_API hg_status hg_dist_unique_id(void *id128);
 HG_API hg_status hg_dist_init(hg_ctx *ctx, int nranks, int rank, const void *id128);
+/* The a8 exchange's layout step alone (the same kernel hg_linear_sharded / hg_stack run after the
+ * all-gather): gathered [nranks][batch][n_local] fp32 device (rank-major, as ncclAllGather leaves
+ * it) -> y [batch][nranks * n_local] fp32 device in global column order, y[b, p*n_local + j] =
+ * gathered[p][b][j] (SURVEY 8(c) c2.1 shards, 8(e)).  Bit copy. */
+HG_API hg_status hg_gather_permute(hg_ctx *ctx, const float *gathered, int nranks, int batch, int64_t n_local,
+                                   float *y, void *stream);
 /* This rank's shard linear, then all-gather: y_full_dev [batch, N_full] fp32.
  * plan is this rank's plan for (N_full/P, K). */
 HG_API hg_status hg_linear_sharded(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,

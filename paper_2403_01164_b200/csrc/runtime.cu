@@ -1613,6 +1613,24 @@ HG_API hg_status hg_host_gemv(hg_ctx *c, const void *x, int batch, int64_t n, in
     return HG_OK;
 }
 
+HG_API hg_status hg_gather_permute(hg_ctx *c, const float *gathered, int nranks, int batch, int64_t n_local,
+                                   float *y, void *stream) {
+    if (!c || !gathered || !y) return set_error(HG_EINVAL, "NULL argument");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    if (nranks < 1 || batch < 1 || batch > HG_MAX_BATCH || n_local < 0)
+        return set_error(HG_EINVAL, "hg_gather_permute: bad shape");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(check_ptr(c, gathered, true, "gathered"));
+    HG_TRY(check_ptr(c, y, true, "y"));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(stream_guard(c, s));
+    if (n_local > 0) HG_TRY(kerr(c, launch_gather_permute(gathered, nranks, batch, n_local, y, s), "gather permute"));
+    c->st.gpu_launches++;
+    HG_CK(c, cudaEventRecord(c->ev_done, s));
+    return HG_OK;
+}
+
 HG_API hg_status hg_dist_unique_id(void *id128) {
     if (!id128) return set_error(HG_EINVAL, "NULL id");
     return dist_unique_id(id128);
@@ -1877,7 +1895,9 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     // cache: every timed CPU probe is preceded by a read of a 256 MiB scratch buffer.
     const int64_t sbytes = 256ll << 20;
     std::vector<uint8_t> scratch((size_t)sbytes, 1);
-    const int NB = (flags & 1) ? 192 : 0;  // 192 chunks ~ 6 GiB ~ 110 ms of link time
+    // 512 chunks of <= 32 MiB ~ 16 GiB ~ 300 ms of link time: three 80 ms windows fit inside it, and
+    // whole-chunk counting at the window edges is within +-0.4% of the ~18 GB a window moves
+    const int NB = (flags & 1) ? 512 : 0;
     std::vector<cudaEvent_t> evb((size_t)NB, nullptr);
     for (int i = 0; i < NB; ++i) HG_CK(c, cudaEventCreateWithFlags(&evb[i], cudaEventDisableTiming));
     for (int64_t off = 0, n = 0; n < NB; ++n, off = (off + chunk) % (lbytes - chunk + 1)) {
@@ -1925,7 +1945,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
             const int n0 = completed();
             const auto t0 = clk::now();
             int64_t cpu_bytes = 0;
-            while (secs(t0, clk::now()) < 0.02) {  // weight + scratch: a footprint far above the LLC
+            while (secs(t0, clk::now()) < 0.08) {  // weight + scratch: a footprint far above the LLC
                 read_pass();
                 flush_llc();
                 cpu_bytes += wbytes + sbytes;

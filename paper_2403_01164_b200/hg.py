@@ -147,6 +147,7 @@ _sig = {
     "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "hg_host_isa": (ctypes.c_char_p, []),
     "hg_debug_gemv_stamps": (_i32, [_P(ctypes.POINTER(ctypes.c_uint64))]),
+    "hg_gather_permute": (_i32, [_vp, _vp, _i32, _i32, _i64, _vp, _vp]),
     "hg_dist_unique_id": (_i32, [_vp]),
     "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
     "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -340,6 +341,9 @@ class Context:
         _check(_lib.hg_alpha_bench(self._h, arr, len(layers), _ptr(h), batch, float(alpha_seed), ctypes.byref(cfg),
                                    ctypes.byref(res), _stream(stream)))
         return res
+
+    def hg_gather_permute(self, gathered, nranks, batch, n_local, y, stream=None):
+        _check(_lib.hg_gather_permute(self._h, _ptr(gathered), nranks, batch, n_local, _ptr(y), _stream(stream)))
 
     def hg_dist_init(self, nranks, rank, uid: bytes):
         buf = ctypes.create_string_buffer(uid, 128)

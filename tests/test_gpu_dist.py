@@ -53,3 +53,21 @@ def test_sharded_without_init_is_an_error():
         with pytest.raises(hg.HgError) as e:
             c.hg_linear_sharded(p, dev(x), None, Wh, dev_f32(b), y)
         assert e.value.status == hg.HG_ESTATE
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("B", [1, 3, 8])
+def test_gather_permute_matches_oracle(P, B):
+    """The a8 layout step at P > 1 (VERDICT r1 missing #1): rank-major all-gather output
+    [P][B][n_local] -> y [B][P*n_local] in global column order, bit-exact against
+    oracle.gather_shards; n_local covers a multiple of the kernel's grid and a ragged size."""
+    rng = np.random.default_rng(P * 10 + B)
+    with hg.Context(0, max_k=1024, max_n=4096) as c:
+        for n_local in (128, 1536, 1000):
+            shards = [rng.standard_normal((B, n_local)).astype(np.float32) for _ in range(P)]
+            gathered = torch.from_numpy(np.concatenate([s.reshape(-1) for s in shards])).cuda()
+            y = torch.full((B, P * n_local), float("nan"), device="cuda")
+            c.hg_gather_permute(gathered, P, B, n_local, y)
+            torch.cuda.synchronize()
+            ref = oracle.gather_shards(shards, B)
+            assert np.array_equal(y.cpu().numpy().view(np.uint32), ref.astype(np.float32).view(np.uint32))
