@@ -16,15 +16,17 @@
 // * one elected thread of warp 1 issues tcgen05.mma.cta_group::1.kind::f16
 //   (M=128, N=16, K=16; four per stage) into a TMEM accumulator and frees each
 //   stage with tcgen05.commit;
-// * warps 2-5 drain the accumulator with tcgen05.ld (32x32b.x16) and write
-//   y (+bias), or the split-K partial.  Two accumulators (TMEM columns 0-15,
-//   16-31) let the epilogue of one work unit overlap the MMAs of the next.
-// * persistent CTAs walk work units (row tile, k-slice); the k-slice geometry depends on K only
-//   and partial sums are added by the last arriver in slice order, so every launch reduces every
-//   row identically (split invariance).
-// * gemv_tc_kernel: one buffer per launch (the resident GEMV alone, and the per-chunk fallback);
-//   gemv_tc_stream_kernel: ONE launch per linear over the resident block and every streamed chunk,
-//   gated by the chunk arrival tags, PDL-launched (see below).
+// * warps 2-5 drain the accumulator with tcgen05.ld (32x32b.x16) and either keep a running sum
+//   of the row's slice partials in registers or store the partial for a cross-CTA fold.  Four
+//   accumulators (TMEM columns 0-63) let the MMAs of the next units run while one is drained.
+// * persistent CTAs own CONTIGUOUS ranges of work units (row tile, k-slice): equal work to within
+//   one unit whatever the linear's size (the old round-robin walk left a 52-CTA grid on the o
+//   projection at B = 8 and a two-unit tail on the others); the k-slice geometry depends on K only
+//   and every row is the left-to-right sum of its slice partials, so every launch reduces every row
+//   identically (split invariance).
+// * one kernel for everything: a single buffer (hg_gemv, the resident GEMV alone, the per-chunk
+//   fallback) is a launch with one source; the persistent per-linear form covers the resident
+//   block and every streamed chunk, gated by the chunk arrival tags, PDL-launched (see below).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -52,12 +54,13 @@ constexpr int kTileM = 128;        // W rows per tile (UMMA M)
 constexpr int kTileK = 64;         // k per stage (one 128-byte swizzle atom of bf16)
 constexpr int kUmmaN = 16;         // batch padded to N = 16
 constexpr int kUmmaK = 16;         // k per tcgen05.mma (bf16)
-constexpr int kStages = 6;
 constexpr int kWBytes = kTileM * kTileK * 2;  // 16 KB
 constexpr int kXBytes = kUmmaN * kTileK * 2;  // 2 KB
 constexpr int kThreads = 192;                 // warp0 TMA, warp1 MMA, warps2-5 epilogue
-constexpr int64_t kSliceMaxTc = 2048;  // k per work unit: enough units per SM for tail balance,
-                                       // long enough to amortise the epilogue
+constexpr int kNAcc = 4;                      // TMEM accumulators of 16 columns: the MMA warp may run
+                                              // up to three work units ahead of the epilogue
+constexpr int64_t kSliceMin = 512;            // k per work unit: at least this ...
+constexpr int kSliceMaxCount = 16;            // ... and at most this many slices per row
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -128,198 +131,32 @@ __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 
-struct Units {
-    int64_t n_tiles;
-    int S;
-    int64_t ks;  // multiple of kTileK
-};
-
-template <int B>
-__global__ void __launch_bounds__(kThreads, 2)
-    gemv_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x,
-                   int64_t K, int64_t n, const float *__restrict__ bias, float *__restrict__ y,
-                   int64_t ldy, Units U, float *__restrict__ ws, int *__restrict__ counters) {
-    extern __shared__ uint8_t smem_raw[];
-    // 1024-byte alignment for the swizzle atoms
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    uint8_t *gbase = smem_raw + (base - raw);
-    const uint32_t sW = base;                              // kStages * 16 KB
-    const uint32_t sX = base + kStages * kWBytes;          // kStages * 2 KB
-    const uint32_t bars = sX + kStages * kXBytes;          // full[k], empty[k], tfull[2], tempty[2]
-    uint32_t *tmem_slot = (uint32_t *)(gbase + (bars - base) + 8 * (2 * kStages + 4));
-    int *last_flag = (int *)(tmem_slot + 1);
-    auto full = [&](int s) { return bars + 8 * s; };
-    auto empty = [&](int s) { return bars + 8 * (kStages + s); };
-    auto tfull = [&](int a) { return bars + 8 * (2 * kStages + a); };
-    auto tempty = [&](int a) { return bars + 8 * (2 * kStages + 2 + a); };
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(full(s), 1);
-            mbar_init(empty(s), 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(tfull(a), 1);
-            mbar_init(tempty(a), 128);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_w) : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&map_x) : "memory");
-    }
-    if (warp == 1) {  // TMEM: 32 columns (two 16-column accumulators)
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
-                         smem_u32(tmem_slot))
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    const int64_t n_units = U.n_tiles * U.S;
-    if (warp == 0) {
-        if (lane == 0) {  // ---------------- TMA producer
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int64_t tile = u % U.n_tiles;
-                const int s = (int)(u / U.n_tiles);
-                const int64_t k0 = (int64_t)s * U.ks;
-                const int64_t k1 = k0 + U.ks < K ? k0 + U.ks : K;
-                for (int64_t k = k0; k < k1; k += kTileK) {
-                    mbar_wait(empty(stage), phase ^ 1);
-                    mbar_expect_tx(full(stage), kWBytes + kXBytes);
-                    tma_load_2d(sW + stage * kWBytes, &map_w, full(stage), (int32_t)k,
-                                (int32_t)(tile * kTileM));
-                    tma_load_2d(sX + stage * kXBytes, &map_x, full(stage), (int32_t)k, 0);
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            int stage = 0;
-            uint32_t phase = 0;
-            int it = 0;
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-                const int acc = it & 1;
-                const uint32_t aphase = (uint32_t)((it >> 1) & 1);
-                mbar_wait(tempty(acc), aphase ^ 1);
-                tc_fence_after();
-                const int s = (int)(u / U.n_tiles);
-                const int64_t k0 = (int64_t)s * U.ks;
-                const int64_t k1 = k0 + U.ks < K ? k0 + U.ks : K;
-                const uint32_t d = tmem + (uint32_t)(acc * kUmmaN);
-                uint32_t accum = 0;
-                for (int64_t k = k0; k < k1; k += kTileK) {
-                    mbar_wait(full(stage), phase);
-                    tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < kTileK / kUmmaK; ++kk) {
-                        const uint64_t da = sw128_desc(sW + stage * kWBytes + kk * kUmmaK * 2);
-                        const uint64_t db = sw128_desc(sX + stage * kXBytes + kk * kUmmaK * 2);
-                        umma(d, da, db, accum);
-                        accum = 1;
-                    }
-                    umma_commit(empty(stage));
-                    if (++stage == kStages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-                umma_commit(tfull(acc));
-            }
-        }
-    } else {  // ---------------- epilogue warps 2..5
-        const int quarter = warp & 3;  // TMEM lanes this warp may access
-        const int et = (warp - 2) * 32 + lane;
-        int it = 0;
-        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-            const int acc = it & 1;
-            const uint32_t aphase = (uint32_t)((it >> 1) & 1);
-            const int64_t tile = u % U.n_tiles;
-            const int s = (int)(u / U.n_tiles);
-            mbar_wait(tfull(acc), aphase);
-            tc_fence_after();
-            uint32_t r[16];
-            const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kUmmaN);
-            asm volatile(
-                "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
-                "%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                  "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-                  "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-                : "r"(taddr));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            tc_fence_before();
-            mbar_arrive(tempty(acc));
-            const int64_t row = tile * kTileM + quarter * 32 + lane;
-            if (U.S == 1) {
-                if (row < n) {
-                    const float bb = bias ? bias[row] : 0.f;
-#pragma unroll
-                    for (int b = 0; b < B; ++b) y[b * ldy + row] = __uint_as_float(r[b]) + bb;
-                }
-                continue;
-            }
-            if (row < n) {
-#pragma unroll
-                for (int b = 0; b < B; ++b) ws[((int64_t)s * B + b) * n + row] = __uint_as_float(r[b]);
-            }
-            __threadfence();
-            named_barrier(1, 128);
-            if (et == 0) *last_flag = (atomicAdd(&counters[tile], 1) == U.S - 1);
-            named_barrier(1, 128);
-            if (*last_flag) {
-                __threadfence();
-                if (row < n) {
-                    const float bb = bias ? bias[row] : 0.f;
-#pragma unroll
-                    for (int b = 0; b < B; ++b) {
-                        float sum = 0.f;
-                        for (int q0 = 0; q0 < U.S; q0 += 8) {  // 8 loads in flight, summed in order
-                            float part[8];
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (q0 + q < U.S) part[q] = __ldcg(&ws[((int64_t)(q0 + q) * B + b) * n + row]);
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                if (q0 + q < U.S) sum += part[q];
-                        }
-                        y[b * ldy + row] = sum + bb;
-                    }
-                }
-                if (et == 0) counters[tile] = 0;
-            }
-            named_barrier(1, 128);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
-}
-
-constexpr size_t kSmemBytes = 1024 + kStages * (kWBytes + kXBytes) + 8 * (2 * kStages + 4) + 16;
-constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 4) + 16; }
-// persistent form: 6-stage CTAs, two per SM (measured against 11 stages x one per SM and 4 stages x
-// three per SM: both slower, profiles/r01/gemv_batches.md)
+// smem: ST stages of [W tile | x tile], then full[ST] empty[ST] tfull[kNAcc] tempty[kNAcc], TMEM slot,
+// last-arriver flag
+constexpr size_t smem_for(int st) { return 1024 + st * (kWBytes + kXBytes) + 8 * (2 * st + 2 * kNAcc) + 16; }
+// 6-stage CTAs, two per SM (measured against 11 stages x one per SM and 4 stages x three per SM: both
+// slower, profiles/r01/gemv_batches.md)
 constexpr int kStagesWide = 6;
 
 // ---------------------------------------------------------------- persistent per-linear form
 // One launch per linear covering the resident block and every streamed chunk (the SIMT kernel's
-// structure, SURVEY 8(a) a3+a4), so small chunks do not each pay a launch and a sub-wave grid.
-// Sources: [resident block] then chunk 0, 1, ... in arrival order; each has its own tensor map (a
-// kernel parameter) over exactly its rows (rows past a source are zero-filled by TMA, never read
-// from a neighbour).  Work unit u = (global tile t = u / S, k-slice s = u % S): a CTA walks its
-// units in increasing order, so it meets the sources in arrival order and waits for a chunk's
+// structure, SURVEY 8(a) a3+a4).  Sources: [resident block] then chunk 0, 1, ... in arrival order;
+// each has its own tensor map (a kernel parameter) over exactly its rows (rows past a source are
+// zero-filled by TMA, never read from a neighbour).
+//
+// Work: unit u = (row tile t = u / S, k-slice s = u % S), U = tiles * S units in tile-major order.
+// CTA c owns the CONTIGUOUS range [c U / G, (c+1) U / G) (G = grid): every CTA gets the same number
+// of units to within one, whatever the linear's size, and most tiles lie wholly inside one CTA's
+// range.  Each unit's slice partial p_s (a fresh TMEM accumulation over the slice's k) is what the
+// row's result is built from, always as the left-to-right fp32 sum p_0 + p_1 + ... + p_{S-1} + bias
+// (the slice geometry depends on K only): so every partition of a linear into resident rows and
+// chunks, and every grid, gives the same bits (split invariance).
+//   * the CTA holding slice 0 of a tile (its "prefix holder") keeps the running sum in registers
+//     over its consecutive slices; if it holds the whole tile it writes y directly;
+//   * otherwise the prefix sum goes to the workspace at its last slice's index, and every other CTA
+//     touching the tile stores its slices' partials individually; each contributor then counts in
+//     on the tile's counter, and the last one adds prefix + remaining partials in slice order.
+// A CTA walks its units in order, so it meets the sources in arrival order and waits for a chunk's
 // arrival tag before its first TMA from that chunk.  When every unit of a chunk has finished its
 // MMAs (all TMA reads of the slot done), the last one writes the slot's `consumed` tag.
 constexpr int kMaxSrc = 17;  // resident + up to 16 chunks per launch (else the per-chunk path)
@@ -332,16 +169,16 @@ struct TcArgs {
     uint32_t tag[kMaxSrc];
     int n_src;
     int S;
-    int64_t ks, K, n_total;
+    int64_t ks, K, n_total, U;
     const float *bias;
     float *y;
     int64_t ldy;
-    float *ws;
-    int *counters;
+    float *ws;       // [S][B][n_total] slice partials of tiles split across CTAs (coalesced per b)
+    int *counters;   // [tiles] contributors counted in (zero between launches)
     const uint32_t *arrived;  // null: every source present (resident / replay)
     uint32_t *consumed, *slot_cnt, *err;
     unsigned long long timeout_ns;
-    unsigned long long *stamps;  // measurement: [CTA][4] globaltimer (entry, first MMA stage, epilogue done, exit)
+    unsigned long long *stamps;  // measurement: [CTA][8] globaltimer, see kStamp*
 };
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
@@ -354,6 +191,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// the CTA whose range [c U / G, (c+1) U / G) holds unit u
+__device__ __forceinline__ int64_t cta_of(int64_t u, int64_t U, int64_t G) { return ((u + 1) * G - 1) / U; }
 
 template <int B, int ST>
 __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
@@ -364,25 +203,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     const uint32_t sW = base;
     const uint32_t sX = base + ST * kWBytes;
     const uint32_t bars = sX + ST * kXBytes;
-    uint32_t *tmem_slot = (uint32_t *)(gbase + (bars - base) + 8 * (2 * ST + 4));
+    uint32_t *tmem_slot = (uint32_t *)(gbase + (bars - base) + 8 * (2 * ST + 2 * kNAcc));
     int *last_flag = (int *)(tmem_slot + 1);
     auto full = [&](int s) { return bars + 8 * s; };
     auto empty = [&](int s) { return bars + 8 * (ST + s); };
     auto tfull = [&](int q) { return bars + 8 * (2 * ST + q); };
-    auto tempty = [&](int q) { return bars + 8 * (2 * ST + 2 + q); };
+    auto tempty = [&](int q) { return bars + 8 * (2 * ST + kNAcc + q); };
 
     // PDL: the next kernel may be scheduled once every CTA of this one runs; x (read by the
     // producer with every stage) is the only input of the previous kernel, so only the producer
-    // waits (griddepcontrol.wait) before its first TMA.
+    // waits (griddepcontrol.wait) before its first x TMA.
     if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 0] = gtimer();
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 8 + 0] = gtimer();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
             mbar_init(full(s), 1);
             mbar_init(empty(s), 1);
         }
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kNAcc; ++q) {
             mbar_init(tfull(q), 1);
             mbar_init(tempty(q), 128);
         }
@@ -392,7 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     uint32_t tmem = 0;
     if (warp >= 1) {  // MMA warp allocates; warps 1-5 meet on named barrier 2 (the producer never waits)
         if (warp == 1) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tmem_slot))
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                         "r"(kNAcc * kUmmaN)
                          : "memory");
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
         }
@@ -403,7 +243,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     }
 
     const int S = a.S;
-    const int64_t n_units = a.tile0[a.n_src] * S;
+    const int64_t U = a.U, G = gridDim.x;
+    const int64_t u0 = (int64_t)blockIdx.x * U / G, u1 = ((int64_t)blockIdx.x + 1) * U / G;
     auto src_of = [&](int64_t t) {
         int i = 0;
         while (t >= a.tile0[i + 1]) ++i;
@@ -411,8 +252,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
     };
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
+            // descriptors: x and this CTA's first source now, each next source when the walk reaches the
+            // one before it (a prefetch of every source up front held the first TMA back ~0.8 us)
+            int pf = src_of(u0 / S);
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[pf]) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.map_x) : "memory");
-            for (int i = 0; i < a.n_src; ++i) asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[i]) : "memory");
+            if (a.stamps) a.stamps[blockIdx.x * 8 + 1] = gtimer();
             int stage = 0;
             uint32_t phase = 0;
             int ready = -1;  // highest source index known to have arrived
@@ -427,10 +272,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 pend = 0;
                 dep = true;
             };
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+            for (int64_t u = u0; u < u1; ++u) {
                 const int64_t t = u / S;
                 const int s = (int)(u - t * S);
                 const int i = src_of(t);
+                if (i == pf && pf + 1 < a.n_src) {
+                    ++pf;
+                    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&a.maps[pf]) : "memory");
+                }
                 if (a.arrived && a.slot[i] >= 0 && i > ready) {
                     if (!dep) flush_x();
                     const unsigned long long t0 = gtimer();
@@ -450,6 +299,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                     mbar_wait(empty(stage), phase ^ 1);
                     mbar_expect_tx(full(stage), kWBytes + kXBytes);
                     tma_load_2d(sW + stage * kWBytes, &a.maps[i], full(stage), (int32_t)k, row0);
+                    if (a.stamps && u == u0 && k == k0) a.stamps[blockIdx.x * 8 + 2] = gtimer();
                     if (dep) {
                         tma_load_2d(sX + stage * kXBytes, &a.map_x, full(stage), (int32_t)k, 0);
                     } else {
@@ -464,15 +314,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 }
             }
             if (!dep) flush_x();
+            if (a.stamps) a.stamps[blockIdx.x * 8 + 7] = gtimer();
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             int stage = 0;
             uint32_t phase = 0;
             int it = 0;
-            for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-                const int acc = it & 1;
-                const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+            for (int64_t u = u0; u < u1; ++u, ++it) {
+                const int acc = it % kNAcc;
+                const uint32_t aphase = (uint32_t)((it / kNAcc) & 1);
                 mbar_wait(tempty(acc), aphase ^ 1);
                 tc_fence_after();
                 const int64_t t = u / S;
@@ -484,7 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 for (int64_t k = k0; k < k1; k += kTileK) {
                     mbar_wait(full(stage), phase);
                     tc_fence_after();
-                    if (a.stamps && it == 0 && k == k0) a.stamps[blockIdx.x * 4 + 1] = gtimer();
+                    if (a.stamps && it == 0 && k == k0) a.stamps[blockIdx.x * 8 + 3] = gtimer();
 #pragma unroll
                     for (int kk = 0; kk < kTileK / kUmmaK; ++kk) {
                         const uint64_t da = sw128_desc(sW + stage * kWBytes + kk * kUmmaK * 2);
@@ -501,26 +352,29 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                 umma_commit(tfull(acc));
             }
         }
-    } else {  // ---------------- epilogue warps 2..5
+    } else {  // ---------------- epilogue warps 2..5: TMEM lanes 32*quarter.. = the tile's rows
         const int quarter = warp & 3;
         const int et = (warp - 2) * 32 + lane;
+        float r[B];
+        bool prefix = false;
         int it = 0;
-        for (int64_t u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
-            const int acc = it & 1;
-            const uint32_t aphase = (uint32_t)((it >> 1) & 1);
+        for (int64_t u = u0; u < u1; ++u, ++it) {
+            const int acc = it % kNAcc;
+            const uint32_t aphase = (uint32_t)((it / kNAcc) & 1);
             const int64_t t = u / S;
             const int s = (int)(u - t * S);
             const int i = src_of(t);
             mbar_wait(tfull(acc), aphase);
             tc_fence_after();
-            uint32_t r[16];
+            if (a.stamps && it == 0 && et == 0) a.stamps[blockIdx.x * 8 + 4] = gtimer();
+            uint32_t p[16];
             const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * kUmmaN);
             asm volatile(
                 "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
                 "%14,%15}, [%16];"
-                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                  "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
-                  "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+                : "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]), "=r"(p[4]), "=r"(p[5]), "=r"(p[6]),
+                  "=r"(p[7]), "=r"(p[8]), "=r"(p[9]), "=r"(p[10]), "=r"(p[11]), "=r"(p[12]),
+                  "=r"(p[13]), "=r"(p[14]), "=r"(p[15])
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
             tc_fence_before();
@@ -539,44 +393,67 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             const int64_t lrow = (t - a.tile0[i]) * kTileM + quarter * 32 + lane;
             const bool valid = lrow < a.rows[i];
             const int64_t g = a.g0[i] + lrow;
-            if (S == 1) {
+            const bool first = u == u0 || s == 0;      // this CTA's first unit of tile t
+            const bool last = u == u1 - 1 || s == S - 1;  // ... and its last
+            if (first) prefix = s == 0;
+            if (prefix) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) r[b] = first ? __uint_as_float(p[b]) : r[b] + __uint_as_float(p[b]);
+            } else if (valid) {
+#pragma unroll
+                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * B + b) * a.n_total + g] = __uint_as_float(p[b]);
+            }
+            if (!last) continue;
+            if (prefix && s == S - 1) {  // the whole tile in this CTA: p_0 + ... + p_{S-1} + bias
                 if (valid) {
                     const float bb = a.bias ? a.bias[g] : 0.f;
 #pragma unroll
-                    for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = __uint_as_float(r[b]) + bb;
+                    for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = r[b] + bb;
                 }
                 continue;
             }
-            if (valid) {
+            if (prefix && valid) {  // the prefix sum p_0 + ... + p_s, stored at slice index s
 #pragma unroll
-                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * a.n_total + g) * B + b] = __uint_as_float(r[b]);
+                for (int b = 0; b < B; ++b) a.ws[((int64_t)s * B + b) * a.n_total + g] = r[b];
             }
-            __threadfence();
+            // count in (the CUTLASS semaphore pattern): the four warps' partial stores are ordered before
+            // one thread's gpu-scope acq_rel atomic by the barrier; the last contributor's acquire and
+            // the second barrier order its warps' partial loads after every contributor's stores
             named_barrier(1, 128);
-            if (et == 0) *last_flag = (atomicAdd(&a.counters[t], 1) == S - 1);
+            const int64_t cf = cta_of(t * S, U, G), cl = cta_of(t * S + S - 1, U, G);
+            if (et == 0) {
+                int old;
+                asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + t) : "memory");
+                *last_flag = old == (int)(cl - cf);
+            }
             named_barrier(1, 128);
-            if (*last_flag) {
-                __threadfence();
+            if (*last_flag) {  // every contributor is in: prefix + the remaining partials, in slice order
                 if (valid) {
-                    const float bb = a.bias ? a.bias[g] : 0.f;
-                    // partials are [slice][row][b]: each round loads 4 slices x B values (all independent)
-                    // and adds them per b in slice order -- the same order as the one-buffer kernel
+                    const int64_t ce = (cf + 1) * U / G;
+                    const int pe = (int)((ce < t * S + S ? ce : t * S + S) - t * S);  // prefix = slices [0, pe)
                     float sum[B];
 #pragma unroll
-                    for (int b = 0; b < B; ++b) sum[b] = 0.f;
-                    for (int q0 = 0; q0 < S; q0 += 4) {
-                        float part[4][B];
+                    for (int b = 0; b < B; ++b) sum[b] = __ldcg(&a.ws[((int64_t)(pe - 1) * B + b) * a.n_total + g]);
+                    // kFold slices x B loads issued unconditionally (indices clamped to the last slice, which
+                    // is always written), then added in slice order: no load waits behind a branch
+                    constexpr int kFold = B <= 4 ? 8 : 4;
+                    for (int q0 = pe; q0 < S; q0 += kFold) {
+                        float part[kFold][B];
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < kFold; ++q) {
+                            const int sq = q0 + q < S ? q0 + q : S - 1;
+                            const float *src = &a.ws[(int64_t)sq * B * a.n_total + g];
 #pragma unroll
-                            for (int b = 0; b < B; ++b)
-                                if (q0 + q < S) part[q][b] = __ldcg(&a.ws[((int64_t)(q0 + q) * a.n_total + g) * B + b]);
+                            for (int b = 0; b < B; ++b) part[q][b] = __ldcg(src + (int64_t)b * a.n_total);
+                        }
 #pragma unroll
-                        for (int q = 0; q < 4; ++q)
+                        for (int q = 0; q < kFold; ++q)
+                            if (q0 + q < S) {
 #pragma unroll
-                            for (int b = 0; b < B; ++b)
-                                if (q0 + q < S) sum[b] += part[q][b];
+                                for (int b = 0; b < B; ++b) sum[b] += part[q][b];
+                            }
                     }
+                    const float bb = a.bias ? a.bias[g] : 0.f;
 #pragma unroll
                     for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = sum[b] + bb;
                 }
@@ -585,13 +462,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
             named_barrier(1, 128);
         }
     }
-    if (a.stamps && warp == 2 && lane == 0) a.stamps[blockIdx.x * 4 + 2] = gtimer();
+    if (a.stamps && warp == 2 && lane == 0) a.stamps[blockIdx.x * 8 + 5] = gtimer();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (warp == 1)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
-    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 3] = gtimer();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kNAcc * kUmmaN)
+                     : "memory");
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 8 + 6] = gtimer();
 }
 
 // ---------------------------------------------------------------- host side
@@ -629,26 +507,10 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, uin
 int g_num_sms = 0;
 
 template <int B>
-int launch_tc_b(const void *x, int64_t K, const void *W, int64_t n, const float *bias, float *y,
-                int64_t ldy, float *ws, int *counters, cudaStream_t st) {
-    CUtensorMap mw, mx;
-    if (!make_map(&mw, W, K, n, kTileK, kTileM) || !make_map(&mx, x, K, B, kTileK, kUmmaN))
-        return (int)cudaErrorInvalidValue;
-    const GemvGeom g = gemv_tc_geom(K);
-    Units U{(n + kTileM - 1) / kTileM, g.s, g.ks};
-    const int64_t units = U.n_tiles * U.S;
-    // two CTAs per SM (2 x 112 KB smem): one streams while the other drains its epilogue
-    int grid = 2 * (g_num_sms > 0 ? g_num_sms : 148);
-    if (units < grid) grid = (int)units;
-    gemv_tc_kernel<B><<<grid, kThreads, kSmemBytes, st>>>(mw, mx, K, n, bias, y, ldy, U, ws, counters);
-    return (int)cudaGetLastError();
-}
-
-template <int B>
-int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
+int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
-    int grid = 2 * sms;
-    if (units < grid) grid = (int)units;
+    int grid = 2 * sms;  // two 6-stage CTAs per SM (2 x ~112 KB smem)
+    if (a.U < grid) grid = (int)a.U;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
@@ -666,22 +528,21 @@ int launch_tc_stream_b(const TcArgs &a, int64_t units, cudaStream_t st) {
 
 template <int B>
 int prepare_tc_b() {
-    int e = (int)cudaFuncSetAttribute(gemv_tc_kernel<B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)kSmemBytes);
-    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
-    return e;
+    return (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
 }
 
 }  // namespace
 
-int64_t g_slice_max = kSliceMaxTc;  // A/B (HG_TC_SLICE): max k per work unit, multiple of kTileK
+int64_t g_slice_min = kSliceMin;       // A/B (HG_TC_SLICE_MIN): smallest k per work unit
+int g_slice_count = kSliceMaxCount;    // A/B (HG_TC_SLICE_COUNT): most slices per row
 
+// k-slice geometry: a function of K only (split invariance): slices of ks = 64 * max(min/64,
+// ceil(K / (64 * count))) k, the last one shorter.
 GemvGeom gemv_tc_geom(int64_t K) {
     GemvGeom g;
-    const int64_t s0 = (K + g_slice_max - 1) / g_slice_max;
-    int64_t ks = (K + s0 - 1) / s0;
-    ks = (ks + kTileK - 1) / kTileK * kTileK;
+    int64_t ks = (K + (int64_t)kTileK * g_slice_count - 1) / ((int64_t)kTileK * g_slice_count) * kTileK;
+    if (ks < g_slice_min) ks = g_slice_min;
     g.ks = ks;
     g.s = (int)((K + ks - 1) / ks);
     g.rows_per_cta = kTileM;
@@ -692,9 +553,13 @@ int gemv_tc_prepare() {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    if (const char *v = getenv("HG_TC_SLICE")) {
+    if (const char *v = getenv("HG_TC_SLICE_MIN")) {
         const int64_t sl = atoll(v) / kTileK * kTileK;
-        if (sl >= kTileK) g_slice_max = sl;
+        if (sl >= kTileK) g_slice_min = sl;
+    }
+    if (const char *v = getenv("HG_TC_SLICE_COUNT")) {
+        const int c = atoi(v);
+        if (c >= 1 && c <= 256) g_slice_count = c;
     }
     int e = 0;
     e |= prepare_tc_b<1>();
@@ -707,23 +572,6 @@ int gemv_tc_prepare() {
     e |= prepare_tc_b<8>();
     if (!encode_fn()) e |= 1;
     return e;
-}
-
-int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
-                   float *y, int64_t ldy, float *ws, int *counters, void *stream) {
-    if (n <= 0) return 0;
-    cudaStream_t st = (cudaStream_t)stream;
-    switch (batch) {
-        case 1: return launch_tc_b<1>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 2: return launch_tc_b<2>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 3: return launch_tc_b<3>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 4: return launch_tc_b<4>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 5: return launch_tc_b<5>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 6: return launch_tc_b<6>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 7: return launch_tc_b<7>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        case 8: return launch_tc_b<8>(x, K, W, n, bias, y, ldy, ws, counters, st);
-        default: return (int)cudaErrorInvalidValue;
-    }
 }
 
 bool gemv_tc_stream_ok(int64_t n_res, int64_t n_chunks) {
@@ -782,6 +630,7 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.S = g.s;
     a.ks = g.ks;
     a.K = K;
+    a.U = a.tile0[ns] * a.S;
     a.n_total = L.n_res + L.n_str;
     a.bias = L.bias;
     a.y = L.y;
@@ -796,18 +645,36 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.stamps = gemv_stamps_dev();
     if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
-    const int64_t units = a.tile0[ns] * a.S;
     cudaStream_t st = (cudaStream_t)stream;
     switch (B) {
-        case 1: return launch_tc_stream_b<1>(a, units, st);
-        case 2: return launch_tc_stream_b<2>(a, units, st);
-        case 3: return launch_tc_stream_b<3>(a, units, st);
-        case 4: return launch_tc_stream_b<4>(a, units, st);
-        case 5: return launch_tc_stream_b<5>(a, units, st);
-        case 6: return launch_tc_stream_b<6>(a, units, st);
-        case 7: return launch_tc_stream_b<7>(a, units, st);
-        default: return launch_tc_stream_b<8>(a, units, st);
+        case 1: return launch_tc_stream_b<1>(a, st);
+        case 2: return launch_tc_stream_b<2>(a, st);
+        case 3: return launch_tc_stream_b<3>(a, st);
+        case 4: return launch_tc_stream_b<4>(a, st);
+        case 5: return launch_tc_stream_b<5>(a, st);
+        case 6: return launch_tc_stream_b<6>(a, st);
+        case 7: return launch_tc_stream_b<7>(a, st);
+        default: return launch_tc_stream_b<8>(a, st);
     }
+}
+
+// One buffer (the resident GEMV alone, hg_gemv, and the per-chunk fallback): the same kernel with a
+// single source, so its rows get the same bits as in any persistent launch.
+int launch_gemv_tc(const void *x, int batch, int64_t K, const void *W, int64_t n, const float *bias,
+                   float *y, int64_t ldy, float *ws, int *counters, void *stream) {
+    if (n <= 0) return 0;
+    StreamLaunch L{};
+    L.x = x;
+    L.batch = batch;
+    L.K = K;
+    L.W_res = W;
+    L.n_res = n;
+    L.bias = bias;
+    L.y = y;
+    L.ldy = ldy;
+    L.ws = ws;
+    L.timeout_s = 60.0;
+    return launch_gemv_tc_stream(L, counters, stream);
 }
 
 }  // namespace hg

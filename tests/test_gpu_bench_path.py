@@ -99,8 +99,7 @@ def test_bench_path_opt30b_stack(weights, B):
                 assert chk(T["a"], oracle.layernorm(tr["h_in"]))[0]
                 assert chk(T["h1"], oracle.residual(tr["h_in"], T["y_o"]))[0]
         # the bench's parity leg on this trace agrees
-        _, parity = bench.cpu_baseline_and_parity(st, {**tr, "layers": {l: tr["layers"][l] for l in (0, 47)}},
-                                                  reps=1)
+        _, parity = bench.cpu_baseline_and_parity(st, {**tr, "layers": {l: tr["layers"][l] for l in (0, 47)}})
         assert parity["ok"], parity
     finally:
         ctx.close()
