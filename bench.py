@@ -41,6 +41,8 @@ NAMES = ("qkv", "o", "fc1", "fc2")
 STACK_BYTES = LAYERS * sum(2 * n * k for n, k in SHAPES.values())  # 59,190,018,048
 METRIC = "ms/token offloaded OPT-30B decode linears; HBM & H2D GB/s vs roofline"
 SEED = 1164 + 3  # base seed + config index (BJ:10 is configs[3])
+# hg_strategy: Fig. 5c hybrid (default), 5a naive, 5b pinned-blocking (pageable weights only)
+STRATEGIES = {"hybrid": 0, "naive": 1, "blocking": 2}
 
 
 def set_model(name):
@@ -304,11 +306,32 @@ def pct(sorted_vals, q):
     return sorted_vals[i] + (sorted_vals[j] - sorted_vals[i]) * (x - i)
 
 
-def make_context(args, rank, world, local, **extra):
-    """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores."""
+def placement(args, world, local):
+    """Host placement of this rank: (NUMA node of its GPU or -1, its share of cores, index
+    of its first core in the node's cpulist or -1).  Ranks whose GPUs hang off the same node split that
+    node's cores; with one rank (or --numa off, or no sysfs) the pool is not pinned."""
     from paper_2403_01164_b200 import hg
     ncores = os.cpu_count() or 1
-    per = max(1, ncores // world)
+    if args.numa == "off":
+        return -1, max(1, ncores // world), (local * max(1, ncores // world)) if world > 1 else -1
+    try:
+        nodes = [hg.hg_numa_node(d) for d in range(world)]
+        node = nodes[local]
+        cpus = hg.hg_numa_cpus(node) if node >= 0 else []
+    except Exception:  # noqa: BLE001
+        node, cpus, nodes = -1, [], []
+    if node < 0 or not cpus:
+        return -1, max(1, ncores // world), (local * max(1, ncores // world)) if world > 1 else -1
+    same = [d for d in range(world) if nodes[d] == node]
+    per = max(1, len(cpus) // len(same))
+    return node, per, (same.index(local) * per) if world > 1 else -1
+
+
+def make_context(args, rank, world, local, **extra):
+    """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores (those
+    of its GPU's NUMA node when known)."""
+    from paper_2403_01164_b200 import hg
+    node, per, first = placement(args, world, local)
     pin_threads = 4 if args.pageable else 0  # the pin lane's memcpy threads get their own cores
     # leave cores for the API thread (it enqueues the GPU lanes and joins the CPU rows) and the CUDA
     # driver's threads: with all 16 cores of the GPU box in the pool, a preempted worker stalls the
@@ -316,19 +339,24 @@ def make_context(args, rank, world, local, **extra):
     # the slow runs with the link at ~46 GB/s -- profiles/r01/threads.md)
     reserve = 2 if per >= 12 else (1 if per >= 4 else 0)
     threads = args.threads or max(1, per - pin_threads - reserve)
-    cfg = dict(cpu_threads=threads, cpu_first=(rank * per) if world > 1 else -1,
+    cfg = dict(cpu_threads=threads, cpu_first=first, numa_node=node if first >= 0 else -1,
                chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
                max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
-               pageable=int(args.pageable), pin_threads=max(1, pin_threads))
+               pageable=int(args.pageable), pin_threads=max(1, pin_threads),
+               strategy=STRATEGIES[args.strategy], staging_bytes=args.staging_mb << 20)
     cfg.update(extra)
     return hg.Context(local, **cfg), threads
 
 
 def make_weights(args, rank, world):
-    """This rank's row shard of every linear: W in host memory (pinned unless --pageable), bias on
-    the device and its host copy (the CPU lane adds its rows' bias in the mirrored glue)."""
+    """This rank's row shard of every linear: W in host memory (pinned unless --pageable; bound to the
+    GPU's NUMA node before first touch, hg_host_alloc), bias on the device and its host copy (the CPU
+    lane adds its rows' bias in the mirrored glue)."""
     import torch
     from harness import gen
+    from paper_2403_01164_b200 import hg
+    local = env_rank()[2]
+    node = placement(args, world, local)[0] if torch.cuda.is_available() else -1
     t_setup = time.perf_counter()
     host, biases, biases_h = [], [], []
     for l in range(args.layers):
@@ -336,7 +364,10 @@ def make_weights(args, rank, world):
         for name in NAMES:
             N, K = SHAPES[name]
             r0, r1 = rank * N // world, (rank + 1) * N // world
-            Wt = torch.empty((r1 - r0, K), dtype=torch.int16, pin_memory=not args.pageable)
+            if args.pageable:
+                Wt = torch.empty((r1 - r0, K), dtype=torch.int16)
+            else:
+                Wt = hg.HostBuffer((r1 - r0, K), torch.int16, node=node, lock=True).tensor
             gen.uniform_bf16(SEED, gen.tensor_id(l, name, "W"), (r1 - r0) * K, gen.w_scale(K),
                              offset=r0 * K, out=Wt.data_ptr())
             b = gen.bf16_bits_to_f32(gen.uniform_bf16(SEED, gen.tensor_id(l, name, "bias"), r1 - r0,
@@ -386,6 +417,7 @@ def prepare(args, weights=None, **ctx_extra):
     return {"torch": torch, "dist": dist, "hg": hg, "rank": rank, "world": world, "local": local,
             "threads": threads, "ctx": ctx, "B": B, "host": host, "biases": biases, "biases_h": biases_h,
             "rates": rates, "t_setup": t_setup, "h_host": h_host, "h_dev": h_host.cuda(),
+            "placement": placement(args, world, local),
             "h_out": torch.empty_like(h_host, pin_memory=True), "stream": torch.cuda.Stream(), "v_kind": None}
 
 
@@ -582,7 +614,8 @@ def run_point(st, args, budget_gb=0.0):
     if args.breakdown and world == 1:
         sctx = hg.Context(local, cpu_threads=st["threads"], cpu_first=-1, chunk_bytes=args.chunk_mb << 20,
                           ring_bytes=args.ring_mb << 20, max_k=F, max_n=F, wrap_prefetch=1, collect_stats=1,
-                          pageable=int(args.pageable), pin_threads=4)
+                          pageable=int(args.pageable), pin_threads=4, strategy=STRATEGIES[args.strategy],
+                          staging_bytes=args.staging_mb << 20)
         sctx.hg_stack(layers, h_dev, B, stream=s)  # fill the prefetch pipeline
         sctx.hg_reset_stats()
         for _ in range(2):
@@ -671,11 +704,17 @@ def run_point(st, args, budget_gb=0.0):
                    "alpha_mode": "fixed" if args.alpha is not None else (
                        ("Eq9" if args.pageable else "Eq5") + (" (measured rates) refined by the alpha benchmark "
                                                               "(Sec. 4.4)" if abench else " (measured rates)")),
-                   "host_weights": "pageable, pin lane (Sec. 4.3)" if args.pageable else "pinned once at load",
+                   "host_weights": ("pageable, strategy %s (Fig. 5%s)" % (args.strategy, {"hybrid": "c, pin lane of "
+                                    "Sec. 4.3", "naive": "a", "blocking": "b"}[args.strategy])) if args.pageable
+                   else "pinned once at load",
                    "alpha": next((p.alpha_eff for p in all_plans if p.n_res < p.N), 0.0),
                    "alpha_seed_eq5": alpha_seed,
                    "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
                    "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": st["threads"],
+                   "numa": {"node": st["placement"][0], "cores_per_rank": st["placement"][1],
+                            "pool_pinned_from": st["placement"][2],
+                            "weights": "hg_host_alloc, bound to the node" if st["placement"][0] >= 0
+                            else "hg_host_alloc (no NUMA node reported)"},
                    "l2": "inputs larger than L2: %.1f GB of weights streamed/computed per step" % (shard_bytes / 1e9)},
         "gpu_launches": int(launches),
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms/token", "h2d_bytes_per_step": B * H * 2,
@@ -851,10 +890,18 @@ def parse_args(argv=None):
     ap.add_argument("--abench-gamma", type=float, default=0.06)
     ap.add_argument("--pageable", action="store_true",
                     help="NEXT(1): host weights not page-locked; streamed chunks go through the pin lane")
+    ap.add_argument("--strategy", default="hybrid", choices=sorted(STRATEGIES),
+                    help="with --pageable: how streamed rows reach the device (Fig. 5c hybrid, 5a naive, "
+                         "5b pinned-blocking)")
+    ap.add_argument("--staging-mb", type=int, default=512,
+                    help="with --pageable: the pin lane's pinned staging ring (MiB)")
     ap.add_argument("--resident", type=float, default=0.0,
                     help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
+    ap.add_argument("--numa", default="auto", choices=["auto", "off"],
+                    help="host placement: weights bound to the GPU's NUMA node; with N > 1 each rank's CPU "
+                         "lane pinned to its share of that node's cores")
     ap.add_argument("--ref-layers", type=int, default=2,
                     help="--impl reference: OPT layers per step through the oracle (a bounded sample of the token)")
     ap.add_argument("--no-parity", dest="parity", action="store_false",

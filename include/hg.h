@@ -65,7 +65,7 @@ extern "C" {
 #endif
 
 #define HG_MAX_BATCH 8
-#define HG_ABI_VERSION 2
+#define HG_ABI_VERSION 3
 
 typedef enum {
     HG_OK = 0,
@@ -125,6 +125,12 @@ typedef struct {
     double t_roof;               /* max(t_hbm, 2K n_str / b_link, 2K n_cpu / b_cpu)        */
 } hg_plan_t;
 
+typedef enum {
+    HG_STRATEGY_HYBRID = 0,          /* Fig. 5c: pin || transfer || CPU compute         */
+    HG_STRATEGY_NAIVE = 1,           /* Fig. 5a: async transfer from un-pinned memory   */
+    HG_STRATEGY_PINNED_BLOCKING = 2  /* Fig. 5b: pin first, blocking CPU and transfer   */
+} hg_strategy;
+
 typedef struct {
     int64_t granule;     /* G (default 128; tests use 1)                                 */
     int64_t chunk_bytes; /* streamed chunk target (default 16 MiB)                       */
@@ -159,8 +165,21 @@ typedef struct {
                             weights go through the pin lane -- the asynchronous parameter manager of
                             Sec. 4.3 -- into a pinned staging ring; 0 (default): HG_ENOTPINNED     */
     int32_t pin_threads; /* memcpy threads of the pin lane (default 4)                           */
-    int32_t _pad1;
+    int32_t strategy;    /* how a pageable weight's streamed rows reach the device (Fig. 5, P:225-227;
+                            pinned weights are unaffected): HG_STRATEGY_HYBRID (default, Fig. 5c):
+                            the pin lane pins ahead across linears while the link and the CPU lane
+                            run; HG_STRATEGY_NAIVE (Fig. 5a): no pin lane, a transfer thread copies
+                            straight from the pageable rows (the driver stages them) beside the CPU
+                            lane, within the current linear; HG_STRATEGY_PINNED_BLOCKING (Fig. 5b):
+                            the linear's streamed rows are pinned first on the CPU lane's own threads
+                            -- blocking the CPU lane and the transfer -- then transferred beside the
+                            CPU lane's compute.  Results are bit-identical across strategies.        */
     int64_t staging_bytes; /* pinned staging ring of the pin lane (default 512 MiB, >= 2 slots)  */
+    int32_t numa_node;   /* host placement: -1 (default) = none; -2 = the NUMA node of
+                            `device`'s PCI slot (sysfs); >= 0 = that node.  With a node the CPU lane's
+                            pool threads are pinned to the node's cores starting at index cpu_first of
+                            the node's cpulist (cpu_first < 0: 0), so ranks sharing a node split it   */
+    int32_t _pad2;
 } hg_config;
 
 /* Lane breakdown of the hg_linear / hg_layer / hg_stack calls since the last
@@ -419,6 +438,21 @@ HG_API hg_status hg_gather_permute(hg_ctx *ctx, const float *gathered, int nrank
 HG_API hg_status hg_linear_sharded(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
                                    const void *W_dev, const void *W_host, const float *bias_dev,
                                    float *y_full_dev, void *stream);
+
+/* ---------------------------------------------------------------- host placement */
+/* The NUMA node of CUDA device `device`'s PCI slot (sysfs numa_node), -1 when unknown. */
+HG_API hg_status hg_numa_node(int device, int *node);
+/* The cores of NUMA node `node` (sysfs cpulist), ascending: up to `max` into cpus, the count into *n.
+ * HG_EINVAL for a node with no cpulist. */
+HG_API hg_status hg_numa_cpus(int node, int *cpus, int max, int *n);
+/* Host memory for a rank's offloaded weights: `bytes` of anonymous memory whose pages are bound to
+ * NUMA node `node` (node < 0: not bound) before they are first touched, then page-locked and mapped
+ * for the device (lock = 1; needs a CUDA device) or zero-filled (lock = 0).  The caller frees it with
+ * hg_host_free(ptr, bytes, lock).  HG_ENOMEM on failure. */
+HG_API hg_status hg_host_alloc(size_t bytes, int node, int lock, void **ptr);
+HG_API hg_status hg_host_free(void *ptr, size_t bytes, int lock);
+/* The NUMA node the page holding `ptr` lives on (-1 unknown). */
+HG_API hg_status hg_numa_node_of_ptr(const void *ptr, int *node);
 
 /* ---------------------------------------------------------------- stats */
 HG_API hg_status hg_stats(hg_ctx *ctx, hg_stats_t *out);

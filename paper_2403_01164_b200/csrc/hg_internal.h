@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdint>
+#include <vector>
 
 #include "hg.h"
 
@@ -132,6 +133,16 @@ double pinlane_copy_timed(PinLane *p, void *dst, const void *src, int64_t bytes)
 // ---------------------------------------------------------------- threadpool.cpp
 class ThreadPool;
 ThreadPool *pool_create(int nthreads, int first_core);
+// workers pinned to cpus[i % cpus.size()] (worker 0 is the caller's thread and is not pinned)
+ThreadPool *pool_create_cpus(int nthreads, const std::vector<int> &cpus);
+
+// numa.cpp: host placement of a rank
+std::vector<int> parse_cpulist(const char *s);
+int numa_node_of_device(int device);
+std::vector<int> numa_cpus(int node);
+void *host_alloc_node(size_t bytes, int node, bool lock);
+void host_free_node(void *p, size_t bytes, bool locked);
+int numa_node_of_page(const void *p);
 void pool_destroy(ThreadPool *p);
 int pool_size(const ThreadPool *p);
 // Run fn(arg, worker_index) on every worker (the caller is worker 0); returns when all finished.

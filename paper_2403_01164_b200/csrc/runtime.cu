@@ -25,7 +25,10 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <deque>
+#include <mutex>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -113,6 +116,114 @@ void host_job_run(void *a, int) {
     }
 }
 
+// Fig. 5a transfer thread (hg_config.strategy = HG_STRATEGY_NAIVE): chunks of a pageable weight are
+// copied straight from the un-pinned rows with cudaMemcpyAsync -- the driver stages them through its
+// own pinned buffer and the call returns only when the source is consumed -- so the copies run on this
+// thread and its own stream, beside the CPU lane.  Per chunk, in order on the stream: wait until the
+// ring slot's previous occupant was consumed, copy, write the slot's arrival tag.
+struct NaiveLane {
+    struct Job {
+        const uint32_t *consumed;
+        uint32_t wait_val;  // 0: no wait
+        uint32_t *arrived;
+        uint32_t arrived_val;
+        void *dst;
+        const void *src;
+        int64_t bytes;
+    };
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv, idle;
+    std::deque<Job> q;
+    int busy = 0;
+    bool stop = false;
+    std::atomic<int> err{0};
+    std::atomic<int64_t> busy_ns{0}, bytes{0};  // host time inside the staged copies (the link time)
+
+    void loop() {
+        cudaSetDevice(device);
+        for (;;) {
+            Job j;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stop || !q.empty(); });
+                if (q.empty()) return;
+                j = q.front();
+                q.pop_front();
+                ++busy;
+            }
+            if (!err) {
+                int e = 0;
+                if (j.wait_val) e = g_wait_value((void *)st, (unsigned long long)(uintptr_t)j.consumed, j.wait_val, kWaitGeq);
+                const auto t0 = std::chrono::steady_clock::now();
+                if (!e && cudaMemcpyAsync(j.dst, j.src, (size_t)j.bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) e = 1;
+                busy_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count();
+                bytes += j.bytes;
+                if (!e) e = g_write_value((void *)st, (unsigned long long)(uintptr_t)j.arrived, j.arrived_val, kWriteDefault);
+                if (e) err = 1;
+            }
+            {
+                std::lock_guard<std::mutex> lk(mu);
+                --busy;
+            }
+            idle.notify_all();
+        }
+    }
+    void submit(const Job &j) {
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            q.push_back(j);
+        }
+        cv.notify_one();
+    }
+    void drain() {  // every submitted copy has been enqueued on the stream
+        std::unique_lock<std::mutex> lk(mu);
+        idle.wait(lk, [&] { return q.empty() && busy == 0; });
+    }
+};
+
+NaiveLane *naive_create(int device) {
+    NaiveLane *n = new NaiveLane;
+    n->device = device;
+    if (cudaStreamCreateWithFlags(&n->st, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaGetLastError();
+        delete n;
+        return nullptr;
+    }
+    n->th = std::thread([n] { n->loop(); });
+    return n;
+}
+
+void naive_destroy(NaiveLane *n) {
+    if (!n) return;
+    {
+        std::lock_guard<std::mutex> lk(n->mu);
+        n->stop = true;
+    }
+    n->cv.notify_all();
+    n->th.join();
+    cudaStreamSynchronize(n->st);
+    cudaStreamDestroy(n->st);
+    delete n;
+}
+
+// Parallel memcpy on a thread pool (Fig. 5b's blocking pin runs on the CPU lane's own threads).
+struct PoolCopy {
+    uint8_t *dst;
+    const uint8_t *src;
+    int64_t bytes;
+    int parts;
+};
+void pool_copy_part(void *a, int w) {
+    const PoolCopy *pc = (const PoolCopy *)a;
+    const int64_t per = (pc->bytes / pc->parts + 63) / 64 * 64;
+    const int64_t off = (int64_t)w * per;
+    if (off < pc->bytes) std::memcpy(pc->dst + off, pc->src + off, (size_t)std::min(per, pc->bytes - off));
+    _mm_sfence();
+}
+
 }  // namespace
 }  // namespace hg
 struct hg_ctx;
@@ -188,6 +299,7 @@ struct hg_ctx {
     cudaStream_t d2h = nullptr;                    // side stream for the GPU rows' D2H
     // pin lane (pageable weights, Sec. 4.3): pinned staging ring + mapped tag words
     PinLane *pin = nullptr;
+    NaiveLane *naive = nullptr;  // strategy NAIVE: transfer thread + stream for pageable chunks
     uint8_t *staging = nullptr;
     int nstage = 0;
     uint32_t *pinflags = nullptr;       // mapped host: pinned[nstage], freed[nstage]
@@ -388,6 +500,29 @@ hg_status ensure_pinlane(hg_ctx *c) {
 hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
     const int64_t seq = c->next_seq;
     const int slot = (int)(seq % c->nslots);
+    const bool pageable = c->cfg.pageable && is_pageable(r.src);
+    if (pageable && c->cfg.strategy == HG_STRATEGY_NAIVE) {
+        // Fig. 5a: the transfer thread copies straight from the pageable rows on its own stream; the
+        // slot-reuse wait and the arrival tag travel with the copy, in order on that stream
+        if (!c->tags) return set_error(HG_EUNSUPPORTED, "pageable weights need the device-tag pipeline");
+        if (!c->naive && !(c->naive = naive_create(c->device))) {
+            c->error = true;
+            return set_error(HG_ECUDA, "cannot create the naive-strategy transfer thread");
+        }
+        NaiveLane::Job j;
+        j.consumed = c->consumed + slot;
+        j.wait_val = seq >= c->nslots ? (uint32_t)(seq - c->nslots + 1) : 0u;
+        j.arrived = c->arrived + slot;
+        j.arrived_val = (uint32_t)(seq + 1);
+        j.dst = c->ring + (int64_t)slot * c->slot_bytes;
+        j.src = r.src;
+        j.bytes = r.bytes;
+        c->naive->submit(j);
+        c->slot_used[slot] = 1;
+        if (!bound) c->inflight.push_back({r, slot, seq});
+        ++c->next_seq;
+        return HG_OK;
+    }
     if (c->tags) {
         // The slot's previous occupant (seq - nslots) must have been drained by its GEMV.  ev_free
         // follows that GEMV (or the drop): when the host already sees it complete, the device-side
@@ -412,15 +547,38 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
     const void *src = r.src;
     int pslot = -1;
     uint32_t ptag = 0;
-    if (c->cfg.pageable && is_pageable(r.src)) {  // pin lane: pageable chunk -> pinned staging slot
+    if (pageable) {  // pageable chunk -> pinned staging slot
         if (!c->tags) return set_error(HG_EUNSUPPORTED, "pageable weights need the device-tag pipeline");
         HG_TRY(ensure_pinlane(c));
         const int64_t ps = c->pin_seq++;
         pslot = (int)(ps % c->nstage);
         ptag = (uint32_t)(ps + 1);
-        pinlane_submit(c->pin, r.src, r.bytes, pslot, ptag);
-        HG_TRY(memop(c, g_wait_value, c->copy, c->pinflags_dev + pslot, ptag, kWaitGeq));
         src = c->staging + (int64_t)pslot * c->slot_bytes;
+        if (c->cfg.strategy == HG_STRATEGY_PINNED_BLOCKING) {
+            // Fig. 5b: pin now, on the CPU lane's own threads, before anything else of this linear runs
+            // (the caller posts the CPU rows only after the linear's chunks are issued); the staging
+            // slot's previous DMA must have left it (freed tag, written by the copy stream)
+            if (ps >= c->nstage) {
+                const uint32_t need = (uint32_t)(ps - c->nstage + 1);
+                const auto t0 = clk::now();
+                for (int spin = 0; (int32_t)(((volatile uint32_t *)c->pinflags)[c->nstage + pslot] - need) < 0; ++spin) {
+                    _mm_pause();
+                    if ((spin & 4095) == 4095 && secs(t0, clk::now()) > c->cfg.timeout_s) {
+                        c->error = true;
+                        return set_error(HG_ETIMEOUT, "pinned-blocking: staging slot not freed within %.1f s",
+                                         c->cfg.timeout_s);
+                    }
+                }
+            }
+            const auto t1 = clk::now();
+            PoolCopy pc{(uint8_t *)src, (const uint8_t *)r.src, r.bytes, pool_size(c->pool)};
+            pool_run(c->pool, pool_copy_part, &pc);
+            c->st.pin_busy_s += secs(t1, clk::now());
+            c->st.bytes_pinned += r.bytes;
+        } else {  // Fig. 5c: the pin lane pins ahead; the copy stream waits for the slot's pinned tag
+            pinlane_submit(c->pin, r.src, r.bytes, pslot, ptag);
+            HG_TRY(memop(c, g_wait_value, c->copy, c->pinflags_dev + pslot, ptag, kWaitGeq));
+        }
     }
     HG_CK(c, cudaMemcpyAsync(c->ring + (int64_t)slot * c->slot_bytes, src, (size_t)r.bytes,
                              cudaMemcpyHostToDevice, c->copy));
@@ -473,6 +631,9 @@ hg_status pump(hg_ctx *c) {
         HG_TRY(issue_copy(c, r, true));
         --c->prebound;
     }
+    // speculative run-ahead into later linears: the hybrid strategy's "pin the next weight";
+    // the naive and pinned-blocking strategies (Fig. 5a/5b) move a linear's rows only while it runs
+    if (c->cfg.pageable && c->cfg.strategy != HG_STRATEGY_HYBRID) return HG_OK;
     while ((int)c->inflight.size() < c->nslots && future_next(c, &r)) HG_TRY(issue_copy(c, r));
     return HG_OK;
 }
@@ -703,6 +864,8 @@ hg_status enqueue_gpu_lanes(hg_ctx *c, const Lin &L, cudaStream_t s) {
     return HG_OK;
 }
 
+bool blocking_pin(const hg_ctx *c) { return c->cfg.pageable && c->cfg.strategy == HG_STRATEGY_PINNED_BLOCKING; }
+
 hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
     const hg_plan_t &p = L.plan;
     const int B = (int)p.batch;
@@ -719,7 +882,9 @@ hg_status run_linear(hg_ctx *c, const Lin &L, cudaStream_t s) {
     {  // a5 + a3/a4: workers start on the CPU rows the moment x lands, while this thread
        // enqueues the GPU lanes behind the D2H and then joins the CPU rows itself
        // (HG_ASYNC_POST=0: enqueue the GPU lanes first, then compute -- A/B switch).
-        static const bool async_post = !getenv("HG_ASYNC_POST") || atoi(getenv("HG_ASYNC_POST")) != 0;
+        static const bool async_post_env = !getenv("HG_ASYNC_POST") || atoi(getenv("HG_ASYNC_POST")) != 0;
+        // pinned-blocking (Fig. 5b) pins the linear's streamed rows on the pool threads before the CPU rows
+        const bool async_post = async_post_env && !blocking_pin(c);
         hg_status gst = HG_OK;
         if (!async_post) HG_TRY(enqueue_gpu_lanes(c, L, s));
         HG_TRY(wait_event(c, c->ev_x, &c->st.x_wait_s));
@@ -830,6 +995,19 @@ hg_status check_async_errors(hg_ctx *c) {
         c->error = true;
         return set_error(HG_ETIMEOUT, "the pin lane waited longer than %.1f s for a staging slot", c->cfg.timeout_s);
     }
+    if (c->naive && c->naive->err) {
+        c->error = true;
+        return set_error(HG_ECUDA, "the naive-strategy transfer thread failed to enqueue a copy");
+    }
+    return HG_OK;
+}
+
+// Every copy the naive-strategy transfer thread was handed is enqueued on its stream, and that stream
+// has finished (synchronising points: stats, measurement, reallocation).
+hg_status sync_naive(hg_ctx *c) {
+    if (!c->naive) return HG_OK;
+    c->naive->drain();
+    HG_CK(c, cudaStreamSynchronize(c->naive->st));
     return HG_OK;
 }
 
@@ -860,6 +1038,7 @@ hg_status end_call(hg_ctx *c, cudaStream_t s) {
 hg_status ensure(hg_ctx *c, void **p, int64_t *have, int64_t need_bytes) {
     if (*have >= need_bytes) return HG_OK;
     if (*p) {
+        HG_TRY(sync_naive(c));
         HG_CK(c, cudaDeviceSynchronize());
         cudaFree(*p);
         *p = nullptr;
@@ -1124,6 +1303,33 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
         }
         HostJob job;
         auto t0 = clk::now();
+        // pinned-blocking (Fig. 5b): this linear's streamed rows are pinned on the pool threads first,
+        // so its GPU lanes are enqueued before the CPU rows are posted
+        const bool gpu_first = blocking_pin(c);
+        hg_status gst = HG_OK;
+        bool gpu_done = false;
+        auto gpu_lanes = [&]() {
+            Lin lin{p, c->act, d.W_dev, (const uint8_t *)d.W_host, d.bias, yd, N};
+            gst = enqueue_gpu_lanes(c, lin, s);
+            if (gst == HG_OK && n_gpu > 0) {
+                cudaError_t e = cudaEventRecord(c->ev_g[slot], s);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_g[slot], 0);
+                if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_use[slot], 0);
+                if (e == cudaSuccess)
+                    e = cudaMemcpy2DAsync(c->yhost[slot], (size_t)N * 4, yd, (size_t)N * 4, (size_t)n_gpu * 4,
+                                          (size_t)B, cudaMemcpyDeviceToHost, c->d2h);
+                if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H");
+            }
+            if (gst == HG_OK) {
+                cudaError_t e = cudaEventRecord(c->ev_yg[slot], c->d2h);
+                if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H event");
+            }
+            gpu_done = true;
+        };
+        if (gpu_first) {  // (the host is already past slot k - R: caught up above)
+            gpu_lanes();
+            if (gst != HG_OK) return gst;
+        }
         if (p.n_cpu > 0) {
             HG_TRY(catch_up(k));
             c->st.mirror_linears++;
@@ -1145,21 +1351,7 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             pool_post(c->pool, host_job_run, &job);
         }
         // ---- GPU rows into the ring slot, then (side stream) their copy to the host slot
-        Lin lin{p, c->act, d.W_dev, (const uint8_t *)d.W_host, d.bias, yd, N};
-        hg_status gst = enqueue_gpu_lanes(c, lin, s);
-        if (gst == HG_OK && n_gpu > 0) {
-            cudaError_t e = cudaEventRecord(c->ev_g[slot], s);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_g[slot], 0);
-            if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_use[slot], 0);
-            if (e == cudaSuccess)
-                e = cudaMemcpy2DAsync(c->yhost[slot], (size_t)N * 4, yd, (size_t)N * 4, (size_t)n_gpu * 4, (size_t)B,
-                                      cudaMemcpyDeviceToHost, c->d2h);
-            if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H");
-        }
-        if (gst == HG_OK) {
-            cudaError_t e = cudaEventRecord(c->ev_yg[slot], c->d2h);
-            if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H event");
-        }
+        if (!gpu_done) gpu_lanes();
         if (p.n_cpu > 0) {
             pool_join(c->pool);  // always: workers reference `job`
             c->st.cpu_busy_s += secs(t0, clk::now());
@@ -1242,6 +1434,7 @@ HG_API hg_status hg_config_default(hg_config *cfg) {
     cfg->pin_threads = 4;
     cfg->staging_bytes = 512ll << 20;
     cfg->verify_mirror = 0;
+    cfg->numa_node = -1;
     return HG_OK;
 }
 
@@ -1260,6 +1453,8 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     if (cfg.granule < 1 || cfg.chunk_bytes < 1 || cfg.max_k < 8 || cfg.max_n < 1 ||
         !(cfg.timeout_s > 0))
         return set_error(HG_EINVAL, "bad config");
+    if (cfg.strategy < HG_STRATEGY_HYBRID || cfg.strategy > HG_STRATEGY_PINNED_BLOCKING)
+        return set_error(HG_EINVAL, "bad strategy %d", cfg.strategy);
     if (cfg.pageable && cfg.stream_mode == 1)  // zero-copy reads need page-locked, mapped rows
         return set_error(HG_EINVAL, "pageable weights cannot be streamed zero-copy (stream_mode 1)");
     hg_ctx *c = new hg_ctx;
@@ -1270,7 +1465,16 @@ HG_API hg_status hg_create(hg_ctx **out, int device, const hg_config *cfg_in) {
     // every core in the pool a preempted worker stalls the lane now and then (profiles/r01/threads.md)
     const int ncpu = (int)sysconf(_SC_NPROCESSORS_ONLN);
     int nthr = cfg.cpu_threads > 0 ? cfg.cpu_threads : ncpu - (ncpu >= 12 ? 2 : ncpu >= 4 ? 1 : 0);
-    c->pool = pool_create(nthr, cfg.cpu_first);
+    // NUMA placement: pool threads on the cores of the GPU's node, from cpu_first on
+    const int node = cfg.numa_node == -2 ? (device >= 0 ? numa_node_of_device(device) : -1) : cfg.numa_node;
+    std::vector<int> cpus = numa_cpus(node);
+    if (!cpus.empty()) {
+        const size_t first = cfg.cpu_first > 0 ? (size_t)cfg.cpu_first % cpus.size() : 0;
+        std::rotate(cpus.begin(), cpus.begin() + first, cpus.end());
+        c->pool = pool_create_cpus(nthr, cpus);
+    } else {
+        c->pool = pool_create(nthr, cfg.cpu_first);
+    }
     c->host_fn = host_rows_select(nullptr);
     {
         const char *v = getenv("HG_AMX_MIN_BATCH");
@@ -1377,6 +1581,7 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
         }
         if (c->yring) cudaFree(c->yring);
         if (c->pin) pinlane_destroy(c->pin);
+        if (c->naive) naive_destroy(c->naive);
         if (c->staging) cudaFreeHost(c->staging);
         if (c->pinflags) cudaFreeHost(c->pinflags);
         if (c->d2h) cudaStreamDestroy(c->d2h);
@@ -1647,6 +1852,39 @@ HG_API hg_status hg_dist_init(hg_ctx *c, int nranks, int rank, const void *id128
     return st;
 }
 
+HG_API hg_status hg_numa_node(int device, int *node) {
+    if (!node) return set_error(HG_EINVAL, "NULL node");
+    *node = numa_node_of_device(device);
+    return HG_OK;
+}
+
+HG_API hg_status hg_numa_cpus(int node, int *cpus, int max, int *n) {
+    if (!n || (max > 0 && !cpus)) return set_error(HG_EINVAL, "NULL argument");
+    const std::vector<int> v = numa_cpus(node);
+    if (v.empty()) return set_error(HG_EINVAL, "NUMA node %d has no cpulist", node);
+    for (int i = 0; i < max && i < (int)v.size(); ++i) cpus[i] = v[(size_t)i];
+    *n = (int)v.size();
+    return HG_OK;
+}
+
+HG_API hg_status hg_host_alloc(size_t bytes, int node, int lock, void **ptr) {
+    if (!ptr || bytes == 0) return set_error(HG_EINVAL, "bad arguments");
+    *ptr = host_alloc_node(bytes, node, lock != 0);
+    if (!*ptr) return set_error(HG_ENOMEM, "host_alloc of %zu bytes on node %d failed", bytes, node);
+    return HG_OK;
+}
+
+HG_API hg_status hg_host_free(void *ptr, size_t bytes, int lock) {
+    host_free_node(ptr, bytes, lock != 0);
+    return HG_OK;
+}
+
+HG_API hg_status hg_numa_node_of_ptr(const void *ptr, int *node) {
+    if (!ptr || !node) return set_error(HG_EINVAL, "NULL argument");
+    *node = numa_node_of_page(ptr);
+    return HG_OK;
+}
+
 HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
     if (!c || !out) return set_error(HG_EINVAL, "NULL argument");
     if (c->device >= 0 && c->call_timed) {
@@ -1657,6 +1895,7 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
         HG_CK(c, cudaEventElapsedTime(&ms, c->ev_call0, c->ev_call1));
         c->st.wall_s = ms * 1e-3;
         if (c->cfg.collect_stats) {
+            HG_TRY(sync_naive(c));
             HG_CK(c, cudaStreamSynchronize(c->copy));
             // busy time inside the calls' window [ev_call0, ev_call1]: the copy stream also runs
             // ahead into chunks of later calls (prefetch), which belong to those calls
@@ -1686,11 +1925,13 @@ HG_API hg_status hg_stats(hg_ctx *c, hg_stats_t *out) {
             for (auto &pr : c->gemv_ev) gpu += clipped(pr);
             cudaGetLastError();
             c->st.link_busy_s = (bytes > 0 && dur > 0) ? (double)c->st.bytes_str / (bytes / dur) : 0.0;
+            if (c->naive && c->naive->bytes > 0)  // naive strategy: the transfer thread's staged-copy rate
+                c->st.link_busy_s = (double)c->st.bytes_str * (c->naive->busy_ns * 1e-9) / (double)c->naive->bytes;
             if (c->cfg.stream_mode == 1) c->st.link_busy_s = gpu;  // zero-copy: the GEMVs are the transfer
             c->st.gpu_busy_s = gpu;
         }
     }
-    if (c->pin) {
+    if (c->pin && c->cfg.strategy == HG_STRATEGY_HYBRID) {  // (pinned-blocking counts its pins as it does them)
         double busy = 0;
         int64_t pinned = 0;
         pinlane_stats(c->pin, &busy, &pinned, false);
@@ -1713,12 +1954,17 @@ HG_API hg_status hg_reset_stats(hg_ctx *c) {
         HG_CK(c, cudaSetDevice(c->device));
         if (cudaEventSynchronize(c->ev_done) != cudaSuccess) dbg_trace_report(c);
         HG_CK(c, cudaEventSynchronize(c->ev_done));
+        HG_TRY(sync_naive(c));
         HG_CK(c, cudaStreamSynchronize(c->copy));
     }
     if (c->pin) {
         double b;
         int64_t n;
         pinlane_stats(c->pin, &b, &n, true);
+    }
+    if (c->naive) {  // the lane's counters restart with the stats window
+        c->naive->busy_ns = 0;
+        c->naive->bytes = 0;
     }
     c->tev_used = 0;
     c->copy_ev.clear();
@@ -1804,6 +2050,7 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     HG_TRY(drop_inflight(c));
     c->future.clear();
     c->fpos = 0;
+    HG_TRY(sync_naive(c));
     HG_CK(c, cudaDeviceSynchronize());
     HG_TRY(check_device_error(c));
     std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
@@ -1816,10 +2063,13 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     float ms = 0;
     // pageable weight (hg_config.pageable): the link is probed from the pin lane's staging ring and
     // V_PIN is the lane's own rate (Eq. (9)); pinned weight: V_PIN = +inf (reading R7)
-    const bool pageable = c->cfg.pageable && is_pageable(W_host);
+    // (naive strategy, Fig. 5a: no pin lane; the link is probed straight from the pageable rows)
+    const bool pageable = c->cfg.pageable && is_pageable(W_host) && c->cfg.strategy != HG_STRATEGY_NAIVE;
     const uint8_t *src = (const uint8_t *)W_host;
     int64_t lbytes = wbytes;
     double v_pin = INFINITY;
+    if (c->cfg.pageable && is_pageable(W_host) && c->cfg.strategy == HG_STRATEGY_NAIVE)
+        lbytes = std::min<int64_t>(wbytes, (int64_t)c->nslots * c->slot_bytes);
     if (pageable) {
         HG_TRY(ensure_pinlane(c));
         lbytes = std::min<int64_t>(wbytes, (int64_t)c->nstage * c->slot_bytes);

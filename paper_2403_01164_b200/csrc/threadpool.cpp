@@ -31,6 +31,15 @@ class ThreadPool {
             });
         }
     }
+    ThreadPool(int n, const std::vector<int> &cpus) : n_(n < 1 ? 1 : n) {
+        for (int i = 1; i < n_; ++i) {
+            const int core = cpus.empty() ? -1 : cpus[(size_t)i % cpus.size()];
+            threads_.emplace_back([this, i, core] {
+                if (core >= 0) pin(core);
+                loop(i);
+            });
+        }
+    }
     ~ThreadPool() {
         stop_.store(true, std::memory_order_release);
         gen_.fetch_add(1, std::memory_order_acq_rel);
@@ -111,6 +120,7 @@ class ThreadPool {
 static_assert(sizeof(std::atomic<uint32_t>) == 4, "futex word");
 
 ThreadPool *pool_create(int nthreads, int first_core) { return new ThreadPool(nthreads, first_core); }
+ThreadPool *pool_create_cpus(int nthreads, const std::vector<int> &cpus) { return new ThreadPool(nthreads, cpus); }
 void pool_destroy(ThreadPool *p) { delete p; }
 int pool_size(const ThreadPool *p) { return p->size(); }
 void pool_run(ThreadPool *p, void (*fn)(void *, int), void *arg) { p->run(fn, arg); }

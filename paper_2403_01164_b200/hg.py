@@ -30,6 +30,7 @@ STATUS_NAMES = {0: "HG_OK", -1: "HG_EINVAL", -2: "HG_ENOTPINNED", -3: "HG_ENOTDE
                 -10: "HG_EUNSUPPORTED"}
 HG_MAX_BATCH = 8
 EXACT, APPROX, TPRIME, ASYNC, FIXED = 0, 1, 2, 3, 4
+HYBRID, NAIVE, PINNED_BLOCKING = 0, 1, 2  # hg_strategy (Fig. 5c / 5a / 5b)
 
 
 class HgError(RuntimeError):
@@ -70,7 +71,8 @@ class Config(ctypes.Structure):
                 ("gemv_tc_min_batch", ctypes.c_int32), ("handshake", ctypes.c_int32),
                 ("mirror_glue", ctypes.c_int32), ("verify_mirror", ctypes.c_int32),
                 ("stream_mode", ctypes.c_int32), ("pageable", ctypes.c_int32), ("pin_threads", ctypes.c_int32),
-                ("_pad1", ctypes.c_int32), ("staging_bytes", ctypes.c_int64)]
+                ("strategy", ctypes.c_int32), ("staging_bytes", ctypes.c_int64), ("numa_node", ctypes.c_int32),
+                ("_pad2", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -154,6 +156,11 @@ _sig = {
     "hg_alpha_solve": (_i32, [_P(_dbl), _P(_dbl), _P(_dbl), _P(_dbl), _i32, _i32, _dbl, _dbl, _dbl,
                               _P(_dbl), _P(_i32)]),
     "hg_alpha_bench": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _dbl, _P(AbenchCfg), _P(AbenchResult), _vp]),
+    "hg_numa_node": (_i32, [_i32, _P(_i32)]),
+    "hg_numa_cpus": (_i32, [_i32, _P(_i32), _i32, _P(_i32)]),
+    "hg_host_alloc": (_i32, [ctypes.c_size_t, _i32, _i32, _P(_vp)]),
+    "hg_host_free": (_i32, [_vp, ctypes.c_size_t, _i32]),
+    "hg_numa_node_of_ptr": (_i32, [_vp, _P(_i32)]),
     "hg_stats": (_i32, [_vp, _P(Stats)]),
     "hg_reset_stats": (_i32, [_vp]),
 }
@@ -244,6 +251,57 @@ def hg_alpha_solve(alphas, t_cpu, t_com, degree, lo, hi, seed, t_pin=None):
     _check(_lib.hg_alpha_solve(arr(alphas), arr(t_cpu), arr(t_com), None if t_pin is None else arr(t_pin), n,
                                degree, float(lo), float(hi), float(seed), ctypes.byref(out), ctypes.byref(cl)))
     return out.value, bool(cl.value)
+
+
+def hg_numa_node(device: int) -> int:
+    n = _i32()
+    _check(_lib.hg_numa_node(device, ctypes.byref(n)))
+    return n.value
+
+
+def hg_numa_cpus(node: int) -> list:
+    n = _i32()
+    _check(_lib.hg_numa_cpus(node, None, 0, ctypes.byref(n)))
+    arr = (_i32 * max(1, n.value))()
+    _check(_lib.hg_numa_cpus(node, arr, n.value, ctypes.byref(n)))
+    return [int(arr[i]) for i in range(n.value)]
+
+
+def hg_numa_node_of_ptr(ptr) -> int:
+    n = _i32()
+    _check(_lib.hg_numa_node_of_ptr(_ptr(ptr), ctypes.byref(n)))
+    return n.value
+
+
+class HostBuffer:
+    """hg_host_alloc'ed memory (NUMA-bound, optionally page-locked) viewed as a torch tensor; freed on
+    close() / garbage collection.  Replaces torch's pinned allocator for GB-sized weights (no
+    power-of-two rounding, pages placed on the rank's node before first touch)."""
+
+    def __init__(self, shape, dtype, node: int = -1, lock: bool = True):
+        import numpy as np
+        import torch
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        self.nbytes = int(np.prod(shape)) * itemsize
+        self.lock = int(bool(lock))
+        p = _vp()
+        _check(_lib.hg_host_alloc(self.nbytes, node, self.lock, ctypes.byref(p)))
+        self.ptr = p.value
+        buf = (ctypes.c_byte * self.nbytes).from_address(self.ptr)
+        buf._hg_owner = self  # views of the tensor keep the allocation alive
+        self.tensor = torch.frombuffer(buf, dtype=dtype).view(*shape)
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.tensor = None
+            _lib.hg_host_free(self.ptr, self.nbytes, self.lock)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def hg_dist_unique_id() -> bytes:

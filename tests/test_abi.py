@@ -26,7 +26,7 @@ def test_every_declared_symbol_is_exported_and_bound():
     for n in names:
         assert hasattr(lib, n), n
         assert n in hg.EXPORTED, f"{n} not bound in hg.py"
-    assert hg.hg_abi_version() == 2
+    assert hg.hg_abi_version() == 3
 
 
 def test_library_has_sm100a_code():
@@ -164,3 +164,40 @@ def test_hg_plan_hand_worked_time_fields():
     assert (p.n_res, p.n_str, p.n_cpu, p.chunk_rows, p.n_chunks) == (128, 768, 256, 384, 2)
     assert abs(p.t_pred - 1.1) <= 1e-12 and abs(p.t_eq4 - 1.2) <= 1e-12
     assert p.t_hbm == 1.0 and p.t_roof == 1.0
+
+
+def test_numa_cpulist_and_host_alloc():
+    """Host placement helpers: node 0's cpulist from sysfs matches the kernel's view,
+    a bad node is an error, and NUMA-bound host memory (not page-locked here: no GPU) is usable and
+    lives on its node when the kernel reports page placement."""
+    import os
+    path = "/sys/devices/system/node/node0/cpulist"
+    if not os.path.exists(path):
+        pytest.skip("no NUMA sysfs")
+    cpus = hg.hg_numa_cpus(0)
+    assert cpus and cpus == sorted(set(cpus))
+    assert set(cpus) <= set(range(os.cpu_count() or 1)) | set(os.sched_getaffinity(0))
+    with pytest.raises(hg.HgError):
+        hg.hg_numa_cpus(100000)
+    import torch
+    buf = hg.HostBuffer((1024, 512), torch.int16, node=0, lock=False)
+    t = buf.tensor
+    assert t.shape == (1024, 512) and int(t.abs().sum()) == 0
+    t.fill_(7)
+    assert int(t.sum()) == 7 * 1024 * 512
+    assert hg.hg_numa_node_of_ptr(t.data_ptr()) in (-1, 0)
+    buf.close()
+
+
+def test_parse_cpulist_via_node_file_format():
+    """hg_numa_cpus parses sysfs ranges ("0-3,8,10-11"): the running machine's lists are consistent
+    with /proc's online cpu count."""
+    import os
+    nodes = [d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")] \
+        if os.path.isdir("/sys/devices/system/node") else []
+    if not nodes:
+        pytest.skip("no NUMA sysfs")
+    allc = []
+    for d in nodes:
+        allc += hg.hg_numa_cpus(int(d[4:]))
+    assert len(allc) == len(set(allc)) and len(allc) <= (os.cpu_count() or 1)

@@ -232,13 +232,16 @@ def test_mirrored_glue_mixed_residency():
     assert np.array_equal(outs[0], outs[1])
 
 
-def test_stack_pageable_weights_equal_pinned():
-    """A stack whose host weights are pageable (pin lane, Sec. 4.3) gives the same bits as pinned."""
+@pytest.mark.parametrize("strategy", [hg.HYBRID, hg.NAIVE, hg.PINNED_BLOCKING])
+def test_stack_pageable_weights_equal_pinned(strategy):
+    """A stack whose host weights are pageable gives the same bits as pinned under every strategy of
+    Fig. 5 (hybrid: pin lane, Sec. 4.3; naive: copies from un-pinned rows; pinned-blocking: pin first
+    on the CPU lane's threads)."""
     H, F, B = 256, 1024, 2
     outs = []
     for pageable in (1, 0):
         with hg.Context(0, chunk_bytes=256 << 10, ring_bytes=4 << 20, max_k=4096, max_n=8192, pageable=pageable,
-                        staging_bytes=1 << 20, wrap_prefetch=1) as c:
+                        staging_bytes=1 << 20, wrap_prefetch=1, strategy=strategy) as c:
             keep, layers = [], []
             for l in range(2):
                 L = make_layer_mirror(c, H, F, B, layer=l, alpha=0.6, keep=keep)
@@ -261,5 +264,6 @@ def test_stack_pageable_weights_equal_pinned():
                 torch.cuda.synchronize()
             outs.append(bits(h))
             if pageable:
-                assert c.hg_stats().bytes_pinned > 0
+                assert (c.hg_stats().bytes_pinned > 0) == (strategy != hg.NAIVE)
+                assert c.hg_stats().mirror_linears > 0
     assert np.array_equal(outs[0], outs[1])

@@ -303,15 +303,16 @@ def _pageable(bits):
     return torch.from_numpy(np.ascontiguousarray(bits, np.uint16).view(np.int16).copy())
 
 
+@pytest.mark.parametrize("strategy", [hg.HYBRID, hg.NAIVE, hg.PINNED_BLOCKING])
 @pytest.mark.parametrize("B,stage_mb", [(1, 512), (2, 2), (8, 2)])
-def test_pageable_weights_pin_lane(B, stage_mb):
+def test_pageable_weights_pin_lane(B, stage_mb, strategy):
     """hg_config.pageable: streamed chunks of a pageable weight go through the pin lane (pinned staging
     ring, tags in mapped memory) -- results bit-identical to the pinned-weight path; a 2-slot staging
     ring (1 MiB chunks) forces slot reuse."""
     N, K = 3072, 1024
     x, W, b = gen.linear_inputs(36, 0, "fc1", B, N, K)
     with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=4096, max_n=4096, pageable=1,
-                    staging_bytes=stage_mb << 20) as cp, \
+                    staging_bytes=stage_mb << 20, strategy=strategy) as cp, \
             hg.Context(0, chunk_bytes=1 << 20, ring_bytes=16 << 20, max_k=4096, max_n=4096) as cq:
         for n_res, alpha in ((0, 0.7), (512, 1.0)):
             Wd = dev(W[:n_res]) if n_res else None
@@ -323,7 +324,16 @@ def test_pageable_weights_pin_lane(B, stage_mb):
             assert np.array_equal(y_pg.cpu().numpy(), y_pin.cpu().numpy()), (n_res, alpha)
             assert oracle.within_tol(y_pg.cpu().numpy(), oracle.linear(x, W, b))[0]
         s = cp.hg_stats()
-        assert s.bytes_pinned > 0 and s.pin_busy_s > 0
+        if strategy == hg.NAIVE:  # Fig. 5a: no pin lane; the driver stages the pageable rows
+            assert s.bytes_pinned == 0
+        else:
+            assert s.bytes_pinned > 0 and s.pin_busy_s > 0
+
+
+def test_strategy_config_validated():
+    with pytest.raises(hg.HgError) as e:
+        hg.Context(0, max_k=1024, max_n=1024, strategy=3)
+    assert e.value.status == hg.HG_EINVAL
 
 
 def test_pageable_measure_reports_pin_rate():

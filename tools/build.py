@@ -69,6 +69,7 @@ PRODUCT_SOURCES = [
     ("glue_sm100.cu", "cu"),
     ("runtime.cu", "cu"),
     ("dist.cpp", "cxx"),
+    ("numa.cpp", "cxx"),
 ]
 
 
