@@ -30,6 +30,9 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# one hardware work queue per stream (see tests/conftest.py): the peer exchange's wait kernel spins,
+# and an unrelated copy queued behind it in a shared queue would wait for it
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 # OPT decoder dimensions (hidden, ffn, layers) and BASELINE.json config index (seed offset)
 MODELS = {"opt-6.7b": (4096, 16384, 32, 1), "opt-13b": (5120, 20480, 40, 2), "opt-30b": (7168, 28672, 48, 3),
@@ -400,7 +403,13 @@ def prepare(args, weights=None, **ctx_extra):
     if world > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx, threads = make_context(args, rank, world, local, **ctx_extra)
-    if world > 1:
+    if world > 1 and args.exchange == "peer":
+        # a8 over peer memory (peer.cu): device boxes opened by CUDA IPC over NVLink, one host segment
+        # shared by the ranks' CPU lanes (mirrored glue at any P)
+        blobs = [None] * world
+        dist.all_gather_object(blobs, ctx.hg_peer_export(world, rank))
+        ctx.hg_peer_open(blobs)
+    elif world > 1:
         uid = hg.hg_dist_unique_id() if rank == 0 else None
         obj = [uid]
         dist.broadcast_object_list(obj, src=0)
@@ -709,7 +718,7 @@ def run_point(st, args, budget_gb=0.0):
                    else "pinned once at load",
                    "alpha": next((p.alpha_eff for p in all_plans if p.n_res < p.N), 0.0),
                    "alpha_seed_eq5": alpha_seed,
-                   "parallelism": f"tp{world} column shards" if world > 1 else "1 GPU",
+                   "parallelism": (f"tp{world} column shards, %s exchange" % args.exchange) if world > 1 else "1 GPU",
                    "chunk_MiB": args.chunk_mb, "ring_MiB": args.ring_mb, "cpu_threads": st["threads"],
                    "numa": {"node": st["placement"][0], "cores_per_rank": st["placement"][1],
                             "pool_pinned_from": st["placement"][2],
@@ -899,6 +908,9 @@ def parse_args(argv=None):
                     help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,
                     help="NEXT(3): GPU memory for resident weights, placed by the module scheduler (Sec. 4.5)")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"],
+                    help="N > 1: the shard exchange after each linear -- peer-memory pushes + shared host segment "
+                         "(default) or NCCL all-gather (GPU-only glue)")
     ap.add_argument("--numa", default="auto", choices=["auto", "off"],
                     help="host placement: weights bound to the GPU's NUMA node; with N > 1 each rank's CPU "
                          "lane pinned to its share of that node's cores")

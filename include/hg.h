@@ -427,6 +427,27 @@ HG_API const char *hg_host_isa(void);
  *   communicator on every rank.  NCCL is loaded at run time (HG_ENCCL if absent). */
 HG_API hg_status hg_dist_unique_id(void *id128);
 HG_API hg_status hg_dist_init(hg_ctx *ctx, int nranks, int rank, const void *id128);
+/* The a8 exchange over peer memory (peer.cu), the alternative to NCCL: after each linear every rank
+ * pushes its [B, N/P] rows straight into every rank's device "box" at their global columns (stores
+ * through peer pointers -- NVLink P2P between GPUs, plain stores between ranks sharing a GPU) and
+ * raises its flag there; a rank's wait kernel copies the box into y once all P flags are up.  On the
+ * host, the ranks share one segment (POSIX shm) holding each linear's full y: every rank's CPU lane
+ * writes its CPU rows there and its GPU rows land there by D2H, so the mirrored glue (reading R24)
+ * runs at any P with no device round trip on the CPU lane's critical path.
+ * Setup, in every rank (one process per GPU, or one thread per rank in one process):
+ *   hg_peer_export(ctx, P, p, blob)  -> this rank's HG_PEER_BLOB bytes (rank 0 creates the segment)
+ *   all-gather the blobs in rank order (e.g. torch.distributed.all_gather_object)
+ *   hg_peer_open(ctx, blobs)         -> opens every peer (CUDA IPC for other processes) and the segment
+ * Then hg_linear_sharded and hg_stack / hg_layer with per-rank row shards use the peer exchange.
+ * Every rank must issue the same sequence of calls.  Exclusive with hg_dist_init.  Errors: HG_EINVAL
+ * (bad shape, mismatching blobs), HG_ECUDA (IPC / peer access), HG_ENOMEM. */
+#define HG_PEER_BLOB 512
+HG_API hg_status hg_peer_export(hg_ctx *ctx, int nranks, int rank, void *blob);
+HG_API hg_status hg_peer_open(hg_ctx *ctx, const void *blobs);
+/* Debug: this rank's exchange flags [4][8], done word, exchange count and flag addresses per rank
+ * (synchronous copies) into out[0 .. 50). */
+HG_API hg_status hg_debug_peer_words(hg_ctx *ctx, uint32_t *out);
+
 /* The a8 exchange's layout step alone (the same kernel hg_linear_sharded / hg_stack run after the
  * all-gather): gathered [nranks][batch][n_local] fp32 device (rank-major, as ncclAllGather leaves
  * it) -> y [batch][nranks * n_local] fp32 device in global column order, y[b, p*n_local + j] =

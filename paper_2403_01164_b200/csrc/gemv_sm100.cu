@@ -41,6 +41,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "hg_internal.h"
@@ -311,6 +312,9 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
                 __nanosleep(64);
                 if (globaltimer() - t0 > a.timeout_ns) {
                     *(volatile uint32_t *)a.err = 1u;  // mapped host word: a plain store (no PCIe atomic)
+                    if (blockIdx.x == 0)
+                        printf("hg gemv: timed out on slot %d tag %u (arrived %u, consumed %u)\n", (int)src.slot,
+                               (unsigned)src.tag, ld_acquire(a.arrived + src.slot), ld_acquire(a.consumed + src.slot));
                     return;
                 }
             }
@@ -640,7 +644,7 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.err = L.err;
     a.trace = L.trace;
     a.trace_id = L.trace_id;
-    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
+    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9 * dev_timeout_scale());
     a.stamps = g_stamps;
     if (a.P > 1 && (!a.ws || !a.gbar || !a.err || a.gp > kGroupCounters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;

@@ -641,7 +641,7 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.consumed = L.consumed;
     a.slot_cnt = L.slot_cnt;
     a.err = L.err;
-    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9);
+    a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9 * dev_timeout_scale());
     a.stamps = gemv_stamps_dev();
     if (a.S > 1 && (!a.ws || !counters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;

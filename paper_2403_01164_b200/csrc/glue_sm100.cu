@@ -9,6 +9,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <utility>
 
 #include <cstdint>
@@ -169,7 +171,8 @@ int pdl_launch(void (*kernel)(Exp...), unsigned grid, void *stream, Act &&...arg
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    static const bool pdl = !getenv("HG_GLUE_PDL") || atoi(getenv("HG_GLUE_PDL")) != 0;
+    cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, std::forward<Act>(args)...);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();

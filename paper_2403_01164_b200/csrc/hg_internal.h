@@ -4,6 +4,7 @@
 
 #include <cstdarg>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
 
 #include "hg.h"
@@ -135,6 +136,34 @@ class ThreadPool;
 ThreadPool *pool_create(int nthreads, int first_core);
 // workers pinned to cpus[i % cpus.size()] (worker 0 is the caller's thread and is not pinned)
 ThreadPool *pool_create_cpus(int nthreads, const std::vector<int> &cpus);
+
+// Device-side bounded waits use timeout_s x this (HG_DEV_TIMEOUT_SCALE, default 1; debugging: < 1
+// lets the kernels give up -- and print what they waited for -- before the host's own waits do).
+inline double dev_timeout_scale() {
+    static const double s = getenv("HG_DEV_TIMEOUT_SCALE") ? atof(getenv("HG_DEV_TIMEOUT_SCALE")) : 1.0;
+    return s > 0 ? s : 1.0;
+}
+
+// peer.cu: the a8 exchange over peer memory (device pushes + flags; shared host segment)
+constexpr int kMaxPeers = 8;
+constexpr int kDevSlots = 4;
+struct PeerGroup;
+hg_status peer_export(PeerGroup **pg, int device, int nranks, int rank, int64_t box_floats, int64_t host_floats,
+                      void *blob_out);
+hg_status peer_open(PeerGroup *g, const void *blobs);
+void peer_destroy(PeerGroup *g);
+int peer_nranks(const PeerGroup *g);
+void peer_debug_words(PeerGroup *g, uint32_t *out);
+int peer_rank(const PeerGroup *g);
+int peer_exchange(PeerGroup *g, const float *ylocal, int B, int64_t n_local, float *y, int64_t ldy, uint32_t *err,
+                  double timeout_s, void *stream);
+float *peer_host_y(PeerGroup *g, int64_t k);
+float *peer_host_y_dev(PeerGroup *g, int64_t k);
+int peer_host_slots();
+void peer_host_publish(PeerGroup *g, int64_t k);
+hg_status peer_host_wait_ready(PeerGroup *g, int64_t k, double timeout_s);
+void peer_host_consumed(PeerGroup *g, int64_t k);
+hg_status peer_host_wait_free(PeerGroup *g, int64_t k, double timeout_s);
 
 // numa.cpp: host placement of a rank
 std::vector<int> parse_cpulist(const char *s);

@@ -324,8 +324,12 @@ struct hg_ctx {
     void *h1 = nullptr;
     int64_t act_elems = 0, yscr_elems = 0, h1_elems = 0;
 
-    // multi-GPU
+    // multi-GPU: NCCL all-gather (hg_dist_init) or the peer-memory exchange (hg_peer_open, peer.cu)
     Dist *dist = nullptr;
+    PeerGroup *peer = nullptr, *peer_pending = nullptr;
+    float *ylring = nullptr;  // P > 1 mirrored stack: this rank's rows per linear, device [kMirrorRing][...]
+    int64_t hseq = 0;         // linears run through the mirrored stack so far (host-segment index)
+    std::vector<void *> retired;  // outgrown scratch buffers (freed by hg_destroy)
     float *ylocal = nullptr, *gbuf = nullptr;
     int64_t ylocal_elems = 0, gbuf_elems = 0;
 
@@ -342,6 +346,7 @@ struct hg_ctx {
 
 namespace hg {
 namespace {
+int nranks_of(const hg_ctx *c) { return c->peer ? peer_nranks(c->peer) : dist_nranks(c->dist); }
 host_rows_fn host_fn_for(hg_ctx *c, int batch) {
     return (c->amx_min_batch > 0 && batch >= c->amx_min_batch) ? host_rows_amx : c->host_fn;
 }
@@ -455,6 +460,11 @@ hg_status wait_event(hg_ctx *c, cudaEvent_t ev, double *waited) {
         for (int i = 0; i < 16; ++i) _mm_pause();
         if ((spin & 1023) == 1023 && secs(t0, clk::now()) > c->cfg.timeout_s) {
             c->error = true;
+            if (getenv("HG_PEER_DEBUG"))
+                fprintf(stderr, "hg: event wait timeout: next_seq %lld inflight %zu (front seq %lld) prebound %lld "
+                        "fpos %zu/%zu err %u\n", (long long)c->next_seq, c->inflight.size(),
+                        c->inflight.empty() ? -1ll : (long long)c->inflight.front().seq, (long long)c->prebound, c->fpos,
+                        c->future.size(), c->err_host ? c->err_host[0] : 0u);
             return set_error(HG_ETIMEOUT, "event wait exceeded %.1f s", c->cfg.timeout_s);
         }
     }
@@ -989,7 +999,9 @@ hg_status validate_lin(hg_ctx *c, const hg_plan_t &p, const void *x, const void 
 hg_status check_async_errors(hg_ctx *c) {
     if (c->err_host && c->err_host[0]) {
         c->error = true;
-        return set_error(HG_ETIMEOUT, "a GEMV waited longer than %.1f s for a streamed chunk", c->cfg.timeout_s);
+        return set_error(HG_ETIMEOUT, c->err_host[0] == 2u ? "a peer exchange waited longer than %.1f s for another rank"
+                                                           : "a GEMV waited longer than %.1f s for a streamed chunk",
+                         c->cfg.timeout_s);
     }
     if (c->pin && pinlane_error(c->pin)) {
         c->error = true;
@@ -1035,12 +1047,13 @@ hg_status end_call(hg_ctx *c, cudaStream_t s) {
     return HG_OK;
 }
 
+// Grow a scratch buffer.  The old one may still be read by queued work, and freeing it would
+// synchronise the whole device (cudaFree) -- a deadlock when other ranks share the device and spin on
+// this rank's next exchange -- so it is retired and freed with the context.
 hg_status ensure(hg_ctx *c, void **p, int64_t *have, int64_t need_bytes) {
     if (*have >= need_bytes) return HG_OK;
     if (*p) {
-        HG_TRY(sync_naive(c));
-        HG_CK(c, cudaDeviceSynchronize());
-        cudaFree(*p);
+        c->retired.push_back(*p);
         *p = nullptr;
     }
     HG_CK(c, cudaMalloc(p, (size_t)need_bytes));
@@ -1050,7 +1063,13 @@ hg_status ensure(hg_ctx *c, void **p, int64_t *have, int64_t need_bytes) {
 
 // all-gather this rank's [B, n_local] shard into y [B, P*n_local]
 hg_status gather(hg_ctx *c, const float *ylocal, int B, int64_t n_local, float *y, cudaStream_t s) {
-    const int P = dist_nranks(c->dist);
+    const int P = nranks_of(c);
+    if (c->peer) {  // peer-memory exchange: pushes + flags, the full y in global column order
+        HG_TRY(kerr(c, peer_exchange(c->peer, ylocal, B, n_local, y, (int64_t)P * n_local, c->err, c->cfg.timeout_s, s),
+                    "peer exchange"));
+        c->st.gpu_launches += 2;
+        return HG_OK;
+    }
     if (B == 1) return dist_allgather(c->dist, ylocal, y, (size_t)n_local, s);
     HG_TRY(ensure(c, (void **)&c->gbuf, &c->gbuf_elems, (int64_t)P * B * n_local * 4));
     HG_TRY(dist_allgather(c->dist, ylocal, c->gbuf, (size_t)B * n_local, s));
@@ -1062,7 +1081,7 @@ hg_status gather(hg_ctx *c, const float *ylocal, int B, int64_t n_local, float *
 // One linear of a layer: sharded (P > 1: local rows then all-gather) or not.
 hg_status layer_linear(hg_ctx *c, const hg_linear_desc &d, const void *x, float *y, int64_t N_full,
                        cudaStream_t s) {
-    const int P = dist_nranks(c->dist);
+    const int P = nranks_of(c);
     Lin L{d.plan, x, d.W_dev, (const uint8_t *)d.W_host, d.bias, y, N_full};
     if (P == 1) return run_linear(c, L, s);
     HG_TRY(ensure(c, (void **)&c->ylocal, &c->ylocal_elems, d.plan.batch * d.plan.N * 4));
@@ -1073,7 +1092,7 @@ hg_status layer_linear(hg_ctx *c, const hg_linear_desc &d, const void *x, float 
 }
 
 hg_status validate_layer(hg_ctx *c, const hg_opt_layer &l, int B) {
-    const int P = dist_nranks(c->dist);
+    const int P = nranks_of(c);
     const int64_t H = l.hidden, F = l.ffn;
     const int64_t Ns[4] = {3 * H, H, F, H}, Ks[4] = {H, H, H, F};
     if (H <= 0 || F <= 0) return set_error(HG_EINVAL, "layer: hidden/ffn must be > 0");
@@ -1139,7 +1158,8 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
 
 // ---------------------------------------------------------------- mirrored glue (reading R24)
 bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n) {
-    if (!c->cfg.mirror_glue || dist_nranks(c->dist) != 1 || !hglue_supported()) return false;
+    // P > 1 mirrors only through the peer group's shared host segment (not with NCCL)
+    if (!c->cfg.mirror_glue || (nranks_of(c) != 1 && !c->peer) || !hglue_supported()) return false;
     bool any_cpu = false;  // without CPU rows nobody needs the glue on the host
     for (int l = 0; l < n; ++l)
         for (int i = 0; i < 4; ++i) any_cpu |= layers[l].lin[i].plan.n_cpu > 0;
@@ -1205,6 +1225,7 @@ hg_status ensure_mirror(hg_ctx *c) {
         HG_CK(c, cudaEventCreateWithFlags(&c->ev_use[r], cudaEventDisableTiming));
     }
     HG_CK(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    if (c->peer) HG_CK(c, cudaMalloc((void **)&c->ylring, per * 4 * hg_ctx::kMirrorRing));
     return HG_OK;
 }
 
@@ -1236,6 +1257,32 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
     const int total = 4 * nl;
     auto lin_of = [&](int k) -> const hg_linear_desc & { return layers[k / 4].lin[k % 4]; };
     auto ydev = [&](int k) { return c->yring + (int64_t)(k % R) * ystride; };
+    // P > 1 (peer group, peer.cu): linear k's full y lives in the host segment shared by all ranks (this
+    // rank's columns start at pr * n_local); the device computes its rows into a local ring slot and the
+    // peer exchange assembles the full y in ydev(k)
+    PeerGroup *g = c->peer;
+    const int Pn = g ? peer_nranks(g) : 1, pr = g ? peer_rank(g) : 0;
+    const int64_t hk0 = c->hseq;  // host-segment index of linear 0 of this call
+    c->hseq += total;
+    auto ylocal = [&](int k) { return Pn > 1 ? c->ylring + (int64_t)(k % R) * ystride : ydev(k); };
+    auto yhost_of = [&](int k) { return Pn > 1 ? peer_host_y(g, hk0 + k) : c->yhost[k % R]; };
+    auto yhost_dev_of = [&](int k) { return Pn > 1 ? peer_host_y_dev(g, hk0 + k) : c->ymap[k % R]; };
+    // this rank's part of linear j in the host segment: CPU rows written (its CPU job was joined in
+    // iteration j) and GPU rows' D2H landed; published in order, eagerly when the D2H is already done
+    int published = -1;
+    auto publish_upto = [&](int j, bool block) -> hg_status {
+        while (published < j) {
+            const int q = published + 1;
+            if (block) HG_TRY(wait_event(c, c->ev_yg[q % R], &c->st.x_wait_s));
+            else if (cudaEventQuery(c->ev_yg[q % R]) != cudaSuccess) {
+                cudaGetLastError();
+                return HG_OK;
+            }
+            peer_host_publish(g, hk0 + q);
+            published = q;
+        }
+        return HG_OK;
+    };
     // host catch-up: apply the glue of linears (done, upto] to the host residual stream; the input
     // x itself is produced only for `upto` (the linear whose CPU rows are about to run)
     int done = -1;
@@ -1246,8 +1293,15 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             const bool want_x = k == upto;
             const float *yp = nullptr;  // previous linear's full y on the host
             if (k > 0) {
-                HG_TRY(wait_event(c, c->ev_yg[(k - 1) % R], &c->st.x_wait_s));
-                yp = c->yhost[(k - 1) % R];
+                if (Pn > 1) {  // every rank's rows of linear k-1 in the shared segment
+                    HG_TRY(publish_upto(k - 1, true));
+                    const auto tw = clk::now();
+                    HG_TRY(peer_host_wait_ready(g, hk0 + k - 1, c->cfg.timeout_s));
+                    c->st.x_wait_s += secs(tw, clk::now());
+                } else {
+                    HG_TRY(wait_event(c, c->ev_yg[(k - 1) % R], &c->st.x_wait_s));
+                }
+                yp = yhost_of(k - 1);
             }
             const auto tg = clk::now();
             if (i == 0) {
@@ -1262,6 +1316,7 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
                 if (want_x) hglue_relu_bf16(yp, L.ffn, L.ffn, B, xh);
             }
             c->st.glue_s += secs(tg, clk::now());
+            if (Pn > 1 && k > 0) peer_host_consumed(g, hk0 + k - 1);
             done = k;
         }
         return HG_OK;
@@ -1273,8 +1328,11 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
         const hg_linear_desc &d = lin_of(k);
         const hg_plan_t &p = d.plan;
         const int64_t N = p.N, K = p.K, n_gpu = p.n_res + p.n_str;
+        const int64_t N_full = N * Pn, col0 = (int64_t)pr * N;  // this rank's columns of the full y
         const int slot = k % R;
-        float *yd = ydev(k);
+        float *yd = ydev(k);          // full y on the device
+        float *yl = ylocal(k);        // this rank's rows (== yd at P = 1)
+        float *yh = yhost_of(k);      // full y on the host (ld N_full)
         const float *yprev_d = k > 0 ? ydev(k - 1) : nullptr;
         HG_TRY(pump(c));
         // ---- GPU glue -> act (run_layer's kernels, reading the previous linear's ring slot)
@@ -1301,6 +1359,12 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             HG_CK(c, cudaStreamWaitEvent(s, c->ev_yg[slot], 0));
             if (done < k - R + 1) HG_TRY(catch_up(k - R + 1));
         }
+        if (Pn > 1) {  // the shared host slot's previous occupant has been read by every rank
+            HG_TRY(publish_upto(k - 1, false));
+            const auto tw = clk::now();
+            HG_TRY(peer_host_wait_free(g, hk0 + k, c->cfg.timeout_s));
+            c->st.x_wait_s += secs(tw, clk::now());
+        }
         HostJob job;
         auto t0 = clk::now();
         // pinned-blocking (Fig. 5b): this linear's streamed rows are pinned on the pool threads first,
@@ -1309,14 +1373,14 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
         hg_status gst = HG_OK;
         bool gpu_done = false;
         auto gpu_lanes = [&]() {
-            Lin lin{p, c->act, d.W_dev, (const uint8_t *)d.W_host, d.bias, yd, N};
+            Lin lin{p, c->act, d.W_dev, (const uint8_t *)d.W_host, d.bias, yl, N};
             gst = enqueue_gpu_lanes(c, lin, s);
             if (gst == HG_OK && n_gpu > 0) {
                 cudaError_t e = cudaEventRecord(c->ev_g[slot], s);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_g[slot], 0);
                 if (e == cudaSuccess) e = cudaStreamWaitEvent(c->d2h, c->ev_use[slot], 0);
                 if (e == cudaSuccess)
-                    e = cudaMemcpy2DAsync(c->yhost[slot], (size_t)N * 4, yd, (size_t)N * 4, (size_t)n_gpu * 4,
+                    e = cudaMemcpy2DAsync(yh + col0, (size_t)N_full * 4, yl, (size_t)N * 4, (size_t)n_gpu * 4,
                                           (size_t)B, cudaMemcpyDeviceToHost, c->d2h);
                 if (e != cudaSuccess) gst = kerr(c, (int)e, "y D2H");
             }
@@ -1342,8 +1406,8 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             job.n = p.n_cpu;
             job.W = (const uint16_t *)((const uint8_t *)d.W_host + 2 * K * p.n_str);
             job.bias = d.bias_host ? d.bias_host + n_gpu : nullptr;
-            job.y = c->yhost[slot] + n_gpu;
-            job.ldy = N;
+            job.y = yh + col0 + n_gpu;
+            job.ldy = N_full;
             job.block = 16;
             job.next.store(0);
             t0 = clk::now();  // CPU-lane busy time starts here (catch-up waits are x_wait)
@@ -1361,14 +1425,19 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
         HG_TRY(dbg_sync(c, s, "gemv + y D2H", k));
         // ---- join: the CPU rows (bias already added on the host) into the ring slot on the device
         if (p.n_cpu > 0) {
-            HG_TRY(kerr(c, launch_join(yd, N, n_gpu, p.n_cpu, B, c->ymap[slot] + n_gpu, N,
+            HG_TRY(kerr(c, launch_join(yl, N, n_gpu, p.n_cpu, B, yhost_dev_of(k) + col0 + n_gpu, N_full,
                                        d.bias_host ? nullptr : d.bias, s), "join"));
             c->st.gpu_launches++;
             HG_TRY(dbg_sync(c, s, "join", k));
         }
+        if (Pn > 1) {  // a8: every rank's rows into every rank's y (peer stores), full y in yd
+            HG_TRY(kerr(c, peer_exchange(g, yl, B, N, yd, N_full, c->err, c->cfg.timeout_s, s), "peer exchange"));
+            c->st.gpu_launches += 2;
+            if (Pn > 1) HG_TRY(publish_upto(k, false));
+        }
         if (tr) {  // the linear's full output y (GPU rows + joined CPU rows)
             float *yt = i == 0 ? tr->y_qkv : i == 1 ? tr->y_o : i == 2 ? tr->y_fc1 : tr->y_fc2;
-            HG_TRY(trace_copy(c, yt, yd, (size_t)B * N * 4, s));
+            HG_TRY(trace_copy(c, yt, yd, (size_t)B * N_full * 4, s));
         }
         HG_CK(c, cudaEventRecord(c->ev_use[slot], s));
         c->st.n_linears++;
@@ -1377,6 +1446,8 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             c->st.gpu_launches++;
         }
     }
+    // every rank may be waiting on this rank's last rows: publish them before returning
+    if (Pn > 1) HG_TRY(publish_upto(total - 1, true));
     // the d2h stream must not run past this call's buffers unseen: order it before the caller's next work
     HG_CK(c, cudaEventRecord(c->ev_x, c->d2h));
     HG_CK(c, cudaStreamWaitEvent(s, c->ev_x, 0));
@@ -1571,6 +1642,8 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
         cudaSetDevice(c->device);
         cudaDeviceSynchronize();
         if (c->dist) dist_destroy(c->dist);
+        if (c->peer_pending) peer_destroy(c->peer_pending);
+        if (c->ylring) cudaFree(c->ylring);
         for (auto e : c->ev_arrived) if (e) cudaEventDestroy(e);
         for (auto e : c->ev_free) if (e) cudaEventDestroy(e);
         for (auto e : c->tev) cudaEventDestroy(e);
@@ -1593,6 +1666,7 @@ HG_API hg_status hg_destroy(hg_ctx *c) {
                         (void *)c->gbuf, (void *)c->tagmem})
             if (p) cudaFree(p);
         if (c->x_host) cudaFreeHost(c->x_host);
+        for (void *q : c->retired) cudaFree(q);
         if (c->err_host) cudaFreeHost((void *)c->err_host);
         for (float *p : c->ycpu_host)
             if (p) cudaFreeHost(p);
@@ -1634,7 +1708,7 @@ HG_API hg_status hg_linear_sharded(hg_ctx *c, const hg_plan_t *p, const void *x,
                                    const void *W_host, const float *bias, float *y_full,
                                    void *stream) {
     if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
-    if (!c->dist) return set_error(HG_ESTATE, "hg_dist_init not called");
+    if (!c->dist && !c->peer) return set_error(HG_ESTATE, "neither hg_dist_init nor hg_peer_open called");
     if (c->error) return set_error(HG_ESTATE, "context is in an error state");
     HG_CK(c, cudaSetDevice(c->device));
     HG_TRY(validate_lin(c, *p, x, W_dev, W_host, bias, y_full));
@@ -1644,7 +1718,7 @@ HG_API hg_status hg_linear_sharded(hg_ctx *c, const hg_plan_t *p, const void *x,
     push_chunks(list, *p, W_host);
     set_future(c, std::move(list), false);
     hg_linear_desc d{W_dev, W_host, bias, *p};
-    HG_TRY(layer_linear(c, d, x, y_full, p->N * dist_nranks(c->dist), s));
+    HG_TRY(layer_linear(c, d, x, y_full, p->N * nranks_of(c), s));
     return end_call(c, s);
 }
 
@@ -1833,6 +1907,47 @@ HG_API hg_status hg_gather_permute(hg_ctx *c, const float *gathered, int nranks,
     if (n_local > 0) HG_TRY(kerr(c, launch_gather_permute(gathered, nranks, batch, n_local, y, s), "gather permute"));
     c->st.gpu_launches++;
     HG_CK(c, cudaEventRecord(c->ev_done, s));
+    return HG_OK;
+}
+
+HG_API hg_status hg_peer_export(hg_ctx *c, int nranks, int rank, void *blob) {
+    if (!c || !blob) return set_error(HG_EINVAL, "NULL argument");
+    if (c->device < 0) return set_error(HG_ESTATE, "host-only context");
+    if (c->dist) return set_error(HG_ESTATE, "NCCL group already initialised (hg_dist_init)");
+    if (c->peer && (peer_nranks(c->peer) != nranks || peer_rank(c->peer) != rank))
+        return set_error(HG_ESTATE, "peer group already exported with another shape");
+    HG_CK(c, cudaSetDevice(c->device));
+    const int64_t floats = (int64_t)HG_MAX_BATCH * c->cfg.max_n;
+    PeerGroup *g = c->peer;
+    HG_TRY(peer_export(&g, c->device, nranks, rank, floats, floats, blob));
+    c->peer_pending = g;
+    return HG_OK;
+}
+
+HG_API hg_status hg_peer_open(hg_ctx *c, const void *blobs) {
+    if (!c || !blobs) return set_error(HG_EINVAL, "NULL argument");
+    if (!c->peer_pending) return set_error(HG_ESTATE, "hg_peer_export not called");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(peer_open(c->peer_pending, blobs));
+    c->peer = c->peer_pending;
+    // every buffer a call may need, allocated now: an allocation inside a call (cudaMalloc,
+    // cudaHostAlloc) can wait for the device to go idle -- a deadlock when another rank on the same
+    // device is spinning on this rank's next push
+    const int64_t n = (int64_t)HG_MAX_BATCH * c->cfg.max_n;
+    HG_TRY(ensure(c, (void **)&c->ylocal, &c->ylocal_elems, n * 4));
+    HG_TRY(ensure(c, &c->act, &c->act_elems, n * 2));
+    HG_TRY(ensure(c, (void **)&c->yscr, &c->yscr_elems, n * 4));
+    HG_TRY(ensure(c, &c->h1, &c->h1_elems, n * 2));
+    HG_TRY(ensure_mirror(c));
+    if (c->cfg.pageable) HG_TRY(ensure_pinlane(c));
+    HG_CK(c, cudaDeviceSynchronize());
+    return HG_OK;
+}
+
+HG_API hg_status hg_debug_peer_words(hg_ctx *c, uint32_t *out) {
+    if (!c || !out || !c->peer) return set_error(HG_EINVAL, "no peer group");
+    cudaSetDevice(c->device);
+    peer_debug_words(c->peer, out);
     return HG_OK;
 }
 
@@ -2050,8 +2165,11 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
     HG_TRY(drop_inflight(c));
     c->future.clear();
     c->fpos = 0;
+    // this context's streams only (ranks sharing the device may be mid-exchange)
     HG_TRY(sync_naive(c));
-    HG_CK(c, cudaDeviceSynchronize());
+    if (c->have_last) HG_CK(c, cudaEventSynchronize(c->ev_done));
+    HG_CK(c, cudaStreamSynchronize(c->copy));
+    if (c->d2h) HG_CK(c, cudaStreamSynchronize(c->d2h));
     HG_TRY(check_device_error(c));
     std::fill(c->slot_used.begin(), c->slot_used.end(), 0);
 

@@ -29,6 +29,7 @@ STATUS_NAMES = {0: "HG_OK", -1: "HG_EINVAL", -2: "HG_ENOTPINNED", -3: "HG_ENOTDE
                 -5: "HG_ECUDA", -6: "HG_ENCCL", -7: "HG_ENOMEM", -8: "HG_ESTATE", -9: "HG_ETIMEOUT",
                 -10: "HG_EUNSUPPORTED"}
 HG_MAX_BATCH = 8
+PEER_BLOB = 512  # bytes per rank exchanged by hg_peer_export / hg_peer_open
 EXACT, APPROX, TPRIME, ASYNC, FIXED = 0, 1, 2, 3, 4
 HYBRID, NAIVE, PINNED_BLOCKING = 0, 1, 2  # hg_strategy (Fig. 5c / 5a / 5b)
 
@@ -150,6 +151,9 @@ _sig = {
     "hg_host_isa": (ctypes.c_char_p, []),
     "hg_debug_gemv_stamps": (_i32, [_P(ctypes.POINTER(ctypes.c_uint64))]),
     "hg_gather_permute": (_i32, [_vp, _vp, _i32, _i32, _i64, _vp, _vp]),
+    "hg_peer_export": (_i32, [_vp, _i32, _i32, _vp]),
+    "hg_peer_open": (_i32, [_vp, _vp]),
+    "hg_debug_peer_words": (_i32, [_vp, _P(ctypes.c_uint32)]),
     "hg_dist_unique_id": (_i32, [_vp]),
     "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
     "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
@@ -402,6 +406,23 @@ class Context:
 
     def hg_gather_permute(self, gathered, nranks, batch, n_local, y, stream=None):
         _check(_lib.hg_gather_permute(self._h, _ptr(gathered), nranks, batch, n_local, _ptr(y), _stream(stream)))
+
+    def hg_peer_export(self, nranks, rank) -> bytes:
+        """This rank's 512-byte peer blob (device box + IPC handle; rank 0 also names the shared host
+        segment).  All-gather the blobs (rank order) and pass them to hg_peer_open."""
+        buf = ctypes.create_string_buffer(PEER_BLOB)
+        _check(_lib.hg_peer_export(self._h, nranks, rank, buf))
+        return buf.raw
+
+    def hg_peer_open(self, blobs):
+        data = b"".join(blobs)
+        buf = ctypes.create_string_buffer(data, len(data))
+        _check(_lib.hg_peer_open(self._h, buf))
+
+    def hg_debug_peer_words(self):
+        arr = (ctypes.c_uint32 * 64)()
+        _check(_lib.hg_debug_peer_words(self._h, arr))
+        return list(arr)
 
     def hg_dist_init(self, nranks, rank, uid: bytes):
         buf = ctypes.create_string_buffer(uid, 128)

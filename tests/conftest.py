@@ -1,6 +1,12 @@
 import os
 import sys
 
+# More hardware work queues than streams in flight: with the default 8, streams of different ranks
+# (and a rank's copy / D2H streams) share queues, and an operation queued behind a peer exchange's
+# spinning wait kernel in the same queue waits for it -- a false dependency that can deadlock ranks
+# (test_gpu_peer.py runs several ranks on one GPU).  Must be set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

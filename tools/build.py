@@ -67,6 +67,7 @@ PRODUCT_SOURCES = [
     ("gemv_sm100.cu", "cu"),
     ("gemv_tc_sm100.cu", "cu"),
     ("glue_sm100.cu", "cu"),
+    ("peer.cu", "cu"),
     ("runtime.cu", "cu"),
     ("dist.cpp", "cxx"),
     ("numa.cpp", "cxx"),
