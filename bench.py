@@ -431,31 +431,24 @@ def prepare(args, weights=None, **ctx_extra):
 
 
 def cpu_rate_per_kind(st):
-    """T-bar_CPU per module kind for the scheduler: the CPU lane's GEMV rate on layer 0's weight
-    of each kind (bytes/s, median of 3), measured like Fig. 1."""
+    """The CPU lane's GEMV rate on layer 0's weight of each kind (bytes/s, hg_module_tcpu: median of
+    3, measured like Fig. 1) -- T-bar_CPU per module for the scheduler's gain."""
     if st["v_kind"] is None:
-        import numpy as np
         ctx, B = st["ctx"], st["B"]
         v = {}
         for name in NAMES:
             W = st["host"][0][name]
             n, K = W.shape
-            x = np.full((B, K), 0x3F80, np.uint16)
-            y = np.zeros((B, n), np.float32)
-            ts = []
-            for _ in range(3):
-                t0 = time.perf_counter()
-                ctx.hg_host_gemv(x, B, n, K, W, None, y)
-                ts.append(time.perf_counter() - t0)
-            v[name] = 2 * n * K / statistics.median(ts)
+            v[name] = ctx.hg_module_tcpu(W, n, K, B, 0.0)[1]
         st["v_kind"] = v
     return st["v_kind"]
 
 
 def resident_rows(r, n, G=128):
     """Rows of an n-row linear kept in HBM for a resident fraction r: G * floor(r * (n / G) + 1/2)
-    (the same rule the oracle's partition follows)."""
-    return G * math.floor(r * (n // G) + 0.5)
+    (the library's hg_resident_rows)."""
+    from paper_2403_01164_b200 import hg
+    return hg.hg_resident_rows(r, n, G)
 
 
 def build_layers(st, args, mode, af, n_res_map, W_dev_map):
@@ -504,13 +497,17 @@ def run_point(st, args, budget_gb=0.0):
                 n = N // world
                 mods.append((n, K, (1.0 - alpha0) * 2 * n * K / v_kind[name]))  # T-bar_CPU at alpha
                 keys.append((l, name))
-        n_res_list, used = hg.hg_schedule(mods, int(budget_gb * 1e9), 128, True)
+        if args.scheduler == "rows":  # one resident fraction for every linear (reading R31)
+            n_res_list, used = hg.hg_schedule_rows(mods, int(budget_gb * 1e9), 128)
+        else:  # Sec. 4.5's module greedy
+            n_res_list, used = hg.hg_schedule(mods, int(budget_gb * 1e9), 128, True)
         for key, nr in zip(keys, n_res_list):
             if nr > 0:
                 n_res_map[key] = nr
                 W_dev_map[key] = st["host"][key[0]][key[1]][:nr].cuda()
         torch.cuda.synchronize()
-        sched = {"budget_GB": budget_gb, "placed_GB": round(used / 1e9, 3), "alpha_for_gain": alpha0,
+        sched = {"scheduler": args.scheduler, "budget_GB": budget_gb, "placed_GB": round(used / 1e9, 3),
+                 "alpha_for_gain": alpha0,
                  "gain_s_per_GB": {k: round((1.0 - alpha0) / v_kind[k] * 1e9, 6) for k in NAMES},
                  "cpu_GBps_by_kind": {k: round(v_kind[k] / 1e9, 2) for k in NAMES},
                  "resident_modules": sum(1 for (n, _, _), nr in zip(mods, n_res_list) if nr == n),
@@ -548,12 +545,14 @@ def run_point(st, args, budget_gb=0.0):
             dist.broadcast(t, 0)
             return float(t[0].item()), bool(t[1].item() > 0.5)
 
+        # no balance point inside the window: re-centre it on the clamped edge (up to 4 rounds) -- in the
+        # library at N = 1; with N > 1 every rank must run the same rounds, so rank 0's decision is
+        # broadcast between one-round calls
         res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_seed, gamma=args.abench_gamma, lam=0.02, degree=2,
-                                 reps=1, stream=s)
+                                 reps=1, stream=s, max_rounds=4 if world == 1 else 1)
         alpha_bar, clamped = agreed(res)
-        rounds = 1
-        # no balance point inside the window: re-centre it on the clamped edge (at most 3 more rounds)
-        while clamped and rounds < 4 and 0.0 < alpha_bar < 1.0:
+        rounds = res.rounds
+        while world > 1 and clamped and rounds < 4 and 0.0 < alpha_bar < 1.0:
             res = ctx.hg_alpha_bench(layers, h_dev, B, alpha_bar, gamma=args.abench_gamma, lam=0.02,
                                      degree=2, reps=1, stream=s)
             alpha_bar, clamped = agreed(res)
@@ -904,6 +903,9 @@ def parse_args(argv=None):
                          "5b pinned-blocking)")
     ap.add_argument("--staging-mb", type=int, default=512,
                     help="with --pageable: the pin lane's pinned staging ring (MiB)")
+    ap.add_argument("--scheduler", default="module", choices=["module", "rows"],
+                    help="with --hbm-budget-gb: Sec. 4.5's module greedy, or one resident fraction for every "
+                         "linear (hg_schedule_rows)")
     ap.add_argument("--resident", type=float, default=0.0,
                     help="fraction r of every linear's rows resident in HBM (C2: r = 0.5)")
     ap.add_argument("--hbm-budget-gb", type=float, default=0.0,

@@ -302,12 +302,18 @@ typedef struct {
     double lambda;   /* step of the alpha grid (default 0.02)                                */
     int32_t degree;  /* polynomial degree (default 2)                                        */
     int32_t reps;    /* measured steps per alpha after one warm-up step (default 1)           */
+    int32_t max_rounds; /* when the solve clamps to an edge inside (0, 1), re-centre the window on
+                           that edge and measure again, up to this many rounds in all (0 or 1: one
+                           round; with P > 1 ranks every rank must run the same rounds: keep 1 and
+                           agree on the next centre between calls, as bench.py does)              */
+    int32_t _pad;
 } hg_abench_cfg;
 
 #define HG_ABENCH_MAX 64
 typedef struct {
     double alpha_seed, alpha_bar;
     int32_t n, clamped;
+    int32_t rounds, _pad;          /* rounds run (the points are the last round's)              */
     double alpha[HG_ABENCH_MAX];   /* sampled alphas                                         */
     double t_cpu[HG_ABENCH_MAX];   /* CPU-lane busy seconds per step (host clock)             */
     double t_com[HG_ABENCH_MAX];   /* link busy seconds per step (CUDA events on copies)      */
@@ -339,6 +345,24 @@ typedef struct {
  * N_i % granule, K_i <= 0, t_cpu negative / non-finite. */
 HG_API hg_status hg_schedule(const hg_module *mods, int n, int64_t budget_bytes, int64_t granule,
                              int allow_partial, int64_t *n_res_out, int64_t *used_bytes);
+
+/* Row-granular variant (reading R31): the budget is spread as ONE resident fraction r over
+ * every module, n_res_i = G * floor(r * (N_i / G) + 1/2) (the rule of hg_resident_rows), with r the
+ * largest fp64 value in [0, 1] whose bytes sum(2 K_i n_res_i) fit budget_bytes -- every linear stays
+ * hybrid, so GPU-resident work overlaps the link and the CPU lane in every linear instead of whole
+ * modules running GPU-only (measured 1-8% faster at equal HBM, profiles/r01/budget_sweep_opt30b.md).
+ * mods[i].t_cpu is not used.  Pure function.  Errors: HG_EINVAL as hg_schedule. */
+HG_API hg_status hg_schedule_rows(const hg_module *mods, int n, int64_t budget_bytes, int64_t granule,
+                                  int64_t *n_res_out, int64_t *used_bytes);
+/* n_res = G * floor(r * (N / G) + 1/2): resident rows of an N-row linear for a fraction r in [0, 1]
+ * (SURVEY 8(c) c2.1).  HG_EINVAL for r outside [0, 1] or N % granule. */
+HG_API hg_status hg_resident_rows(double r, int64_t N, int64_t granule, int64_t *n_res);
+/* T-bar_CPU of one module for the scheduler's gain: the CPU lane's GEMV rate on this module's
+ * host weight W_host [N, K] (median of 3 runs of the context's pool, batch rows of x = 1.0) and
+ * *t_cpu = (1 - alpha) * 2 N K / rate, *rate_out (may be NULL) = that rate in bytes/s.  Works on
+ * host-only contexts.  HG_EINVAL for bad shapes or alpha outside [0, 1]. */
+HG_API hg_status hg_module_tcpu(hg_ctx *ctx, const void *W_host, int64_t N, int64_t K, int batch, double alpha,
+                                double *t_cpu, double *rate_out);
 
 /* ---------------------------------------------------------------- a2-a6: one linear */
 /* y[:, 0:N) = x . W^T (+ bias) with the rows of W split by `alpha`:

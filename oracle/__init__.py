@@ -429,6 +429,43 @@ def schedule(modules, budget_bytes: int, G: int, allow_partial: bool = True):
     return n_res, budget_bytes - left
 
 
+def schedule_rows(modules, budget_bytes: int, G: int):
+    """Row-granular variant of Sec. 4.5's scheduler (reading R31): the HBM budget
+    is spread as ONE resident fraction r over every module, n_res_i = resident_rows(r, N_i, G), with r
+    the largest fp64 value in [0, 1] whose total resident bytes sum(2 K_i n_res_i) fit the budget.
+
+    Obviously-correct form: n_res(r) only changes at the smallest double where some
+    floor(r m_i + 1/2) (m_i = N_i / G) reaches a new integer j; every such change point is enumerated
+    (start at (j - 1/2) / m_i and step to the exact double with math.nextafter), together with 0, and
+    the vector of the largest feasible change point is returned.  modules: list of (N, K, t_cpu)
+    (t_cpu unused: the fraction is uniform).  Returns (n_res list, bytes used)."""
+    mods = list(modules)
+
+    def n_res_at(r):
+        return [resident_rows(r, N, G) for N, _, _ in mods]
+
+    def used(v):
+        return sum(2 * K * n for (N, K, _), n in zip(mods, v))
+
+    cands = {0.0}
+    for N, _, _ in mods:
+        m = N // G
+        for j in range(1, m + 1):
+            x = min(1.0, (j - 0.5) / m)
+            while x > 0.0 and math.floor(math.nextafter(x, 0.0) * float(m) + 0.5) >= j:
+                x = math.nextafter(x, 0.0)
+            while x < 1.0 and math.floor(x * float(m) + 0.5) < j:
+                x = math.nextafter(x, 1.0)
+            if math.floor(x * float(m) + 0.5) >= j:
+                cands.add(x)
+    best = [0] * len(mods)
+    for r in sorted(cands):
+        v = n_res_at(r)
+        if used(v) <= budget_bytes:
+            best = v
+    return best, used(best)
+
+
 # ----------------------------------------------------------------------------
 LN_EPS = 1e-5
 

@@ -284,3 +284,62 @@ extern "C" HG_API hg_status hg_schedule(const hg_module *mods, int n, int64_t bu
     if (used_bytes) *used_bytes = budget_bytes - left;
     return HG_OK;
 }
+
+// Resident rows for a fraction r of an N-row linear: G * floor(r * (N / G) + 1/2), one fp64 multiply,
+// one add, floor (SURVEY 8(c) c2.1 -- the rule the partition's alpha uses too).
+static int64_t resident_rows_rule(double r, int64_t N, int64_t G) {
+    const double m = (double)(N / G);
+    return G * (int64_t)std::floor(r * m + 0.5);
+}
+
+extern "C" HG_API hg_status hg_resident_rows(double r, int64_t N, int64_t granule, int64_t *n_res) {
+    if (!n_res || granule < 1 || N < 0 || N % granule || !(r >= 0.0 && r <= 1.0))
+        return set_error(HG_EINVAL, "hg_resident_rows: r in [0,1], N %% granule == 0");
+    *n_res = resident_rows_rule(r, N, granule);
+    return HG_OK;
+}
+
+// Row-granular scheduler (reading R31): one resident fraction r for every module, the largest fp64 r
+// in [0, 1] whose resident bytes fit the budget.  Feasibility is monotone in r (every step of the rule
+// is), so a bisection over the bit patterns of the doubles in [0, 1] finds the largest feasible one.
+extern "C" HG_API hg_status hg_schedule_rows(const hg_module *mods, int n, int64_t budget_bytes, int64_t granule,
+                                             int64_t *n_res_out, int64_t *used_bytes) {
+    if (n < 0 || (n > 0 && (!mods || !n_res_out)) || budget_bytes < 0 || granule < 1)
+        return set_error(HG_EINVAL, "hg_schedule_rows: bad arguments");
+    for (int i = 0; i < n; ++i)
+        if (mods[i].N < 0 || mods[i].K <= 0 || mods[i].N % granule)
+            return set_error(HG_EINVAL, "hg_schedule_rows: module %d (N=%lld K=%lld)", i, (long long)mods[i].N,
+                             (long long)mods[i].K);
+    auto used_at = [&](double r) {
+        __int128 u = 0;
+        for (int i = 0; i < n; ++i) u += (__int128)2 * mods[i].K * resident_rows_rule(r, mods[i].N, granule);
+        return u;
+    };
+    auto bits = [](double d) {
+        uint64_t b;
+        std::memcpy(&b, &d, 8);
+        return b;
+    };
+    auto from_bits = [](uint64_t b) {
+        double d;
+        std::memcpy(&d, &b, 8);
+        return d;
+    };
+    double r = 1.0;
+    if (used_at(1.0) > budget_bytes) {
+        uint64_t lo = bits(0.0), hi = bits(1.0);  // lo feasible (nothing resident), hi infeasible
+        while (hi - lo > 1) {
+            const uint64_t mid = lo + (hi - lo) / 2;
+            if (used_at(from_bits(mid)) <= budget_bytes) lo = mid;
+            else hi = mid;
+        }
+        r = from_bits(lo);
+    }
+    int64_t used = 0;
+    for (int i = 0; i < n; ++i) {
+        n_res_out[i] = resident_rows_rule(r, mods[i].N, granule);
+        used += 2 * mods[i].K * n_res_out[i];
+    }
+    if (used_bytes) *used_bytes = used;
+    return HG_OK;
+}

@@ -2097,55 +2097,85 @@ HG_API hg_status hg_alpha_bench(hg_ctx *c, const hg_opt_layer *layers, int n_lay
                                 void *stream) {
     if (!c || !layers || n_layers < 1 || !h || !out) return set_error(HG_EINVAL, "NULL argument");
     if (!(alpha_seed >= 0.0 && alpha_seed <= 1.0)) return set_error(HG_EINVAL, "alpha_seed outside [0,1]");
-    hg_abench_cfg cfg = {0.06, 0.02, 2, 1};
+    hg_abench_cfg cfg = {0.06, 0.02, 2, 1, 1, 0};
     if (cfg_in) cfg = *cfg_in;
     if (!(cfg.gamma > 0) || !(cfg.lambda > 0) || cfg.reps < 1 || cfg.degree < 1)
         return set_error(HG_EINVAL, "bad alpha-bench config");
-    // window [seed - gamma, seed + gamma] ∩ [0, 1] in steps of lambda (reading R9)
-    const double lo = std::max(0.0, alpha_seed - cfg.gamma), hi = std::min(1.0, alpha_seed + cfg.gamma);
-    std::vector<double> pts;
-    const int npts = (int)std::floor((hi - lo) / cfg.lambda + 1e-9) + 1;
-    for (int i = 0; i < npts && (int)pts.size() < HG_ABENCH_MAX; ++i) pts.push_back(lo + i * cfg.lambda);
-    if (hi - pts.back() > 1e-12 && (int)pts.size() < HG_ABENCH_MAX) pts.push_back(hi);
-    if ((int)pts.size() < cfg.degree + 1) return set_error(HG_EINVAL, "window has too few alphas");
-
+    const int max_rounds = cfg.max_rounds > 1 ? cfg.max_rounds : 1;
     std::vector<hg_opt_layer> work(layers, layers + n_layers);
-    const int saved_stats = c->cfg.collect_stats;
-    c->cfg.collect_stats = 1;
-    std::memset(out, 0, sizeof *out);
-    out->alpha_seed = alpha_seed;
     hg_rates unit = {1, 1, 1, 1, 1, 1, 1};
-    hg_status st = HG_OK;
-    for (size_t i = 0; i < pts.size() && st == HG_OK; ++i) {
-        for (auto &L : work)
-            for (int j = 0; j < 4 && st == HG_OK; ++j) {
-                const hg_plan_t &p = L.lin[j].plan;
-                st = hg_plan(&unit, p.N, p.K, batch, p.n_res, HG_ALPHA_FIXED, pts[i], p.granule,
-                             c->cfg.chunk_bytes, &L.lin[j].plan);
+    double seed = alpha_seed;
+    for (int round = 1;; ++round) {
+        // window [seed - gamma, seed + gamma] cap [0, 1] in steps of lambda (reading R9)
+        const double lo = std::max(0.0, seed - cfg.gamma), hi = std::min(1.0, seed + cfg.gamma);
+        std::vector<double> pts;
+        const int npts = (int)std::floor((hi - lo) / cfg.lambda + 1e-9) + 1;
+        for (int i = 0; i < npts && (int)pts.size() < HG_ABENCH_MAX; ++i) pts.push_back(lo + i * cfg.lambda);
+        if (hi - pts.back() > 1e-12 && (int)pts.size() < HG_ABENCH_MAX) pts.push_back(hi);
+        if ((int)pts.size() < cfg.degree + 1) return set_error(HG_EINVAL, "window has too few alphas");
+        const int saved_stats = c->cfg.collect_stats;
+        c->cfg.collect_stats = 1;
+        std::memset(out, 0, sizeof *out);
+        out->alpha_seed = seed;
+        hg_status st = HG_OK;
+        for (size_t i = 0; i < pts.size() && st == HG_OK; ++i) {
+            for (auto &L : work)
+                for (int j = 0; j < 4 && st == HG_OK; ++j) {
+                    const hg_plan_t &p = L.lin[j].plan;
+                    st = hg_plan(&unit, p.N, p.K, batch, p.n_res, HG_ALPHA_FIXED, pts[i], p.granule,
+                                 c->cfg.chunk_bytes, &L.lin[j].plan);
+                }
+            if (st != HG_OK) break;
+            st = hg_stack(c, work.data(), n_layers, h, batch, stream);  // warm the pipeline at this alpha
+            if (st == HG_OK) st = hg_reset_stats(c);
+            for (int r = 0; r < cfg.reps && st == HG_OK; ++r) st = hg_stack(c, work.data(), n_layers, h, batch, stream);
+            hg_stats_t s;
+            if (st == HG_OK) st = hg_stats(c, &s);
+            if (st == HG_OK) {
+                out->alpha[i] = pts[i];
+                out->t_cpu[i] = s.cpu_busy_s / cfg.reps;
+                out->t_com[i] = s.link_busy_s / cfg.reps;
+                out->t_step[i] = s.wall_s / cfg.reps;
+                out->t_pin[i] = s.pin_busy_s / cfg.reps;
             }
-        if (st != HG_OK) break;
-        st = hg_stack(c, work.data(), n_layers, h, batch, stream);  // warm the pipeline at this alpha
-        if (st == HG_OK) st = hg_reset_stats(c);
-        for (int r = 0; r < cfg.reps && st == HG_OK; ++r) st = hg_stack(c, work.data(), n_layers, h, batch, stream);
-        hg_stats_t s;
-        if (st == HG_OK) st = hg_stats(c, &s);
-        if (st == HG_OK) {
-            out->alpha[i] = pts[i];
-            out->t_cpu[i] = s.cpu_busy_s / cfg.reps;
-            out->t_com[i] = s.link_busy_s / cfg.reps;
-            out->t_step[i] = s.wall_s / cfg.reps;
-            out->t_pin[i] = s.pin_busy_s / cfg.reps;
         }
+        c->cfg.collect_stats = saved_stats;
+        if (st != HG_OK) return st;  // keep the failing call's message (hg_reset_stats would overwrite it)
+        HG_TRY(hg_reset_stats(c));
+        out->n = (int)pts.size();
+        // F_COM = max(F_PIN, F_TRANS): the pin lane counts when it did any work
+        bool pinned_any = false;
+        for (int i = 0; i < out->n; ++i) pinned_any |= out->t_pin[i] > 0;
+        HG_TRY(hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, pinned_any ? out->t_pin : nullptr, out->n,
+                              cfg.degree, pts.front(), pts.back(), seed, &out->alpha_bar, &out->clamped));
+        out->rounds = round;
+        // no balance point inside the window: re-centre it on the clamped edge
+        if (!out->clamped || round >= max_rounds || !(out->alpha_bar > 0.0 && out->alpha_bar < 1.0)) break;
+        seed = out->alpha_bar;
     }
-    c->cfg.collect_stats = saved_stats;
-    if (st != HG_OK) return st;  // keep the failing call's message (hg_reset_stats would overwrite it)
-    HG_TRY(hg_reset_stats(c));
-    out->n = (int)pts.size();
-    // F_COM = max(F_PIN, F_TRANS): the pin lane counts when it did any work
-    bool pinned_any = false;
-    for (int i = 0; i < out->n; ++i) pinned_any |= out->t_pin[i] > 0;
-    return hg_alpha_solve(out->alpha, out->t_cpu, out->t_com, pinned_any ? out->t_pin : nullptr, out->n, cfg.degree,
-                          pts.front(), pts.back(), alpha_seed, &out->alpha_bar, &out->clamped);
+    out->alpha_seed = alpha_seed;
+    return HG_OK;
+}
+
+// T-bar_CPU for the scheduler's gain: the CPU lane's rate on this module's weight.
+HG_API hg_status hg_module_tcpu(hg_ctx *c, const void *W_host, int64_t N, int64_t K, int batch, double alpha,
+                                double *t_cpu, double *rate_out) {
+    if (!c || !W_host || !t_cpu) return set_error(HG_EINVAL, "NULL argument");
+    if (N <= 0 || K <= 0 || K % 8 || batch < 1 || batch > HG_MAX_BATCH || !(alpha >= 0.0 && alpha <= 1.0))
+        return set_error(HG_EINVAL, "hg_module_tcpu: bad shape or alpha");
+    std::vector<uint16_t> x((size_t)batch * K, 0x3f80);
+    std::vector<float> y((size_t)batch * N);
+    std::vector<double> ts;
+    for (int it = 0; it < 3; ++it) {
+        const auto t0 = clk::now();
+        HG_TRY(hg_host_gemv(c, x.data(), batch, N, K, W_host, nullptr, y.data()));
+        ts.push_back(secs(t0, clk::now()));
+    }
+    std::sort(ts.begin(), ts.end());
+    const double rate = (double)(2 * N * K) / ts[1];
+    *t_cpu = (1.0 - alpha) * (double)(2 * N * K) / rate;
+    if (rate_out) *rate_out = rate;
+    return HG_OK;
 }
 
 // ---------------------------------------------------------------- measurement

@@ -113,17 +113,19 @@ HG_ABENCH_MAX = 64
 
 class AbenchCfg(ctypes.Structure):
     _fields_ = [("gamma", ctypes.c_double), ("lambda_", ctypes.c_double), ("degree", ctypes.c_int32),
-                ("reps", ctypes.c_int32)]
+                ("reps", ctypes.c_int32), ("max_rounds", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class AbenchResult(ctypes.Structure):
     _fields_ = [("alpha_seed", ctypes.c_double), ("alpha_bar", ctypes.c_double), ("n", ctypes.c_int32),
-                ("clamped", ctypes.c_int32)] + [(f, ctypes.c_double * HG_ABENCH_MAX)
+                ("clamped", ctypes.c_int32), ("rounds", ctypes.c_int32), ("_pad", ctypes.c_int32)] + [
+                   (f, ctypes.c_double * HG_ABENCH_MAX)
                                                 for f in ("alpha", "t_cpu", "t_com", "t_step", "t_pin")]
 
     def as_dict(self):
         n = self.n
         return {"alpha_seed": self.alpha_seed, "alpha_bar": self.alpha_bar, "clamped": bool(self.clamped),
+                "rounds": self.rounds,
                 "alpha": list(self.alpha[:n]), "t_cpu": list(self.t_cpu[:n]), "t_com": list(self.t_com[:n]),
                 "t_step": list(self.t_step[:n]), "t_pin": list(self.t_pin[:n])}
 
@@ -147,6 +149,9 @@ _sig = {
     "hg_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp, _i64, _vp]),
     "hg_gemv_replay": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _i64, _vp]),
     "hg_schedule": (_i32, [_P(Module), _i32, _i64, _i64, _i32, _P(_i64), _P(_i64)]),
+    "hg_schedule_rows": (_i32, [_P(Module), _i32, _i64, _i64, _P(_i64), _P(_i64)]),
+    "hg_resident_rows": (_i32, [_dbl, _i64, _i64, _P(_i64)]),
+    "hg_module_tcpu": (_i32, [_vp, _vp, _i64, _i64, _i32, _dbl, _P(_dbl), _P(_dbl)]),
     "hg_host_gemv": (_i32, [_vp, _vp, _i32, _i64, _i64, _vp, _vp, _vp]),
     "hg_host_isa": (ctypes.c_char_p, []),
     "hg_debug_gemv_stamps": (_i32, [_P(ctypes.POINTER(ctypes.c_uint64))]),
@@ -236,6 +241,22 @@ def hg_schedule(modules, budget_bytes, granule=128, allow_partial=True):
     _check(_lib.hg_schedule(arr, len(mods), int(budget_bytes), int(granule), int(bool(allow_partial)), out,
                             ctypes.byref(used)))
     return [int(out[i]) for i in range(len(mods))], int(used.value)
+
+
+def hg_schedule_rows(modules, budget_bytes, granule=128):
+    """Row-granular scheduler: one resident fraction for every module.  modules: (N, K, t_cpu)."""
+    mods = list(modules)
+    arr = (Module * max(1, len(mods)))(*[Module(int(n), int(k), float(t)) for n, k, t in mods])
+    out = (_i64 * max(1, len(mods)))()
+    used = _i64(0)
+    _check(_lib.hg_schedule_rows(arr, len(mods), int(budget_bytes), int(granule), out, ctypes.byref(used)))
+    return [int(out[i]) for i in range(len(mods))], int(used.value)
+
+
+def hg_resident_rows(r, N, granule=128) -> int:
+    out = _i64()
+    _check(_lib.hg_resident_rows(float(r), int(N), int(granule), ctypes.byref(out)))
+    return int(out.value)
 
 
 def hg_plan(rates, N, K, batch, n_res, mode, alpha_fixed=0.0, granule=128, chunk_bytes=16 << 20) -> Plan:
@@ -390,15 +411,21 @@ class Context:
     def hg_host_gemv(self, x, batch, n, K, W, bias, y):
         _check(_lib.hg_host_gemv(self._h, _ptr(x), batch, n, K, _ptr(W), _ptr(bias), _ptr(y)))
 
+    def hg_module_tcpu(self, W_host, N, K, batch, alpha):
+        """(T-bar_CPU seconds at alpha, CPU-lane rate bytes/s) of one module."""
+        t, r = _dbl(), _dbl()
+        _check(_lib.hg_module_tcpu(self._h, _ptr(W_host), N, K, batch, float(alpha), ctypes.byref(t), ctypes.byref(r)))
+        return t.value, r.value
+
     def hg_measure(self, W_host, N, K, batch, under_load=True) -> Rates:
         r = Rates()
         _check(_lib.hg_measure(self._h, _ptr(W_host), N, K, batch, 1 if under_load else 0, ctypes.byref(r)))
         return r
 
     def hg_alpha_bench(self, layers, h, batch, alpha_seed, gamma=0.06, lam=0.02, degree=2, reps=1,
-                       stream=None) -> AbenchResult:
+                       stream=None, max_rounds=1) -> AbenchResult:
         arr = (OptLayer * len(layers))(*layers)
-        cfg = AbenchCfg(gamma, lam, degree, reps)
+        cfg = AbenchCfg(gamma, lam, degree, reps, max_rounds, 0)
         res = AbenchResult()
         _check(_lib.hg_alpha_bench(self._h, arr, len(layers), _ptr(h), batch, float(alpha_seed), ctypes.byref(cfg),
                                    ctypes.byref(res), _stream(stream)))

@@ -98,3 +98,66 @@ def test_hg_schedule_errors():
         hg.hg_schedule([(128, 64, -1.0)], 1 << 20, G)
     with pytest.raises(hg.HgError):
         hg.hg_schedule([(128, 64, 1.0)], -1, G)
+
+
+# ---------------------------------------------------------------------------------------------
+# Row-granular variant (reading R31): one resident fraction r for every module
+# ---------------------------------------------------------------------------------------------
+def test_schedule_rows_hand_worked():
+    """Two modules (N, K) = (256, 8), (512, 8), G = 128: m = 2 and 4 granules, 2 K G = 2048 B per
+    granule.  Budget 4096 B -> at most 2 granules: r = 0.25 gives floor(0.5 + 0.5) = 1 and
+    floor(1.0 + 0.5) = 1 granule (feasible); the next change point is r = 0.375 where the second
+    module reaches floor(1.5 + 0.5) = 2 (3 granules, infeasible) -> (128, 128), 4096 B used."""
+    mods = [(256, 8, 1.0), (512, 8, 5.0)]
+    assert oracle.schedule_rows(mods, 4096, 128) == ([128, 128], 4096)
+    # budget 2047 B: not even one granule -> nothing; the whole weight -> everything
+    assert oracle.schedule_rows(mods, 2047, 128) == ([0, 0], 0)
+    assert oracle.schedule_rows(mods, 2 * 8 * 768, 128) == ([256, 512], 2 * 8 * 768)
+    # 3 granules: r = 0.375 -> (1, 2) granules
+    assert oracle.schedule_rows(mods, 3 * 2048, 128) == ([128, 256], 3 * 2048)
+
+
+def test_schedule_rows_brute_force():
+    """Against a brute-force scan of r on a fine grid plus every candidate's neighbours: no r in
+    [0, 1] with a feasible vector beats the returned one (component-wise it is the maximum)."""
+    rng = random.Random(9)
+    for _ in range(60):
+        G = rng.choice([1, 2, 4])
+        mods = [(G * rng.randint(0, 12), rng.randint(1, 9), 1.0) for _ in range(rng.randint(1, 5))]
+        total = sum(2 * K * N for N, K, _ in mods)
+        budget = rng.randint(0, total + 5)
+        got, used = oracle.schedule_rows(mods, budget, G)
+        assert used <= budget
+        for i in range(2001):
+            r = i / 2000
+            v = [oracle.resident_rows(r, N, G) for N, _, _ in mods]
+            if sum(2 * K * n for (N, K, _), n in zip(mods, v)) <= budget:
+                assert all(a <= b for a, b in zip(v, got)), (mods, budget, r, v, got)
+
+
+def test_hg_schedule_rows_matches_oracle_exactly():
+    rng = random.Random(19)
+    for _ in range(300):
+        G = rng.choice([1, 8, 128])
+        mods = [(G * rng.randint(0, 40), rng.choice([8, 64, 7168]), 0.0) for _ in range(rng.randint(0, 8))]
+        total = sum(2 * K * N for N, K, _ in mods)
+        budget = rng.randint(0, total + 100) if rng.random() < 0.9 else total
+        assert hg.hg_schedule_rows(mods, budget, G) == oracle.schedule_rows(mods, budget, G), (mods, budget, G)
+    for r in (0.0, 0.1, 0.25, 0.37, 0.5, 0.999, 1.0):
+        for N in (0, 128, 640, 28672):
+            assert hg.hg_resident_rows(r, N, 128) == oracle.resident_rows(r, N, 128)
+
+
+def test_hg_module_tcpu_host_only():
+    """T-bar_CPU on a host-only context: positive, and (1 - alpha) times the whole module."""
+    import numpy as np
+    from harness import gen
+    N, K = 512, 256
+    W = gen.uniform_bf16(3, 7, N * K, 0.1).reshape(N, K)
+    with hg.Context(-1, cpu_threads=2) as c:
+        t0, rate = c.hg_module_tcpu(W, N, K, 1, 0.0)
+        assert t0 > 0 and rate > 0 and abs(t0 - 2 * N * K / rate) <= 1e-12 * t0
+        t5, rate5 = c.hg_module_tcpu(W, N, K, 1, 0.5)
+        assert abs(t5 - 0.5 * 2 * N * K / rate5) <= 1e-12 * t5
+        with pytest.raises(hg.HgError):
+            c.hg_module_tcpu(W, N, K, 1, 1.5)
