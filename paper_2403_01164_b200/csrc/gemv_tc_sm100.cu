@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __gri
                     for (int b = 0; b < B; ++b) sum[b] = __ldcg(&a.ws[((int64_t)(pe - 1) * B + b) * a.n_total + g]);
                     // kFold slices x B loads issued unconditionally (indices clamped to the last slice, which
                     // is always written), then added in slice order: no load waits behind a branch
-                    constexpr int kFold = B <= 4 ? 8 : 4;
+                    constexpr int kFold = 8;
                     for (int q0 = pe; q0 < S; q0 += kFold) {
                         float part[kFold][B];
 #pragma unroll

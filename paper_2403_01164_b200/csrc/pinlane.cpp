@@ -80,7 +80,7 @@ struct PinLane {
             if (!error && j.tag > (uint32_t)nslots) {
                 const uint32_t need = j.tag - (uint32_t)nslots;
                 const auto t0 = std::chrono::steady_clock::now();
-                for (int spin = 0; (int32_t)(freed[j.slot] - need) < 0; ++spin) {
+                for (int spin = 0; (int32_t)(__atomic_load_n(&freed[j.slot], __ATOMIC_ACQUIRE) - need) < 0; ++spin) {
                     _mm_pause();
                     if ((spin & 4095) == 4095) {
                         std::this_thread::yield();
@@ -96,8 +96,9 @@ struct PinLane {
                 CopyPart cp{j.src, staging + (int64_t)j.slot * slot_bytes, j.bytes, threads};
                 pool_run(pool, copy_part, &cp);
             }
-            std::atomic_thread_fence(std::memory_order_release);
-            pinned[j.slot] = j.tag;
+            // the memcpy pool's writes happen-before the join; the release store publishes them to the
+            // copy stream (device memops on mapped memory) or any host reader (tools/tsan)
+            __atomic_store_n(&pinned[j.slot], j.tag, __ATOMIC_RELEASE);
             _mm_sfence();
             busy_ns += std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t1).count();
             bytes += j.bytes;

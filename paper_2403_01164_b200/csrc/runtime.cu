@@ -571,7 +571,8 @@ hg_status issue_copy(hg_ctx *c, const ChunkReq &r, bool bound = false) {
             if (ps >= c->nstage) {
                 const uint32_t need = (uint32_t)(ps - c->nstage + 1);
                 const auto t0 = clk::now();
-                for (int spin = 0; (int32_t)(((volatile uint32_t *)c->pinflags)[c->nstage + pslot] - need) < 0; ++spin) {
+                for (int spin = 0; (int32_t)(__atomic_load_n(&c->pinflags[c->nstage + pslot], __ATOMIC_ACQUIRE) - need) < 0;
+                     ++spin) {
                     _mm_pause();
                     if ((spin & 4095) == 4095 && secs(t0, clk::now()) > c->cfg.timeout_s) {
                         c->error = true;
