@@ -285,10 +285,10 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
 
 def ncu_traffic():
     """DRAM traffic per launch of the dominant kernel from the committed `ncu --set full` capture
-    of the same launch configuration (profiles/r01/ncu_gemv_replay_traffic.json): mean over the
+    of the same launch configuration (profiles/r02/ncu_gemv_replay_traffic.json): mean over the
     four linears of dram__bytes_read.sum + dram__bytes_write.sum, beside their algorithmic bytes."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01", "ncu_gemv_replay_traffic.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r02", "ncu_gemv_replay_traffic.json")))
     except Exception:
         return None, None
     per = d["per_launch"]

@@ -398,6 +398,9 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
                     }
                 }
             }
+            // the stage is refilled by the async proxy (TMA bulk copy) once the producer sees this
+            // arrival: order this lane's generic-proxy reads of it before that write (WAR across proxies)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(empty0 + 8 * st);
             // butterfly: every lane then holds every part sum (static indices keep acc in registers)

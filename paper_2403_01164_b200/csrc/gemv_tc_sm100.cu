@@ -195,7 +195,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 __device__ __forceinline__ int64_t cta_of(int64_t u, int64_t U, int64_t G) { return ((u + 1) * G - 1) / U; }
 
 template <int B, int ST>
-__global__ void __launch_bounds__(kThreads, 1) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) gemv_tc_stream_kernel(const __grid_constant__ TcArgs a) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
