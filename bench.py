@@ -62,8 +62,16 @@ def set_model(name):
 
 
 def env_rank():
-    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(
-        os.environ.get("LOCAL_RANK", "0"))
+    """(rank, world, local device).  HG_BENCH_ONE_GPU=1 (functional check of the N > 1 flow on a one-GPU
+    box: every rank on device 0, gloo for the process group; timings meaningless) maps every rank to
+    device 0."""
+    local = 0 if os.environ.get("HG_BENCH_ONE_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), local
+
+
+def coll_device():
+    """Device of the small tensors the bench's collectives carry (gloo: CPU)."""
+    return "cpu" if os.environ.get("HG_BENCH_ONE_GPU") == "1" else "cuda"
 
 
 def peaks():
@@ -401,7 +409,10 @@ def prepare(args, weights=None, **ctx_extra):
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
     if world > 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("HG_BENCH_ONE_GPU") == "1":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     ctx, threads = make_context(args, rank, world, local, **ctx_extra)
     if world > 1 and args.exchange == "peer":
         # a8 over peer memory (peer.cu): device boxes opened by CUDA IPC over NVLink, one host segment
@@ -533,7 +544,7 @@ def run_point(st, args, budget_gb=0.0):
     any_host = any(p.n_res < p.N for p in all_plans)
     if args.alpha is None and args.abench and any_host:
         if world > 1:  # every rank must sample the same alpha grid (the stack all-gathers)
-            t = torch.tensor([alpha_seed], dtype=torch.float64, device="cuda")
+            t = torch.tensor([alpha_seed], dtype=torch.float64, device=coll_device())
             dist.broadcast(t, 0)
             alpha_seed = float(t.item())
         def agreed(r):
@@ -541,7 +552,7 @@ def run_point(st, args, budget_gb=0.0):
             # round runs the stack, whose all-gathers need every rank): take rank 0's decision
             if world == 1:
                 return r.alpha_bar, bool(r.clamped)
-            t = torch.tensor([r.alpha_bar, 1.0 if r.clamped else 0.0], dtype=torch.float64, device="cuda")
+            t = torch.tensor([r.alpha_bar, 1.0 if r.clamped else 0.0], dtype=torch.float64, device=coll_device())
             dist.broadcast(t, 0)
             return float(t[0].item()), bool(t[1].item() > 0.5)
 
@@ -649,7 +660,7 @@ def run_point(st, args, budget_gb=0.0):
     rates_post = ctx.hg_measure(st["host"][0]["fc1"], st["host"][0]["fc1"].shape[0], H, B, under_load=True)
     rdp = rates_post.as_dict()
 
-    times = torch.tensor([dev_s, e2e_s, wall], device="cuda")
+    times = torch.tensor([dev_s, e2e_s, wall], device=coll_device())
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     dev_s, e2e_s, wall = times.tolist()
