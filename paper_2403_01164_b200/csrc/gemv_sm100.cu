@@ -25,8 +25,8 @@
 // Work split (depends on K and B only, never on the partition, so every row -- resident or
 // streamed, any alpha, any chunking -- is reduced identically; SURVEY 8(c) c4 split invariance):
 //   * K is cut into P parts of equal length len (multiple of 8, <= 8192 elements for B = 1,
-//     <= 4096 for B >= 3); CTA (p, j) handles part p of rows [j*R/gp, (j+1)*R/gp) of every
-//     source (resident block, then chunk 0, 1, ...), gp = #CTAs per part;
+//     <= 4096 for B >= 3); CTA (p, j) handles part p of the row groups dealt to it round-robin
+//     over all sources (resident block, then chunk 0, 1, ...; see first_group), gp = #CTAs per part;
 //   * a part sum: lane l accumulates 16-byte vectors l, l+32, l+64, ... in ascending order
 //     (8 fmaf each, k ascending), then a butterfly over the 32 lanes;
 //   * y = (((S_0 + S_1) + ...) + S_{P-1}) + bias: for P > 1 the part sums are stored to a
@@ -134,6 +134,23 @@ __device__ __forceinline__ Src source(const SArgs &a, int64_t s) {
         r.flagged = a.arrived != nullptr;
     }
     return r;
+}
+
+// Row groups (R rows each) of all the launch's sources, in source order, are dealt to the gp CTAs of a
+// K-part round-robin: CTA j takes the groups g of source s with (gbase(s) + g) % gp == j, gbase(s) =
+// the groups of the sources before s.  Every CTA gets the same number of groups to within one for the
+// whole launch (a per-source split left up to one extra row per source on some CTAs: 14 vs 11.8 rows
+// on qkv's three chunks), and every chunk still spreads over every CTA as it lands.
+__device__ __forceinline__ int64_t groups_of(int64_t rows, int R) { return (rows + R - 1) / R; }
+__device__ __forceinline__ int64_t group_base(const SArgs &a, int64_t s, int R) {
+    if (s == -2) return 0;
+    const int64_t b = groups_of(a.n_res, R);
+    if (s == -1) return b;
+    return b + groups_of(a.W_dir ? a.n_dir : 0, R) + s * groups_of(a.chunk_rows, R);
+}
+__device__ __forceinline__ int64_t first_group(const SArgs &a, int64_t s, int R, int j) {
+    const int64_t m = ((int64_t)j - group_base(a, s, R)) % a.gp;
+    return m < 0 ? m + a.gp : m;
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -322,14 +339,15 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
         for (int64_t s = s_begin; s < a.n_chunks; ++s) {
             const Src src = source(a, s);
             if (src.flagged) wait_arrival(src);
-            const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
-            for (int64_t r = ra; r < rb; r += R) {
+            const int64_t ng = groups_of(src.rows, R);
+            for (int64_t gi = first_group(a, s, R, j); gi < ng; gi += a.gp) {
+                const int64_t r = gi * R;
                 const int st = (int)(issued % S);
                 if (issued >= S) {
                     consume_upto(issued - S);
                     flush();
                 }
-                const int nrows = rb - r < R ? (int)(rb - r) : R;
+                const int nrows = src.rows - r < R ? (int)(src.rows - r) : R;
                 const uint32_t fb = full0 + 8 * st;
                 mbar_expect_tx(fb, (uint32_t)nrows * bytes_p);
                 const uint8_t *g = src.base + (r * a.K + k0) * 2;
@@ -362,11 +380,12 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     int64_t it = 0;
     for (int64_t s = s_begin; s < a.n_chunks; ++s) {
         const Src src = source(a, s);
-        const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
-        for (int64_t r = ra; r < rb; r += R, ++it) {
+        const int64_t ng = groups_of(src.rows, R);
+        for (int64_t gi = first_group(a, s, R, j); gi < ng; gi += a.gp, ++it) {
             if ((int)(it % kConsumerWarps) != warp) continue;
+            const int64_t r = gi * R;
             const int st = (int)(it % S);
-            const int nrows = rb - r < R ? (int)(rb - r) : R;
+            const int nrows = src.rows - r < R ? (int)(src.rows - r) : R;
             mbar_wait(full0 + 8 * st, (uint32_t)((it / S) & 1));
             if (a.stamps && it == 0 && lane == 0) a.stamps[blockIdx.x * 4 + 1] = globaltimer();
             const uint4 *sw = (const uint4 *)(stages + (int64_t)st * R * unit_bytes);
@@ -451,9 +470,12 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
     if (!s_last) return;
     for (int64_t s = s_begin; s < a.n_chunks; ++s) {
         const Src src = source(a, s);
-        const int64_t ra = (int64_t)j * src.rows / a.gp, rb = (int64_t)(j + 1) * src.rows / a.gp;
-        for (int64_t i = threadIdx.x; i < (rb - ra) * B; i += kConsumerThreads) {
-            const int64_t g = src.g0 + ra + i / B;
+        const int64_t ng = groups_of(src.rows, R), g_first = first_group(a, s, R, j);
+        const int64_t mine = g_first < ng ? (ng - g_first + a.gp - 1) / a.gp : 0;  // this CTA's groups
+        for (int64_t i = threadIdx.x; i < mine * R * B; i += kConsumerThreads) {
+            const int64_t row = (g_first + (i / (R * B)) * a.gp) * R + (i / B) % R;
+            if (row >= src.rows) continue;
+            const int64_t g = src.g0 + row;
             const int b = (int)(i % B);
             const float *w = a.ws + g * a.P * B + b;
             float sum = 0.f;
