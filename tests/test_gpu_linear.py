@@ -317,10 +317,15 @@ def test_pageable_weights_pin_lane(B, stage_mb, strategy):
         for n_res, alpha in ((0, 0.7), (512, 1.0)):
             Wd = dev(W[:n_res]) if n_res else None
             y_pg = torch.full((B, N), float("nan"), device="cuda")
-            cp.hg_linear(dev(x), B, N, K, Wd, n_res, _pageable(W[n_res:]), alpha, dev_f32(b), y_pg)
+            # the caller keeps every buffer alive until the stream has passed the call (hg.h): the
+            # pageable rows are copied asynchronously by the pin lane / naive transfer thread
+            W_pg = _pageable(W[n_res:])
+            cp.hg_linear(dev(x), B, N, K, Wd, n_res, W_pg, alpha, dev_f32(b), y_pg)
             y_pin = torch.full((B, N), float("nan"), device="cuda")
-            cq.hg_linear(dev(x), B, N, K, Wd, n_res, pinned(W[n_res:]), alpha, dev_f32(b), y_pin)
+            W_pin = pinned(W[n_res:])
+            cq.hg_linear(dev(x), B, N, K, Wd, n_res, W_pin, alpha, dev_f32(b), y_pin)
             torch.cuda.synchronize()
+            del W_pg, W_pin
             assert np.array_equal(y_pg.cpu().numpy(), y_pin.cpu().numpy()), (n_res, alpha)
             assert oracle.within_tol(y_pg.cpu().numpy(), oracle.linear(x, W, b))[0]
         s = cp.hg_stats()
