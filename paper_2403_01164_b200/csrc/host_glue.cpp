@@ -88,15 +88,16 @@ void layernorm_row(const float *v, int64_t H, const float *g, const float *b, ui
     }
     const float var = block_sum(part) / (float)H;
     const float rstd = 1.0f / std::sqrt(var + kLnEps);
+    // one straight loop per parameter combination (a per-element `if (g)` kept the loop scalar:
+    // ~15 us per 7168-element row against ~1 us vectorised); the same operations in each
     if (g && b) {
         for (int64_t i = 0; i < H; ++i) out[i] = f2bf(((v[i] - mean) * rstd) * g[i] + b[i]);
+    } else if (g) {
+        for (int64_t i = 0; i < H; ++i) out[i] = f2bf(((v[i] - mean) * rstd) * g[i]);
+    } else if (b) {
+        for (int64_t i = 0; i < H; ++i) out[i] = f2bf(((v[i] - mean) * rstd) + b[i]);
     } else {
-        for (int64_t i = 0; i < H; ++i) {
-            float x = (v[i] - mean) * rstd;
-            if (g) x = x * g[i];
-            if (b) x = x + b[i];
-            out[i] = f2bf(x);
-        }
+        for (int64_t i = 0; i < H; ++i) out[i] = f2bf((v[i] - mean) * rstd);
     }
 }
 
@@ -108,19 +109,21 @@ bool hglue_supported() { return __builtin_cpu_supports("avx2") && __builtin_cpu_
 
 void hglue_layernorm(const uint16_t *h, int64_t H, int batch, const float *g, const float *b, uint16_t *out) {
     t_row.resize((size_t)H);
+    float *row = t_row.data();  // (hoisted: a thread_local vector indexed in the loop blocks vectorisation)
     for (int r = 0; r < batch; ++r) {
-        for (int64_t i = 0; i < H; ++i) t_row[i] = bf2f(h[r * H + i]);
-        layernorm_row(t_row.data(), H, g, b, out + r * H);
+        for (int64_t i = 0; i < H; ++i) row[i] = bf2f(h[r * H + i]);
+        layernorm_row(row, H, g, b, out + r * H);
     }
 }
 
 void hglue_residual_ln(const uint16_t *h, const float *y, int64_t ldy, int64_t H, int batch, uint16_t *h1,
                        const float *g, const float *b, uint16_t *a2) {
     t_row.resize((size_t)H);
+    float *row = t_row.data();
     for (int r = 0; r < batch; ++r) {
         for (int64_t i = 0; i < H; ++i) h1[r * H + i] = f2bf(bf2f(h[r * H + i]) + y[r * ldy + i]);
-        for (int64_t i = 0; i < H; ++i) t_row[i] = bf2f(h1[r * H + i]);
-        layernorm_row(t_row.data(), H, g, b, a2 + r * H);
+        for (int64_t i = 0; i < H; ++i) row[i] = bf2f(h1[r * H + i]);
+        layernorm_row(row, H, g, b, a2 + r * H);
     }
 }
 

@@ -2355,6 +2355,8 @@ HG_API hg_status hg_measure(hg_ctx *c, const void *W_host, int64_t N, int64_t K,
                 out->b_host = std::max(out->b_host, ((double)cpu_bytes + (double)(n1 - n0) * chunk) / dt);
         }
     }
+    // the solo CPU probes below must not share host DRAM with the joint probe's remaining DMA
+    HG_CK(c, cudaStreamSynchronize(c->copy));
     std::vector<double> tg, tr;
     for (int it = 0; it < 9; ++it) {
         flush_llc();
