@@ -169,6 +169,8 @@ struct TcArgs {
     uint32_t tag[kMaxSrc];
     int n_src;
     int S;
+    int cluster;     // 1: one unit per CTA, a tile's S slices are one thread-block cluster and its
+                     // slice partials are added through distributed shared memory (no workspace)
     int64_t ks, K, n_total, U;
     const float *bias;
     float *y;
@@ -191,6 +193,22 @@ __device__ __forceinline__ unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t dsmem_addr(uint32_t local_addr, uint32_t rank) {
+    uint32_t remote;
+    asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+    return remote;
+}
+// no memory clobber: the loads of one fold are independent and may all be in flight at once (they
+// are ordered after the cluster barrier, which clobbers memory)
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t remote) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+    return v;
+}
+
 // the CTA whose range [c U / G, (c+1) U / G) holds unit u
 __device__ __forceinline__ int64_t cta_of(int64_t u, int64_t U, int64_t G) { return ((u + 1) * G - 1) / U; }
 
@@ -393,6 +411,13 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_tc_stream_kernel(const __gri
             const int64_t lrow = (t - a.tile0[i]) * kTileM + quarter * 32 + lane;
             const bool valid = lrow < a.rows[i];
             const int64_t g = a.g0[i] + lrow;
+            if (a.cluster) {  // the tile's fold happens through DSMEM after the loop (one unit per CTA)
+                float *red = (float *)gbase;  // stage 0's W tile: free once this unit's MMAs completed
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // (last written by TMA)
+#pragma unroll
+                for (int b = 0; b < B; ++b) red[b * kTileM + quarter * 32 + lane] = __uint_as_float(p[b]);
+                continue;
+            }
             const bool first = u == u0 || s == 0;      // this CTA's first unit of tile t
             const bool last = u == u1 - 1 || s == S - 1;  // ... and its last
             if (first) prefix = s == 0;
@@ -462,6 +487,41 @@ __global__ void __launch_bounds__(kThreads, 2) gemv_tc_stream_kernel(const __gri
             named_barrier(1, 128);
         }
     }
+    if (a.cluster) {
+        // cluster rank r holds slice r of tile blockIdx.x / S: rank 0 adds the S partials in slice order
+        // (the same left-to-right sum as the register / workspace paths) once every rank stored its own
+        __syncwarp();
+        cluster_sync_all();
+        if (warp >= 2 && (blockIdx.x % S) == 0) {
+            const int quarter = warp & 3;
+            const int64_t t = blockIdx.x / S;
+            const int i = src_of(t);
+            const int64_t lrow = (t - a.tile0[i]) * kTileM + quarter * 32 + lane;
+            if (lrow < a.rows[i]) {
+                const int64_t g = a.g0[i] + lrow;
+                const float bb = a.bias ? a.bias[g] : 0.f;
+                const uint32_t red = smem_u32(gbase) + (uint32_t)(quarter * 32 + lane) * 4;
+                float part[kSliceMaxCount][B];
+#pragma unroll
+                for (int r = 0; r < kSliceMaxCount; ++r)
+                    if (r < S) {
+                        const uint32_t base = dsmem_addr(red, (uint32_t)r);
+#pragma unroll
+                        for (int b = 0; b < B; ++b) part[r][b] = ld_dsmem_f32(base + (uint32_t)(b * kTileM) * 4);
+                    }
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    float sum = part[0][b];
+#pragma unroll
+                    for (int r = 1; r < kSliceMaxCount; ++r)
+                        if (r < S) sum += part[r][b];
+                    a.y[b * a.ldy + g] = sum + bb;
+                }
+            }
+        }
+        __syncwarp();
+        cluster_sync_all();  // every rank's shared memory stays valid until rank 0 has read it
+    }
     if (a.stamps && warp == 2 && lane == 0) a.stamps[blockIdx.x * 8 + 5] = gtimer();
     tc_fence_before();
     __syncthreads();
@@ -516,11 +576,19 @@ int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem_for(kStagesWide);
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    int na = 1;
+    if (a.cluster) {  // grid = U = tiles x S, one cluster of S CTAs per tile
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = (unsigned)a.S;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide>, a);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
@@ -528,13 +596,18 @@ int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
 
 template <int B>
 int prepare_tc_b() {
-    return (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
+    int e = (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_for(kStagesWide));
+    // clusters of up to 16 CTAs (one per k-slice of a tile): above the portable 8
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
+                                   cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    return e;
 }
 
 }  // namespace
 
 int64_t g_slice_min = kSliceMin;       // A/B (HG_TC_SLICE_MIN): smallest k per work unit
+int g_tc_cluster = 1;                  // A/B (HG_TC_CLUSTER=0): workspace fold for every split tile
 int g_slice_count = kSliceMaxCount;    // A/B (HG_TC_SLICE_COUNT): most slices per row
 
 // k-slice geometry: a function of K only (split invariance): slices of ks = 64 * max(min/64,
@@ -557,6 +630,7 @@ int gemv_tc_prepare() {
         const int64_t sl = atoll(v) / kTileK * kTileK;
         if (sl >= kTileK) g_slice_min = sl;
     }
+    if (const char *v = getenv("HG_TC_CLUSTER")) g_tc_cluster = atoi(v) != 0;
     if (const char *v = getenv("HG_TC_SLICE_COUNT")) {
         const int c = atoi(v);
         if (c >= 1 && c <= 256) g_slice_count = c;
@@ -631,6 +705,10 @@ int launch_gemv_tc_stream(const StreamLaunch &L, int *counters, void *stream) {
     a.ks = g.ks;
     a.K = K;
     a.U = a.tile0[ns] * a.S;
+    // few units (at most two per SM): one unit per CTA and a tile's slices as one cluster, folded
+    // through distributed shared memory instead of the workspace + counter round trip
+    const int sms = g_num_sms > 0 ? g_num_sms : 148;
+    a.cluster = (g_tc_cluster && a.S > 1 && a.S <= kSliceMaxCount && a.U <= 2 * sms) ? 1 : 0;
     a.n_total = L.n_res + L.n_str;
     a.bias = L.bias;
     a.y = L.y;
