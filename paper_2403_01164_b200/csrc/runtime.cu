@@ -1158,20 +1158,28 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
 }
 
 // ---------------------------------------------------------------- mirrored glue (reading R24)
+//
+// At P > 1 every rank must take the same decision: the mirrored ranks publish their rows of every
+// linear into the shared host segment and wait for everybody else's, so one rank on the plain path
+// would leave the others waiting.  The decision then depends only on what all ranks pass alike (the
+// configuration and which host copies the descriptors carry), not on this rank's own plans: a rank
+// whose shards have no CPU rows still mirrors (it publishes its GPU rows and keeps its host copy of
+// the residual stream up to date).
 bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n) {
     // P > 1 mirrors only through the peer group's shared host segment (not with NCCL)
-    if (!c->cfg.mirror_glue || (nranks_of(c) != 1 && !c->peer) || !hglue_supported()) return false;
+    const bool multi = nranks_of(c) != 1;
+    if (!c->cfg.mirror_glue || (multi && !c->peer) || !hglue_supported()) return false;
     bool any_cpu = false;  // without CPU rows nobody needs the glue on the host
     for (int l = 0; l < n; ++l)
         for (int i = 0; i < 4; ++i) any_cpu |= layers[l].lin[i].plan.n_cpu > 0;
-    if (!any_cpu) return false;
+    if (!any_cpu && !multi) return false;
     for (int l = 0; l < n; ++l) {
         const hg_opt_layer &L = layers[l];
         if ((L.ln1_g && !L.ln1_g_host) || (L.ln1_b && !L.ln1_b_host) || (L.ln2_g && !L.ln2_g_host) ||
             (L.ln2_b && !L.ln2_b_host))
             return false;
         for (int i = 0; i < 4; ++i)
-            if (L.lin[i].bias && !L.lin[i].bias_host && L.lin[i].plan.n_cpu > 0) return false;
+            if (L.lin[i].bias && !L.lin[i].bias_host && (multi || L.lin[i].plan.n_cpu > 0)) return false;
     }
     return true;
 }
@@ -1447,8 +1455,14 @@ hg_status run_stack_mirror(hg_ctx *c, const hg_opt_layer *layers, int nl, void *
             c->st.gpu_launches++;
         }
     }
-    // every rank may be waiting on this rank's last rows: publish them before returning
-    if (Pn > 1) HG_TRY(publish_upto(total - 1, true));
+    // every rank may be waiting on this rank's last rows: publish them before returning; and this rank
+    // reads none of this call's host slots any more (the next call starts from the device's h), so it
+    // releases them all -- the last linear's y is read by nobody, and a rank whose shards have no CPU
+    // rows has read only the slots its ring forced it to catch up on
+    if (Pn > 1) {
+        HG_TRY(publish_upto(total - 1, true));
+        peer_host_consumed(g, hk0 + total - 1);
+    }
     // the d2h stream must not run past this call's buffers unseen: order it before the caller's next work
     HG_CK(c, cudaEventRecord(c->ev_x, c->d2h));
     HG_CK(c, cudaStreamWaitEvent(s, c->ev_x, 0));

@@ -53,7 +53,7 @@ def main():
             dist.all_gather_object(blobs, c.hg_peer_export(P, p))
             c.hg_peer_open(blobs)
             keep = []
-            layers = [shard_layer(c, H, F, B, l, P, p, 0.35 + 0.1 * p, keep, seed) for l in range(NL)]
+            layers = [shard_layer(c, H, F, B, l, P, p, (0.35 + 0.1 * p) % 1.0, keep, seed) for l in range(NL)]
             h0 = gen.uniform_bf16(seed + 1, 989, B * H, 1.0).reshape(B, H)
             hs = [dev(h0) for _ in range(2)]
             st.synchronize()

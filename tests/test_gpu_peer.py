@@ -71,7 +71,7 @@ def make_ctx(P, rank, exchange, **kw):
     return c
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 @pytest.mark.parametrize("B", [1, 3])
 def test_peer_linear_sharded(P, B):
     N, K = 4096, 1024
@@ -83,7 +83,7 @@ def test_peer_linear_sharded(P, B):
         try:
             r0, r1 = oracle.shard(N, P, p, 128)
             n_res = 128 * p % (r1 - r0)  # different residency per rank
-            plan = c.plan(hg.make_rates(1, 1, 1), r1 - r0, K, B, n_res, hg.FIXED, 0.3 + 0.2 * p)
+            plan = c.plan(hg.make_rates(1, 1, 1), r1 - r0, K, B, n_res, hg.FIXED, (0.3 + 0.2 * p) % 1.0)
             Wd = dev(W[r0:r0 + n_res]) if n_res else None
             Wh = pinned(W[r0 + n_res:r1])
             xd, bd = dev(x), dev_f32(b[r0:r1])
@@ -134,26 +134,32 @@ def run_procs(P, tmp_path, **env):
         except subprocess.TimeoutExpired:
             pr.kill()
             logs.append(pr.communicate()[0])
-    for pr, log in zip(procs, logs):
-        assert pr.returncode == 0, log[-3000:]
+    bad = [f"--- rank {p} rc={pr.returncode}\n{log[-1500:]}" for p, (pr, log) in enumerate(zip(procs, logs))
+           if pr.returncode != 0]
+    assert not bad, "\n".join(bad)
     return [np.load(o) for o in outs]
 
 
-@pytest.mark.parametrize("P,B", [(2, 1), (2, 4), (4, 2)])
+@pytest.mark.parametrize("P,B", [(2, 1), (2, 4), (4, 2), (8, 1)])
 def test_peer_stack_mirrored_processes(P, B, tmp_path):
     """Ranks as processes: peer blobs all-gathered over gloo, device boxes opened by CUDA IPC, the host
     segment by name (the bench's multi-GPU path).  Every rank ends with the same bits, twice; the
     mirrored glue ran on every linear with 0 mismatches (verify_mirror) and gives the same bits as the
     GPU-only glue at the same P; and the output stays within tolerance of the fp64 oracle."""
-    H, F, NL, seed = 512, 2048, 3, 71
+    H, F, NL, seed = (1024, 4096, 2, 71) if P == 8 else (512, 2048, 3, 71)  # N/P a multiple of 128
     res = run_procs(P, tmp_path, H=H, F=F, NL=NL, B=B, SEED=seed)
     ref = res[0]["m1_0"]
     for r in res:
         assert np.array_equal(r["m1_0"], ref) and np.array_equal(r["m1_1"], ref)
         assert np.array_equal(r["m0_0"], ref) and np.array_equal(r["m0_1"], ref)
         ml, mm, nlin, with_cpu = r["m1_stats"]
-        assert with_cpu > 0 and ml == 2 * with_cpu and mm == 0, (ml, mm, with_cpu)
+        assert ml == 2 * with_cpu and mm == 0, (ml, mm, with_cpu)
         assert r["m0_stats"][0] == 0
+    # at P = 8 (alpha 0.95 on rank 6) one rank's shards have no CPU rows at all: it still takes the
+    # mirrored path with the others (can_mirror decides alike on every rank)
+    assert any(r["m1_stats"][3] > 0 for r in res)
+    if P == 8:
+        assert any(r["m1_stats"][3] == 0 for r in res)
     shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
     h = gen.uniform_bf16(seed + 1, 989, B * H, 1.0).reshape(B, H)
     for l in range(NL):
