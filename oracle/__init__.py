@@ -220,6 +220,74 @@ def gather_shards(shard_outputs, B: int):
 
 
 # ----------------------------------------------------------------------------
+# Megatron pairing (not in the paper, which runs one GPU; DESIGN.md
+# reading R32): QKV and fc1 column-parallel with no exchange, O and fc2 row-parallel (each rank holds
+# the K columns matching its share of the previous linear's outputs) followed by one all-reduce.
+# ----------------------------------------------------------------------------
+def megatron_qkv_rows(H: int, P: int, p: int, G: int) -> np.ndarray:
+    """Rows of the fused QKV weight [3H, H] rank p holds: its heads' rows of q, of k and of v, in that
+    order -- [pH/P, (p+1)H/P) + {0, H, 2H} (so the V slice of its output feeds its O columns)."""
+    r0, r1 = shard(H, P, p, G)
+    return np.concatenate([np.arange(r0, r1) + off for off in (0, H, 2 * H)])
+
+
+def shard_k(K: int, P: int, p: int, G: int):
+    """Rank p of a row-parallel linear holds input columns [pK/P, (p+1)K/P) of W [N, K]."""
+    return shard(K, P, p, G)
+
+
+def linear_rowpar(x_parts, W_parts, bias=None) -> np.ndarray:
+    """Row-parallel linear: rank p's partial x_p . W_p^T over its K columns (fp64, `linear`), the
+    partials summed in rank order (the all-reduce), the bias added once after the sum."""
+    y = None
+    for xp, Wp in zip(x_parts, W_parts):
+        part = linear(xp, Wp)
+        y = part if y is None else y + part
+    if bias is not None:
+        y = y + np.asarray(bias, dtype=np.float64)
+    return y
+
+
+def megatron_layer(h_bits, Wd: dict, bd: dict, H: int, P: int, G: int = 128) -> dict:
+    """The OPT layer of `layer` computed the Megatron way by P ranks, step by step: every rank runs
+    LN1 on the full h, its QKV rows (megatron_qkv_rows) -> its V slice, its O columns -> partial, the
+    partials all-reduced (+ bias) -> y_o, residual + LN2 on the full h1, its fc1 rows -> ReLU, its fc2
+    columns -> partial, all-reduced (+ bias), residual.  Returns layer's keys (full tensors, the
+    column-parallel ones concatenated over ranks in rank order) plus "y_qkv_p", "v_p", "y_fc1_p",
+    "u_p": the per-rank local tensors."""
+    F = np.asarray(Wd["fc1"]).shape[0]
+    out = {"h": np.asarray(h_bits, dtype=np.uint16)}
+    out["a"] = layernorm(out["h"])
+    rows = [megatron_qkv_rows(H, P, p, G) for p in range(P)]
+    bq = bd.get("qkv")
+    out["y_qkv_p"] = [linear(out["a"], np.asarray(Wd["qkv"])[r], None if bq is None else np.asarray(bq)[r])
+                      for r in rows]
+    Hl = H // P
+    out["v_p"] = [round_to_bf16(y[:, 2 * Hl:3 * Hl]) for y in out["y_qkv_p"]]
+    Wo = np.asarray(Wd["o"])
+    out["y_o"] = linear_rowpar(out["v_p"], [Wo[:, slice(*shard_k(H, P, p, G))] for p in range(P)], bd.get("o"))
+    out["h1"] = residual(out["h"], out["y_o"])
+    out["a2"] = layernorm(out["h1"])
+    W1, b1 = np.asarray(Wd["fc1"]), bd.get("fc1")
+    f_rows = [shard(F, P, p, G) for p in range(P)]
+    out["y_fc1_p"] = [linear(out["a2"], W1[r0:r1], None if b1 is None else np.asarray(b1)[r0:r1])
+                      for r0, r1 in f_rows]
+    out["u_p"] = [relu_bf16(y) for y in out["y_fc1_p"]]
+    W2 = np.asarray(Wd["fc2"])
+    out["y_fc2"] = linear_rowpar(out["u_p"], [W2[:, slice(*shard_k(F, P, p, G))] for p in range(P)], bd.get("fc2"))
+    out["out"] = residual(out["h1"], out["y_fc2"])
+    # full views for comparison with `layer`
+    y_qkv = np.empty((out["a"].shape[0], 3 * H))
+    for r, y in zip(rows, out["y_qkv_p"]):
+        y_qkv[:, r] = y
+    out["y_qkv"] = y_qkv
+    out["v"] = np.concatenate(out["v_p"], axis=1)
+    out["y_fc1"] = np.concatenate(out["y_fc1_p"], axis=1)
+    out["u"] = np.concatenate(out["u_p"], axis=1)
+    return out
+
+
+# ----------------------------------------------------------------------------
 # c2.3 Cost model (P:141-173 Sec. 3.2; P:229-233 Sec. 4.2), fp64
 #   V_X are "parameter size divided by processing time" (P:46): bytes/s.
 # ----------------------------------------------------------------------------
