@@ -65,7 +65,7 @@ extern "C" {
 #endif
 
 #define HG_MAX_BATCH 8
-#define HG_ABI_VERSION 3
+#define HG_ABI_VERSION 4
 
 typedef enum {
     HG_OK = 0,
@@ -223,19 +223,38 @@ typedef struct {
     const float *bias_host; /* host copy of bias [N_local] fp32 or NULL (mirror_glue, reading R24) */
 } hg_linear_desc;
 
+/* How a layer's linears are sharded over P > 1 ranks (BJ:5; not in the
+ * paper, which runs one GPU).  Ignored at P = 1. */
+typedef enum {
+    HG_TP_COLUMN = 0,   /* every linear column-sharded (rank p holds W rows [pN/P, (p+1)N/P)), its
+                           outputs all-gathered after it: 4 exchanges per layer (BJ:5's form)       */
+    HG_TP_MEGATRON = 1  /* Megatron pairing (reading R32): qkv holds the rank's heads' rows of q, k
+                           and v ([3H/P, H]: rows [pH/P, (p+1)H/P) + {0, H, 2H}) and fc1 rows
+                           [pF/P, (p+1)F/P) ([F/P, H]) -- column-parallel, no exchange; o [H, H/P]
+                           and fc2 [H, F/P] hold the input columns matching those outputs --
+                           row-parallel, their partial sums all-reduced in rank order with the bias
+                           added once after the sum: 2 exchanges per layer.  Peer group only.    */
+} hg_tp;
+
 /* One OPT pre-LN decoder layer (reading R22).  lin[0..3] =
  * {qkv [3H,H], o [H,H], fc1 [F,H], fc2 [H,F]}; with P ranks each rank's
- * descriptors hold its row shard (N/P rows).  LN parameters are device fp32 [H]
- * or NULL (gamma = 1, beta = 0). */
+ * descriptors hold its shard (tp: HG_TP_COLUMN row shards of N/P rows, or the
+ * HG_TP_MEGATRON shapes above; a row-parallel linear's bias / bias_host are the
+ * full [H] vectors).  LN parameters are device fp32 [H] or NULL (gamma = 1,
+ * beta = 0). */
 typedef struct {
     int64_t hidden, ffn;
     hg_linear_desc lin[4];
     const float *ln1_g, *ln1_b, *ln2_g, *ln2_b;
     const float *ln1_g_host, *ln1_b_host, *ln2_g_host, *ln2_b_host; /* host copies (mirror_glue) */
+    int32_t tp;   /* hg_tp (0 = HG_TP_COLUMN)                                                 */
+    int32_t _pad;
 } hg_opt_layer;
 
 /* Optional per-step device copies of a layer's intermediates (teacher-forced
- * parity tests).  Every pointer is device memory or NULL (skipped). */
+ * parity tests).  Every pointer is device memory or NULL (skipped).  With
+ * HG_TP_MEGATRON at P > 1, y_qkv, v, y_fc1 and u hold this rank's local
+ * tensors ([B,3H/P] in its qkv row order, [B,H/P], [B,F/P], [B,F/P]). */
 typedef struct {
     void *a;      /* bf16 [B,H]   LN1(h)                        input of qkv */
     float *y_qkv; /* fp32 [B,3H]                                             */
@@ -483,6 +502,15 @@ HG_API hg_status hg_gather_permute(hg_ctx *ctx, const float *gathered, int nrank
 HG_API hg_status hg_linear_sharded(hg_ctx *ctx, const hg_plan_t *plan, const void *x_dev,
                                    const void *W_dev, const void *W_host, const float *bias_dev,
                                    float *y_full_dev, void *stream);
+
+/* Row-parallel linear (HG_TP_MEGATRON's o / fc2, reading R32): this rank's partial
+ * x_local . W_p^T over its K_local input columns, with the rows of W_p [N, K_local] split by the plan
+ * like any linear (plan for (N, K_local)), then the partials all-reduced over the peer group in rank
+ * order and bias_dev [N] (device fp32 or NULL) added once: y_full_dev [batch, N] fp32, the same bits
+ * on every rank.  x_local_dev [batch, K_local] bf16 device.  Needs hg_peer_open (HG_ESTATE). */
+HG_API hg_status hg_linear_rowpar(hg_ctx *ctx, const hg_plan_t *plan, const void *x_local_dev,
+                                  const void *W_dev, const void *W_host, const float *bias_dev,
+                                  float *y_full_dev, void *stream);
 
 /* ---------------------------------------------------------------- host placement */
 /* The NUMA node of CUDA device `device`'s PCI slot (sysfs numa_node), -1 when unknown. */

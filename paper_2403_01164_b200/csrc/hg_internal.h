@@ -157,6 +157,8 @@ void peer_debug_words(PeerGroup *g, uint32_t *out);
 int peer_rank(const PeerGroup *g);
 int peer_exchange(PeerGroup *g, const float *ylocal, int B, int64_t n_local, float *y, int64_t ldy, uint32_t *err,
                   double timeout_s, void *stream);
+int peer_reduce(PeerGroup *g, const float *partial, int B, int64_t N, const float *bias, float *y, int64_t ldy,
+                uint32_t *err, double timeout_s, void *stream);
 float *peer_host_y(PeerGroup *g, int64_t k);
 float *peer_host_y_dev(PeerGroup *g, int64_t k);
 int peer_host_slots();

@@ -74,7 +74,8 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 struct PushArgs {
     const float *src;        // this rank's [B][n_local]
-    int64_t n_local, N_full;
+    int64_t n_local;
+    int64_t dst0, dst_ld;    // element (b, j) lands at box slot + dst0 + b * dst_ld + j
     int B, P, p, slot;
     uint32_t tag;            // exchange sequence + 1
     int64_t box_floats;
@@ -86,8 +87,8 @@ struct PushArgs {
     unsigned long long timeout_ns;
 };
 
-// Push [B][n_local] into every rank's box at columns [p n_local, (p+1) n_local), then raise this
-// rank's flag in every box.  The box slot is reused every kDevSlots exchanges: first wait until every
+// Push [B][n_local] into every rank's box (all-gather: at columns [p n_local, (p+1) n_local) of
+// [B][N_full]; all-reduce: as partial p of [P][B][N]), then raise this rank's flag in every box.  The box slot is reused every kDevSlots exchanges: first wait until every
 // rank has copied out the exchange that used it before.
 __global__ void peer_push_kernel(const __grid_constant__ PushArgs a) {
     if (threadIdx.x < a.P && a.tag > (uint32_t)kDevSlots) {
@@ -106,11 +107,11 @@ __global__ void peer_push_kernel(const __grid_constant__ PushArgs a) {
     }
     __syncthreads();
     const int64_t total = (int64_t)a.B * a.n_local;
-    const int64_t off = (int64_t)a.slot * a.box_floats + (int64_t)a.p * a.n_local;
+    const int64_t off = (int64_t)a.slot * a.box_floats + a.dst0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / a.n_local, j = i - b * a.n_local;
         const float v = a.src[i];
-        for (int r = 0; r < a.P; ++r) a.box[r][off + b * a.N_full + j] = v;
+        for (int r = 0; r < a.P; ++r) a.box[r][off + b * a.dst_ld + j] = v;
     }
     __threadfence_system();
     __syncthreads();
@@ -129,16 +130,19 @@ struct WaitArgs {
     const uint32_t *flag;    // this rank's flags
     uint32_t *done;          // this rank's consumed word
     float *y;
+    const float *bias;       // all-reduce: added once after the sum (NULL = none)
     int64_t ldy, N_full, box_floats;
     int B, P, slot;
+    int reduce;              // 0: copy [B][N_full]; 1: y = sum over ranks of [P][B][N_full], rank order
     uint32_t tag;
     uint32_t *count;
     uint32_t *err;
     unsigned long long timeout_ns;
 };
 
-// Wait until every rank's rows of this exchange are in this rank's box, copy them into y, and mark
-// the box slot consumed.
+// Wait until every rank's part of this exchange is in this rank's box, copy them into y (all-gather)
+// or sum them into y in rank order and add the bias (all-reduce: every rank adds the same values in
+// the same order, so every rank holds the same bits), and mark the box slot consumed.
 __global__ void peer_wait_kernel(const __grid_constant__ WaitArgs a) {
     if (threadIdx.x < a.P) {
         const unsigned long long t0 = gtime();
@@ -158,7 +162,12 @@ __global__ void peer_wait_kernel(const __grid_constant__ WaitArgs a) {
     const int64_t total = (int64_t)a.B * a.N_full;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t b = i / a.N_full, j = i - b * a.N_full;
-        a.y[b * a.ldy + j] = __ldcv(src + i);
+        float v = __ldcv(src + i);
+        if (a.reduce) {
+            for (int q = 1; q < a.P; ++q) v = __fadd_rn(v, __ldcv(src + (int64_t)q * total + i));
+            if (a.bias) v = __fadd_rn(v, a.bias[j]);
+        }
+        a.y[b * a.ldy + j] = v;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -376,23 +385,23 @@ void peer_debug_words(PeerGroup *g, uint32_t *out) {
 }
 int peer_rank(const PeerGroup *g) { return g ? g->p : 0; }
 
-// Device exchange of one linear: ylocal [B][n_local] (this rank's rows) -> y [B][ldy] full, in
-// global column order, on `stream`.
-int peer_exchange(PeerGroup *g, const float *ylocal, int B, int64_t n_local, float *y, int64_t ldy, uint32_t *err,
-                  double timeout_s, void *stream) {
-    const int64_t N_full = n_local * g->P;
-    if ((int64_t)B * N_full > g->box_floats) return (int)cudaErrorInvalidValue;
+namespace {
+// One device exchange: push this rank's [B][n_local] into every box at (dst0, dst_ld), then wait for
+// all P parts and copy (reduce = 0) or sum (reduce = 1) the box's [B][N_out] view into y.
+int exchange(PeerGroup *g, const float *src, int B, int64_t n_local, int64_t dst0, int64_t dst_ld, int64_t N_out,
+             int reduce, const float *bias, float *y, int64_t ldy, uint32_t *err, double timeout_s, void *stream) {
     const uint64_t q = g->seq++;
     static const bool dbg = getenv("HG_PEER_DEBUG") != nullptr;
-    if (dbg) fprintf(stderr, "hg peer: rank %d exchange %llu n_local %lld B %d stream %p\n", g->p, (unsigned long long)q,
-                     (long long)n_local, B, stream);
+    if (dbg) fprintf(stderr, "hg peer: rank %d exchange %llu (%s) n_local %lld B %d stream %p\n", g->p,
+                     (unsigned long long)q, reduce ? "reduce" : "gather", (long long)n_local, B, stream);
     const int slot = (int)(q % kDevSlots);
     const uint32_t tag = (uint32_t)(q + 1);
     const unsigned long long tns = (unsigned long long)(timeout_s * 1e9 * dev_timeout_scale());
     PushArgs pa{};
-    pa.src = ylocal;
+    pa.src = src;
     pa.n_local = n_local;
-    pa.N_full = N_full;
+    pa.dst0 = dst0;
+    pa.dst_ld = dst_ld;
     pa.B = B;
     pa.P = g->P;
     pa.p = g->p;
@@ -418,20 +427,41 @@ int peer_exchange(PeerGroup *g, const float *ylocal, int B, int64_t n_local, flo
     wa.flag = g->flag[g->p];
     wa.done = g->done[g->p];
     wa.y = y;
+    wa.bias = bias;
     wa.ldy = ldy;
-    wa.N_full = N_full;
+    wa.N_full = N_out;
     wa.box_floats = g->box_floats;
     wa.B = B;
     wa.P = g->P;
     wa.slot = slot;
+    wa.reduce = reduce;
     wa.tag = tag;
     wa.count = g->count + 1;
     wa.err = err;
     wa.timeout_ns = tns;
-    int wgrid = (int)std::min<int64_t>(32, ((int64_t)B * N_full + 255) / 256);
+    int wgrid = (int)std::min<int64_t>(32, ((int64_t)B * N_out + 255) / 256);
     if (wgrid < 1) wgrid = 1;
     peer_wait_kernel<<<wgrid, 256, 0, (cudaStream_t)stream>>>(wa);
     return (int)cudaGetLastError();
+}
+}  // namespace
+
+// All-gather of one linear's row shards: ylocal [B][n_local] (this rank's rows) -> y [B][ldy] full, in
+// global column order, on `stream`.
+int peer_exchange(PeerGroup *g, const float *ylocal, int B, int64_t n_local, float *y, int64_t ldy, uint32_t *err,
+                  double timeout_s, void *stream) {
+    const int64_t N_full = n_local * g->P;
+    if ((int64_t)B * N_full > g->box_floats) return (int)cudaErrorInvalidValue;
+    return exchange(g, ylocal, B, n_local, (int64_t)g->p * n_local, N_full, N_full, 0, nullptr, y, ldy, err,
+                    timeout_s, stream);
+}
+
+// All-reduce of a row-parallel linear's partial sums (Megatron pairing, reading R32): partial [B][N]
+// -> y [B][ldy] = sum over ranks in rank order (+ bias once), identical bits on every rank.
+int peer_reduce(PeerGroup *g, const float *partial, int B, int64_t N, const float *bias, float *y, int64_t ldy,
+                uint32_t *err, double timeout_s, void *stream) {
+    if ((int64_t)g->P * B * N > g->box_floats) return (int)cudaErrorInvalidValue;
+    return exchange(g, partial, B, N, (int64_t)g->p * B * N, N, N, 1, bias, y, ldy, err, timeout_s, stream);
 }
 
 // ---- host side: the shared [kHostSlots][B][N_full] segment

@@ -1079,31 +1079,63 @@ hg_status gather(hg_ctx *c, const float *ylocal, int B, int64_t n_local, float *
     return HG_OK;
 }
 
-// One linear of a layer: sharded (P > 1: local rows then all-gather) or not.
+// all-reduce of a row-parallel linear's partial [B, N] into y [B, N] (+ bias once), peer group only
+hg_status reduce(hg_ctx *c, const float *partial, int B, int64_t N, const float *bias, float *y, cudaStream_t s) {
+    if (!c->peer) return set_error(HG_EUNSUPPORTED, "row-parallel linears need the peer group (hg_peer_open)");
+    HG_TRY(kerr(c, peer_reduce(c->peer, partial, B, N, bias, y, N, c->err, c->cfg.timeout_s, s), "peer reduce"));
+    c->st.gpu_launches += 2;
+    return HG_OK;
+}
+
+// How a layer's linear meets the other ranks' shards (hg_tp; one rank: kLocal).
+enum class Xchg { kGather, kLocal, kReduce };
+
+// One linear of a layer: kGather (P > 1: local rows, then all-gather into y [B, P*N]), kLocal (this
+// rank's rows only, y [B, N]), kReduce (partial without bias, then all-reduce + bias into y [B, N]).
 hg_status layer_linear(hg_ctx *c, const hg_linear_desc &d, const void *x, float *y, int64_t N_full,
-                       cudaStream_t s) {
+                       cudaStream_t s, Xchg kind = Xchg::kGather) {
     const int P = nranks_of(c);
     Lin L{d.plan, x, d.W_dev, (const uint8_t *)d.W_host, d.bias, y, N_full};
-    if (P == 1) return run_linear(c, L, s);
+    if (P == 1 || kind == Xchg::kLocal) {
+        L.ldy = d.plan.N;
+        return run_linear(c, L, s);
+    }
     HG_TRY(ensure(c, (void **)&c->ylocal, &c->ylocal_elems, d.plan.batch * d.plan.N * 4));
     L.y = c->ylocal;
     L.ldy = d.plan.N;
+    if (kind == Xchg::kReduce) {
+        L.bias = nullptr;  // added once, after the sum
+        HG_TRY(run_linear(c, L, s));
+        return reduce(c, c->ylocal, (int)d.plan.batch, d.plan.N, d.bias, y, s);
+    }
     HG_TRY(run_linear(c, L, s));
     return gather(c, c->ylocal, (int)d.plan.batch, d.plan.N, y, s);
 }
 
+// Megatron pairing in force for this layer (HG_TP_MEGATRON with more than one rank).
+bool megatron(const hg_ctx *c, const hg_opt_layer &l) { return l.tp == HG_TP_MEGATRON && nranks_of(c) > 1; }
+
 hg_status validate_layer(hg_ctx *c, const hg_opt_layer &l, int B) {
     const int P = nranks_of(c);
     const int64_t H = l.hidden, F = l.ffn;
-    const int64_t Ns[4] = {3 * H, H, F, H}, Ks[4] = {H, H, H, F};
     if (H <= 0 || F <= 0) return set_error(HG_EINVAL, "layer: hidden/ffn must be > 0");
+    if (l.tp != HG_TP_COLUMN && l.tp != HG_TP_MEGATRON) return set_error(HG_EINVAL, "layer: tp %d", l.tp);
+    const bool mg = megatron(c, l);
+    if (mg && (H % P || F % P)) return set_error(HG_EINVAL, "layer: Megatron needs H and F divisible by P");
+    if (mg && !c->peer) return set_error(HG_EUNSUPPORTED, "layer: Megatron pairing needs the peer group");
+    // expected (N, K) of this rank's descriptors: column shards (N_full / P rows), or the Megatron
+    // shapes (hg_tp)
+    const int64_t Nfull[4] = {3 * H, H, F, H};
+    const int64_t Ns[4] = {3 * H / P, mg ? H : H / P, F / P, mg ? H : H / P};
+    const int64_t Ks[4] = {H, mg ? H / P : H, H, mg ? F / P : F};
     for (int i = 0; i < 4; ++i) {
         const hg_linear_desc &d = l.lin[i];
-        if (d.plan.N * P != Ns[i] || d.plan.K != Ks[i] || d.plan.batch != B)
+        const bool rows_split = !mg || i == 0 || i == 2;  // this linear's output columns are sharded
+        if (d.plan.N != Ns[i] || d.plan.K != Ks[i] || d.plan.batch != B || (rows_split && Nfull[i] % P))
             return set_error(HG_EINVAL, "layer linear %d: plan (N=%lld K=%lld B=%lld) does not match "
-                                        "(N=%lld/%d K=%lld B=%d)", i, (long long)d.plan.N,
-                             (long long)d.plan.K, (long long)d.plan.batch, (long long)Ns[i], P,
-                             (long long)Ks[i], B);
+                                        "(N=%lld K=%lld B=%d; %d ranks, %s)", i, (long long)d.plan.N,
+                             (long long)d.plan.K, (long long)d.plan.batch, (long long)Ns[i], (long long)Ks[i], B,
+                             P, mg ? "Megatron" : "column shards");
         HG_TRY(validate_plan(c, d.plan));
         if (d.plan.n_res > 0) HG_TRY(check_ptr(c, d.W_dev, true, "layer W_dev"));
         if (d.plan.n_res < d.plan.N) {
@@ -1123,6 +1155,12 @@ hg_status trace_copy(hg_ctx *c, void *dst, const void *src, size_t bytes, cudaSt
 hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_trace *tr,
                     cudaStream_t s) {
     const int64_t H = l.hidden, F = l.ffn;
+    // Megatron pairing (hg_tp): qkv / fc1 stay local ([B, 3H/P], [B, F/P]; the V slice and the ReLU
+    // act on this rank's columns), o / fc2 are all-reduced; otherwise every linear is all-gathered
+    const bool mg = megatron(c, l);
+    const int P = nranks_of(c);
+    const int64_t Hl = mg ? H / P : H, Fl = mg ? F / P : F;
+    const Xchg col = mg ? Xchg::kLocal : Xchg::kGather, row = mg ? Xchg::kReduce : Xchg::kGather;
     HG_TRY(ensure(c, &c->act, &c->act_elems, (int64_t)B * (F > H ? F : H) * 2));
     HG_TRY(ensure(c, (void **)&c->yscr, &c->yscr_elems, (int64_t)B * (F > 3 * H ? F : 3 * H) * 4));
     HG_TRY(ensure(c, &c->h1, &c->h1_elems, (int64_t)B * H * 2));
@@ -1130,13 +1168,13 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
     HG_TRY(kerr(c, launch_layernorm(h, H, B, l.ln1_g, l.ln1_b, c->act, s), "ln1"));
     if (tr) HG_TRY(trace_copy(c, tr->a, c->act, (size_t)B * H * 2, s));
     // qkv
-    HG_TRY(layer_linear(c, l.lin[0], c->act, c->yscr, 3 * H, s));
-    if (tr && tr->y_qkv) HG_TRY(trace_copy(c, tr->y_qkv, c->yscr, (size_t)B * 3 * H * 4, s));
+    HG_TRY(layer_linear(c, l.lin[0], c->act, c->yscr, 3 * H, s, col));
+    if (tr && tr->y_qkv) HG_TRY(trace_copy(c, tr->y_qkv, c->yscr, (size_t)B * 3 * Hl * 4, s));
     // attention at decode position 0: context = v
-    HG_TRY(kerr(c, launch_slice_to_bf16(c->yscr, 3 * H, 2 * H, H, B, c->act, s), "v"));
-    if (tr) HG_TRY(trace_copy(c, tr->v, c->act, (size_t)B * H * 2, s));
+    HG_TRY(kerr(c, launch_slice_to_bf16(c->yscr, 3 * Hl, 2 * Hl, Hl, B, c->act, s), "v"));
+    if (tr) HG_TRY(trace_copy(c, tr->v, c->act, (size_t)B * Hl * 2, s));
     // o
-    HG_TRY(layer_linear(c, l.lin[1], c->act, c->yscr, H, s));
+    HG_TRY(layer_linear(c, l.lin[1], c->act, c->yscr, H, s, row));
     if (tr) HG_TRY(trace_copy(c, tr->y_o, c->yscr, (size_t)B * H * 4, s));
     // h1 = h + o ; a2 = LN2(h1)
     HG_TRY(kerr(c, launch_residual_ln(h, c->yscr, H, B, c->h1, l.ln2_g, l.ln2_b, c->act, s), "res+ln2"));
@@ -1145,12 +1183,12 @@ hg_status run_layer(hg_ctx *c, const hg_opt_layer &l, void *h, int B, hg_layer_t
         HG_TRY(trace_copy(c, tr->a2, c->act, (size_t)B * H * 2, s));
     }
     // fc1 + ReLU
-    HG_TRY(layer_linear(c, l.lin[2], c->act, c->yscr, F, s));
-    if (tr) HG_TRY(trace_copy(c, tr->y_fc1, c->yscr, (size_t)B * F * 4, s));
-    HG_TRY(kerr(c, launch_relu_bf16(c->yscr, F, B, c->act, s), "relu"));
-    if (tr) HG_TRY(trace_copy(c, tr->u, c->act, (size_t)B * F * 2, s));
+    HG_TRY(layer_linear(c, l.lin[2], c->act, c->yscr, F, s, col));
+    if (tr) HG_TRY(trace_copy(c, tr->y_fc1, c->yscr, (size_t)B * Fl * 4, s));
+    HG_TRY(kerr(c, launch_relu_bf16(c->yscr, Fl, B, c->act, s), "relu"));
+    if (tr) HG_TRY(trace_copy(c, tr->u, c->act, (size_t)B * Fl * 2, s));
     // fc2 + residual
-    HG_TRY(layer_linear(c, l.lin[3], c->act, c->yscr, H, s));
+    HG_TRY(layer_linear(c, l.lin[3], c->act, c->yscr, H, s, row));
     if (tr) HG_TRY(trace_copy(c, tr->y_fc2, c->yscr, (size_t)B * H * 4, s));
     HG_TRY(kerr(c, launch_residual(c->h1, c->yscr, H, B, h, s), "residual"));
     c->st.gpu_launches += 5;
@@ -1169,6 +1207,8 @@ bool can_mirror(hg_ctx *c, const hg_opt_layer *layers, int n) {
     // P > 1 mirrors only through the peer group's shared host segment (not with NCCL)
     const bool multi = nranks_of(c) != 1;
     if (!c->cfg.mirror_glue || (multi && !c->peer) || !hglue_supported()) return false;
+    for (int l = 0; l < n; ++l)  // the Megatron pairing takes the plain path (tp is alike on every rank)
+        if (megatron(c, layers[l])) return false;
     bool any_cpu = false;  // without CPU rows nobody needs the glue on the host
     for (int l = 0; l < n; ++l)
         for (int i = 0; i < 4; ++i) any_cpu |= layers[l].lin[i].plan.n_cpu > 0;
@@ -1737,6 +1777,23 @@ HG_API hg_status hg_linear_sharded(hg_ctx *c, const hg_plan_t *p, const void *x,
     return end_call(c, s);
 }
 
+HG_API hg_status hg_linear_rowpar(hg_ctx *c, const hg_plan_t *p, const void *x, const void *W_dev,
+                                  const void *W_host, const float *bias, float *y_full, void *stream) {
+    if (!c || !p) return set_error(HG_EINVAL, "NULL argument");
+    if (!c->peer) return set_error(HG_ESTATE, "hg_peer_open not called");
+    if (c->error) return set_error(HG_ESTATE, "context is in an error state");
+    HG_CK(c, cudaSetDevice(c->device));
+    HG_TRY(validate_lin(c, *p, x, W_dev, W_host, bias, y_full));
+    cudaStream_t s = (cudaStream_t)stream;
+    HG_TRY(begin_call(c, s));
+    std::vector<ChunkReq> list;
+    push_chunks(list, *p, W_host);
+    set_future(c, std::move(list), false);
+    hg_linear_desc d{W_dev, W_host, bias, *p};
+    HG_TRY(layer_linear(c, d, x, y_full, p->N, s, nranks_of(c) > 1 ? Xchg::kReduce : Xchg::kLocal));
+    return end_call(c, s);
+}
+
 HG_API hg_status hg_layer(hg_ctx *c, const hg_opt_layer *l, void *h, int batch,
                           hg_layer_trace *trace, void *stream) {
     if (!c || !l) return set_error(HG_EINVAL, "NULL argument");
@@ -1932,9 +1989,10 @@ HG_API hg_status hg_peer_export(hg_ctx *c, int nranks, int rank, void *blob) {
     if (c->peer && (peer_nranks(c->peer) != nranks || peer_rank(c->peer) != rank))
         return set_error(HG_ESTATE, "peer group already exported with another shape");
     HG_CK(c, cudaSetDevice(c->device));
+    // device box: a gathered y [B, N] or the P partials [P][B][N] of an all-reduce; host slot: a y
     const int64_t floats = (int64_t)HG_MAX_BATCH * c->cfg.max_n;
     PeerGroup *g = c->peer;
-    HG_TRY(peer_export(&g, c->device, nranks, rank, floats, floats, blob));
+    HG_TRY(peer_export(&g, c->device, nranks, rank, floats * nranks, floats, blob));
     c->peer_pending = g;
     return HG_OK;
 }

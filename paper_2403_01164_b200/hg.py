@@ -32,6 +32,7 @@ HG_MAX_BATCH = 8
 PEER_BLOB = 512  # bytes per rank exchanged by hg_peer_export / hg_peer_open
 EXACT, APPROX, TPRIME, ASYNC, FIXED = 0, 1, 2, 3, 4
 HYBRID, NAIVE, PINNED_BLOCKING = 0, 1, 2  # hg_strategy (Fig. 5c / 5a / 5b)
+TP_COLUMN, TP_MEGATRON = 0, 1  # hg_tp
 
 
 class HgError(RuntimeError):
@@ -101,7 +102,8 @@ class OptLayer(ctypes.Structure):
     _fields_ = [("hidden", ctypes.c_int64), ("ffn", ctypes.c_int64), ("lin", LinearDesc * 4),
                 ("ln1_g", ctypes.c_void_p), ("ln1_b", ctypes.c_void_p), ("ln2_g", ctypes.c_void_p),
                 ("ln2_b", ctypes.c_void_p), ("ln1_g_host", ctypes.c_void_p), ("ln1_b_host", ctypes.c_void_p),
-                ("ln2_g_host", ctypes.c_void_p), ("ln2_b_host", ctypes.c_void_p)]
+                ("ln2_g_host", ctypes.c_void_p), ("ln2_b_host", ctypes.c_void_p), ("tp", ctypes.c_int32),
+                ("_pad", ctypes.c_int32)]
 
 
 class LayerTrace(ctypes.Structure):
@@ -162,6 +164,7 @@ _sig = {
     "hg_dist_unique_id": (_i32, [_vp]),
     "hg_dist_init": (_i32, [_vp, _i32, _i32, _vp]),
     "hg_linear_sharded": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
+    "hg_linear_rowpar": (_i32, [_vp, _P(Plan), _vp, _vp, _vp, _vp, _vp, _vp]),
     "hg_alpha_solve": (_i32, [_P(_dbl), _P(_dbl), _P(_dbl), _P(_dbl), _i32, _i32, _dbl, _dbl, _dbl,
                               _P(_dbl), _P(_i32)]),
     "hg_alpha_bench": (_i32, [_vp, _P(OptLayer), _i32, _vp, _i32, _dbl, _P(AbenchCfg), _P(AbenchResult), _vp]),
@@ -384,6 +387,10 @@ class Context:
         _check(_lib.hg_linear_sharded(self._h, ctypes.byref(plan), _ptr(x), _ptr(W_dev), _ptr(W_host),
                                       _ptr(bias), _ptr(y_full), _stream(stream)))
 
+    def hg_linear_rowpar(self, plan, x_local, W_dev, W_host, bias, y_full, stream=None):
+        _check(_lib.hg_linear_rowpar(self._h, ctypes.byref(plan), _ptr(x_local), _ptr(W_dev), _ptr(W_host),
+                                     _ptr(bias), _ptr(y_full), _stream(stream)))
+
     def hg_layer(self, layer: OptLayer, h, batch, trace: LayerTrace | None = None, stream=None):
         _check(_lib.hg_layer(self._h, ctypes.byref(layer), _ptr(h), batch,
                              ctypes.byref(trace) if trace is not None else None, _stream(stream)))
@@ -470,10 +477,12 @@ def linear_desc(plan: Plan, W_dev=None, W_host=None, bias=None, bias_host=None) 
     return LinearDesc(_ptr(W_dev), _ptr(W_host), _ptr(bias), plan, _ptr(bias_host))
 
 
-def opt_layer(hidden, ffn, descs, ln1_g=None, ln1_b=None, ln2_g=None, ln2_b=None, ln_host=None) -> OptLayer:
-    """ln_host: optional (g1, b1, g2, b2) host copies of the LN parameters (mirrored glue)."""
+def opt_layer(hidden, ffn, descs, ln1_g=None, ln1_b=None, ln2_g=None, ln2_b=None, ln_host=None,
+              tp: int = 0) -> OptLayer:
+    """ln_host: optional (g1, b1, g2, b2) host copies of the LN parameters (mirrored glue); tp: TP_COLUMN
+    or TP_MEGATRON (hg_tp)."""
     L = OptLayer()
-    L.hidden, L.ffn = hidden, ffn
+    L.hidden, L.ffn, L.tp = hidden, ffn, tp
     for i, d in enumerate(descs):
         L.lin[i] = d
     L.ln1_g, L.ln1_b, L.ln2_g, L.ln2_b = (_ptr(t) for t in (ln1_g, ln1_b, ln2_g, ln2_b))

@@ -22,25 +22,36 @@ from paper_2403_01164_b200 import hg  # noqa: E402
 NAMES = ("qkv", "o", "fc1", "fc2")
 
 
-def shard_layer(c, H, F, B, layer, P, p, alpha, keep, seed):
+def shard_layer(c, H, F, B, layer, P, p, alpha, keep, seed, tp="column"):
+    """This rank's descriptors: column shards (rows [pN/P, (p+1)N/P) of every linear), or the Megatron
+    pairing (qkv: its heads' q/k/v rows, fc1: its rows, o / fc2: its input columns, full bias)."""
     shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
     descs = []
     for name in NAMES:
         N, K = shapes[name]
         _, W, bfull = gen.linear_inputs(seed, layer, name, 1, N, K)
-        r0, r1 = oracle.shard(N, P, p, 128)
-        plan = c.plan(hg.make_rates(1, 1, 1), r1 - r0, K, B, 0, hg.FIXED, alpha)
-        Wh = pinned(W[r0:r1])
-        bias, bias_h = dev_f32(bfull[r0:r1]), torch.from_numpy(np.ascontiguousarray(bfull[r0:r1], np.float32))
+        if tp == "megatron" and name in ("o", "fc2"):
+            k0, k1 = oracle.shard_k(K, P, p, 128)
+            Wp, bp = np.ascontiguousarray(W[:, k0:k1]), bfull
+        elif tp == "megatron" and name == "qkv":
+            rows = oracle.megatron_qkv_rows(H, P, p, 128)
+            Wp, bp = np.ascontiguousarray(W[rows]), bfull[rows]
+        else:
+            r0, r1 = oracle.shard(N, P, p, 128)
+            Wp, bp = W[r0:r1], bfull[r0:r1]
+        plan = c.plan(hg.make_rates(1, 1, 1), Wp.shape[0], Wp.shape[1], B, 0, hg.FIXED, alpha)
+        Wh = pinned(Wp)
+        bias, bias_h = dev_f32(bp), torch.from_numpy(np.ascontiguousarray(bp, np.float32))
         keep += [Wh, bias, bias_h]
         descs.append(hg.linear_desc(plan, None, Wh, bias, bias_h))
-    return hg.opt_layer(H, F, descs)
+    return hg.opt_layer(H, F, descs, tp=hg.TP_MEGATRON if tp == "megatron" else hg.TP_COLUMN)
 
 
 def main():
     P, p = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     H, F, NL, B = (int(os.environ[k]) for k in ("H", "F", "NL", "B"))
     seed, out = int(os.environ.get("SEED", 71)), os.environ["OUT"]
+    tp = os.environ.get("TP", "column")
     dist.init_process_group("gloo")
     torch.cuda.set_device(0)
     st = torch.cuda.Stream()
@@ -53,7 +64,7 @@ def main():
             dist.all_gather_object(blobs, c.hg_peer_export(P, p))
             c.hg_peer_open(blobs)
             keep = []
-            layers = [shard_layer(c, H, F, B, l, P, p, (0.35 + 0.1 * p) % 1.0, keep, seed) for l in range(NL)]
+            layers = [shard_layer(c, H, F, B, l, P, p, (0.35 + 0.1 * p) % 1.0, keep, seed, tp) for l in range(NL)]
             h0 = gen.uniform_bf16(seed + 1, 989, B * H, 1.0).reshape(B, H)
             hs = [dev(h0) for _ in range(2)]
             st.synchronize()

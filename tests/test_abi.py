@@ -26,7 +26,7 @@ def test_every_declared_symbol_is_exported_and_bound():
     for n in names:
         assert hasattr(lib, n), n
         assert n in hg.EXPORTED, f"{n} not bound in hg.py"
-    assert hg.hg_abi_version() == 3
+    assert hg.hg_abi_version() == 4
 
 
 def test_library_has_sm100a_code():

@@ -110,6 +110,50 @@ def test_peer_linear_sharded(P, B):
     assert ok, worst
 
 
+@pytest.mark.parametrize("P", [2, 4, 8])
+@pytest.mark.parametrize("B", [1, 3])
+def test_peer_linear_rowpar(P, B):
+    """Row-parallel linear (Megatron's o / fc2, reading R32): rank p holds input columns
+    [pK/P, (p+1)K/P) of W and the matching slice of x, runs its own heterogeneous split over the N rows,
+    and the partials are all-reduced in rank order with the bias added once: the same bits on every
+    rank, within tolerance of the oracle's row-parallel sum (and of the unsharded linear)."""
+    N, K = 1024, 4096
+    x, W, b = gen.linear_inputs(62, 0, "fc2", B, N, K)
+    parts = [oracle.shard_k(K, P, q, 128) for q in range(P)]
+    ref = oracle.linear_rowpar([x[:, a:e] for a, e in parts], [np.ascontiguousarray(W[:, a:e]) for a, e in parts], b)
+
+    def rank_fn(p, exchange, bar):
+        c = make_ctx(P, p, exchange)
+        try:
+            k0, k1 = parts[p]
+            n_res = (128 * p) % N
+            plan = c.plan(hg.make_rates(1, 1, 1), N, k1 - k0, B, n_res, hg.FIXED, (0.3 + 0.2 * p) % 1.0)
+            Wp = np.ascontiguousarray(W[:, k0:k1])
+            Wd = dev(Wp[:n_res]) if n_res else None
+            Wh = pinned(Wp[n_res:])
+            xd, bd = dev(np.ascontiguousarray(x[:, k0:k1])), dev_f32(b)
+            ys_dev = [torch.full((B, N), float("nan"), device="cuda") for _ in range(3)]
+            st = torch.cuda.current_stream()
+            st.synchronize()
+            bar.wait()
+            for y in ys_dev:  # several exchanges: box slots and flags cycle
+                c.hg_linear_rowpar(plan, xd, Wd, Wh, bd, y, stream=st)
+            st.synchronize()
+            ys = [y.cpu().numpy() for y in ys_dev]
+            bar.wait()
+            return ys
+        finally:
+            c.close()
+
+    outs = run_ranks(P, rank_fn)
+    for p in range(P):
+        for y in outs[p]:
+            assert np.array_equal(y.view(np.uint32), outs[0][0].view(np.uint32))
+    ok, worst = oracle.within_tol(outs[0][0], ref)
+    assert ok, worst
+    assert oracle.within_tol(outs[0][0], oracle.linear(x, W, b))[0]
+
+
 def run_procs(P, tmp_path, **env):
     """P ranks as processes (tests/peer_worker.py) on GPU 0; returns their npz results."""
     import socket
@@ -167,4 +211,27 @@ def test_peer_stack_mirrored_processes(P, B, tmp_path):
         for name in NAMES:
             _, Wd[name], bd[name] = gen.linear_inputs(seed, l, name, 1, *shapes[name])
         h = oracle.layer(h, Wd, bd, H)["out"]
+    assert oracle.within_tol(oracle.bf16_to_f64(ref), oracle.bf16_to_f64(h), rtol=5e-2)[0]
+
+
+@pytest.mark.parametrize("P,B", [(2, 1), (4, 3), (8, 1)])
+def test_peer_stack_megatron_processes(P, B, tmp_path):
+    """The Megatron pairing (hg_tp = TP_MEGATRON, reading R32) as processes: qkv / fc1 local, o / fc2
+    all-reduced -- 2 exchanges per layer.  Every rank ends with the same bits (twice, and with
+    mirror_glue on or off: the pairing takes the plain path), and the output stays within tolerance of
+    the fp64 oracle's Megatron layer stack (itself pinned to the unsharded layer)."""
+    H, F, NL, seed = (1024, 4096, 2, 73) if P == 8 else (512, 2048, 3, 73)
+    res = run_procs(P, tmp_path, H=H, F=F, NL=NL, B=B, SEED=seed, TP="megatron")
+    ref = res[0]["m1_0"]
+    for r in res:
+        for k in ("m1_0", "m1_1", "m0_0", "m0_1"):
+            assert np.array_equal(r[k], ref), k
+        assert r["m1_stats"][0] == 0 and r["m0_stats"][0] == 0  # no mirrored linears
+    shapes = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
+    h = gen.uniform_bf16(seed + 1, 989, B * H, 1.0).reshape(B, H)
+    for l in range(NL):
+        Wd, bd = {}, {}
+        for name in NAMES:
+            _, Wd[name], bd[name] = gen.linear_inputs(seed, l, name, 1, *shapes[name])
+        h = oracle.megatron_layer(h, Wd, bd, H, P)["out"]
     assert oracle.within_tol(oracle.bf16_to_f64(ref), oracle.bf16_to_f64(h), rtol=5e-2)[0]
