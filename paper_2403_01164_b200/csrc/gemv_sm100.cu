@@ -103,6 +103,7 @@ struct SArgs {
     uint32_t trace_id;
     unsigned long long timeout_ns;
     unsigned long long *stamps;  // measurement (hg_debug_gemv_stamps): [CTA][4] globaltimer or NULL
+    int32_t slot0;               // seq0 % nslots (host-computed: no 64-bit division on the device)
 };
 
 struct Src {
@@ -207,6 +208,30 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
 }
 __device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// W rows read straight into registers (warp-per-row kernel): not through L1 (streamed once; a ring
+// slot's previous occupant must never be served from it), evict-first in L2
+template <int LD>
+__device__ __forceinline__ uint4 ldg_stream_w(const uint4 *p, uint64_t policy) {
+    uint4 r;
+    if (LD == 0)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p));
+    else if (LD == 1)
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p), "l"(policy));
+    else if (LD == 2)
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p), "l"(policy));
+    else
+        asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(p));
+    return r;
 }
 
 __device__ __forceinline__ float lo_f(uint32_t v) { return __uint_as_float(v << 16); }
@@ -490,6 +515,240 @@ constexpr size_t smem_bytes_for(int64_t len) {
     return (size_t)bars_bytes<S>() + (size_t)S * R * len * 2 + (size_t)B * len * 2;
 }
 
+// ---------------------------------------------------------------- warp-per-row kernel (B = 1, K <= 8192)
+//
+// The staged kernel above keeps its W stages in shared memory (3 CTAs x ~70 KB fill an SM) and, back to
+// back, the step's four GEMVs reach ~0.73 of the copy peak.  A plain streaming read over the same byte
+// sequence reaches ~1.0 when every warp holds a whole row in registers and requests it BEFORE
+// griddepcontrol.wait, and ~0.90 with the GEMV's x staging and arithmetic added
+// (tools/probes/read_ceiling.cu, profiles/r02/gemv_row.md).  This kernel is that read:
+//   * a warp owns rows (row groups of R = 1 dealt round-robin over ALL the launch's warps and sources:
+//     first_group with gp = warps) and reads each row straight into registers: lane l holds 16-byte
+//     vectors l, l+32, ... (NV per lane: 14 KB per warp in flight at K = 7168);
+//   * the rows are double buffered by halves: while the first half of a row is multiplied, the first
+//     half of the warp's next row is requested, and likewise the second (the next row may be in a later
+//     chunk if that chunk has landed);
+//   * the first row is requested before griddepcontrol.wait (W never depends on the previous kernel;
+//     x does); then the CTA stages x in shared memory with asynchronous copies;
+//   * arithmetic exactly as the staged kernel's P = 1 form: lane l accumulates its vectors in
+//     ascending order (8 fmaf each), butterfly over the warp -- the same bits for every partition
+//     (split invariance) and as the staged kernel;
+//   * streamed chunks: lane 0 spins on a chunk's arrival tag before the warp reads it -- or passes it
+//     with no rows in it, because the slot's consumption count is per slot, not per chunk: a CTA may
+//     count in for a chunk only after it landed, i.e. after every CTA counted out the slot's previous
+//     occupant.  A warp done with a chunk counts in to a per-CTA shared counter; the CTA's last warp
+//     counts the CTA in to the slot's `consumed` protocol (signal_consumed).
+//   * the prologue never spins on a tag (only a landed chunk is read before the x barrier), and a warp
+//     counts a chunk out before it waits for a later one: no warp holds back the release of a slot
+//     that a chunk it waits for needs.
+// Compile-time FULL (K = 256 NV) keeps the multiply branch-free, so x's shared loads run ahead of the
+// FMAs (a per-vector predicate serialised them: 0.68 -> 0.82 of the copy peak back to back).
+constexpr int kRowWarps = 4;
+constexpr int kRowThreads = kRowWarps * 32;
+constexpr int kRowMaxSrc = 2 + 64;  // resident, zero-copy, up to 64 chunks (more: the staged kernel)
+
+// source() / first_group() for the warp-per-row kernel in 32-bit arithmetic (every warp walks every
+// source; 64-bit modulo is a ~100-instruction software routine).  Row counts < 2^31.
+__device__ __forceinline__ Src row_source(const SArgs &a, int s) {
+    Src r;
+    if (s < 0) {
+        r.base = s == -2 ? a.W_res : a.W_dir;
+        r.rows = s == -2 ? a.n_res : a.n_dir;
+        r.g0 = s == -2 ? 0 : a.n_res;
+        r.slot = -1;
+        r.tag = 0;
+        r.flagged = false;
+    } else {
+        r.slot = (a.slot0 + s) % (int32_t)a.nslots;
+        r.base = a.ring + r.slot * a.slot_bytes;
+        const int64_t r0 = (int64_t)s * a.chunk_rows;
+        r.rows = a.chunk_rows < a.n_str - r0 ? a.chunk_rows : a.n_str - r0;
+        r.g0 = a.n_res + r0;
+        r.tag = (uint32_t)(a.seq0 + s + 1);
+        r.flagged = a.arrived != nullptr;
+    }
+    return r;
+}
+__device__ __forceinline__ int row_first(const SArgs &a, int s, int jw) {
+    const int gb = s == -2 ? 0 : (s == -1 ? (int)a.n_res : (int)(a.n_res + a.n_dir + (int64_t)s * a.chunk_rows));
+    const int m = (jw - gb) % (int)a.gp;
+    return m < 0 ? m + (int)a.gp : m;
+}
+
+template <int LD, int NV>
+__device__ __forceinline__ void row_load(uint4 (&w)[NV], const uint4 *src, int kv, int lane, uint64_t policy) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+        if (lane + 32 * j < kv) w[j] = ldg_stream_w<LD>(src + lane + 32 * j, policy);
+}
+
+// One half of a row: lane l's vectors l + 32 (J0 + j), j < NH, all requested at once.  FULL: every
+// vector exists (K = 32 * 8 * NV); otherwise the ones past the row (v >= kv) are skipped.
+template <bool FULL, int NH>
+__device__ __forceinline__ void half_load(uint4 (&w)[NH], const uint4 *row, int j0, int kv, int lane) {
+#pragma unroll
+    for (int j = 0; j < NH; ++j)
+        if (FULL || lane + 32 * (j0 + j) < kv) w[j] = ldg_stream_w<3>(row + lane + 32 * (j0 + j), 0);
+}
+// acc[b] += the half's vectors against x, in ascending vector order (8 fmaf each, k ascending): the
+// staged kernel's per-lane order.  Branch-free when FULL, so x's shared loads run ahead of the FMAs.
+template <bool FULL, int B, int NH>
+__device__ __forceinline__ void half_fma(float (&acc)[B], const uint4 (&w)[NH], const uint4 *xs, int64_t KV,
+                                         int j0, int kv, int lane) {
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+        const int v = lane + 32 * (j0 + j);
+        if (FULL || v < kv) {
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const uint4 xv = xs[b * KV + v];
+                const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
+                                     lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+                fma8(acc[b], w[j], xf);
+            }
+        }
+    }
+}
+
+// Rows of up to 8192 elements (one part, P = 1): NV vectors of 16 bytes per lane.
+template <int B, int NV, bool FULL>
+__global__ void __launch_bounds__(kRowThreads, 3) gemv_row_kernel(const __grid_constant__ SArgs a) {
+    constexpr int NA = NV / 2, NB = NV - NV / 2;  // the two halves of a row (double buffered)
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint4 *xs = (const uint4 *)smem;  // x [B][K/8]
+    __shared__ uint32_t s_cnt[kRowMaxSrc];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jw = blockIdx.x * kRowWarps + warp;  // this warp's index in the round-robin deal (gp = warps)
+    const int64_t KV = a.K >> 3;
+    const int kv = (int)KV;
+    const int s_begin = a.n_res > 0 ? -2 : (a.n_dir > 0 ? -1 : 0);
+    const int s_end = (int)a.n_chunks;
+    if (a.stamps && threadIdx.x == 0) a.stamps[blockIdx.x * 4 + 0] = globaltimer();
+
+    auto arrived = [&](int s) {  // chunk s has landed (a test, no wait); unflagged sources always
+        const Src src = row_source(a, s);
+        return !src.flagged || (int32_t)(ld_acquire(a.arrived + src.slot) - src.tag) >= 0;
+    };
+    auto wait_arrival = [&](int s) {  // lane 0 spins on chunk s's arrival tag
+        const Src src = row_source(a, s);
+        if (!src.flagged) return;
+        if (lane == 0) {
+            const unsigned long long t0 = globaltimer();
+            while ((int32_t)(ld_acquire(a.arrived + src.slot) - src.tag) < 0) {
+                __nanosleep(64);
+                if (globaltimer() - t0 > a.timeout_ns) {
+                    *(volatile uint32_t *)a.err = 1u;  // mapped host word: a plain store
+                    break;
+                }
+            }
+        }
+        __syncwarp();
+    };
+    // this warp holds nothing more of chunk s: the CTA counts in for the slot once all its warps did
+    auto count_in = [&](int s) {
+        const Src src = row_source(a, s);
+        if (!src.flagged) return;
+        __syncwarp();
+        if (lane == 0 && atomicAdd(&s_cnt[s - s_begin], 1u) == (uint32_t)kRowWarps - 1)
+            signal_consumed(a, src.slot, src.tag);
+    };
+    // the first source at or after s holding a row of this warp (s_end if none), and that row
+    auto first_at = [&](int s, int64_t &gi) {
+        for (; s < s_end; ++s) {
+            gi = row_first(a, s, jw);
+            if (gi < row_source(a, s).rows) return s;
+        }
+        return s_end;
+    };
+    auto row_ptr = [&](int s, int64_t gi) { return (const uint4 *)row_source(a, s).base + gi * KV; };
+
+    uint4 wa[NA], wb[NB];
+    // the first source's row groups start at 0: the warp's first row there is jw itself
+    int s = s_begin;
+    int64_t gi = jw;
+    if (gi >= row_source(a, s).rows) s = first_at(s + 1, gi);
+    // prologue: the first row, if its chunk is already there, is requested before waiting for the
+    // previous grid (W never depends on it; x does).  No spinning here: a warp waiting for a chunk must
+    // not keep its CTA from the x barrier (and so from counting earlier chunks out)
+    bool issued = false;
+    if (s < s_end && arrived(s)) {
+        const uint4 *r = row_ptr(s, gi);
+        half_load<FULL, NA>(wa, r, 0, kv, lane);
+        half_load<FULL, NB>(wb, r, NA, kv, lane);
+        issued = true;
+    }
+    // x is written by an earlier kernel: wait for the previous grid, then stage x (asynchronous
+    // copies, all in flight at once)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int64_t i = threadIdx.x; i < B * KV; i += kRowThreads)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + 16 * i)),
+                     "l"((const uint4 *)a.x + i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\n cp.async.wait_all;" ::: "memory");
+    for (int i = threadIdx.x; i < kRowMaxSrc; i += kRowThreads) s_cnt[i] = 0;
+    __syncthreads();
+
+    for (int q = s_begin; q < s; ++q) {  // chunks before the first row: none of this warp's rows
+        wait_arrival(q);
+        count_in(q);
+    }
+    if (s < s_end && !issued) {
+        wait_arrival(s);
+        const uint4 *r = row_ptr(s, gi);
+        half_load<FULL, NA>(wa, r, 0, kv, lane);
+        half_load<FULL, NB>(wb, r, NA, kv, lane);
+    }
+    bool stamped = false;
+    while (s < s_end) {
+        const Src src = row_source(a, s);
+        // the next row: in this source, else the first of a later source -- requested while this
+        // one is computed unless a chunk up to it has not landed (then this source is finished and
+        // counted out first, and the wait comes after)
+        int64_t gn = gi + a.gp;
+        int sn = s;
+        if (gn >= src.rows) sn = first_at(s + 1, gn);
+        bool ahead = true;
+        for (int q = s + 1; q <= sn && q < s_end && ahead; ++q) ahead = arrived(q);
+        const uint4 *rn = sn < s_end ? row_ptr(sn, gn) : nullptr;
+        const bool pre = ahead && rn;
+        float acc[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = 0.f;
+        half_fma<FULL, B, NA>(acc, wa, xs, KV, 0, kv, lane);
+        if (pre) half_load<FULL, NA>(wa, rn, 0, kv, lane);
+        half_fma<FULL, B, NB>(acc, wb, xs, KV, NA, kv, lane);
+        if (pre) half_load<FULL, NB>(wb, rn, NA, kv, lane);
+#pragma unroll
+        for (int b = 0; b < B; ++b) acc[b] = warp_sum(acc[b]);
+        if (lane == 0) {
+            const int64_t g = src.g0 + gi;
+            const float bb = a.bias ? a.bias[g] : 0.f;
+#pragma unroll
+            for (int b = 0; b < B; ++b) a.y[b * a.ldy + g] = acc[b] + bb;
+            if (a.stamps && warp == 0 && !stamped) a.stamps[blockIdx.x * 4 + 1] = globaltimer();
+        }
+        stamped = true;
+        if (sn != s) {  // done with source s; the ones in between hold no rows of this warp
+            count_in(s);
+            for (int q = s + 1; q < sn; ++q) {
+                if (!ahead) wait_arrival(q);
+                count_in(q);
+            }
+            if (!pre && rn) {
+                wait_arrival(sn);
+                half_load<FULL, NA>(wa, rn, 0, kv, lane);
+                half_load<FULL, NB>(wb, rn, NA, kv, lane);
+            }
+        }
+        s = sn;
+        gi = gn;
+    }
+    if (a.stamps && lane == 0 && warp == 0) a.stamps[blockIdx.x * 4 + 2] = globaltimer();
+}
+
+
+
 // ---------------------------------------------------------------- read-BW probe
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
     uint4 r;
@@ -512,6 +771,70 @@ __global__ void read_bw_kernel(const uint4 *__restrict__ p, int64_t nvec, float 
 int g_sms = 148;
 bool g_pdl = true;            // launch with programmatic stream serialization (HG_GEMV_PDL=0: off)
 bool g_pdl_coop_bad = false;  // set if the driver rejects PDL together with a cooperative launch
+
+int g_row = 1;  // B = 1 takes the warp-per-row kernel (HG_GEMV_ROW=0: the staged kernel, A/B only)
+constexpr int64_t kRowMaxXBytes = 16 * 1024;  // x [B][K] in shared memory (B = 1, K <= 8192: one part)
+
+template <int B, int NV, bool FULL>
+int launch_row_v(SArgs a, cudaStream_t st) {
+    const size_t smem = (size_t)B * a.K * 2;
+    static thread_local int occ = -1;
+    static thread_local size_t occ_smem = 0;
+    if (occ < 0 || occ_smem != smem) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_row_kernel<B, NV, FULL>, kRowThreads, smem) !=
+                cudaSuccess ||
+            occ < 1) {
+            (void)cudaGetLastError();
+            occ = 1;
+        }
+        occ_smem = smem;
+    }
+    const int grid = std::min(occ, 4) * g_sms;  // every CTA resident (a chunk may reuse a slot of this launch)
+    a.gp = grid * kRowWarps;                   // rows are dealt over warps
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kRowThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_row_kernel<B, NV, FULL>, a);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+
+// NV = vectors per lane of a full part (len / 8 / 32, rounded up to an instantiated size)
+template <int B, int NV>
+int launch_row_ld(const SArgs &a, cudaStream_t st) {
+    return (a.K >> 3) == NV * 32 ? launch_row_v<B, NV, true>(a, st) : launch_row_v<B, NV, false>(a, st);
+}
+template <int B>
+int launch_row(const SArgs &a, cudaStream_t st) {
+    const int64_t nv = ((a.len >> 3) + 31) / 32;
+    if (nv <= 4) return launch_row_ld<B, 4>(a, st);
+    if (nv <= 8) return launch_row_ld<B, 8>(a, st);
+    if (nv <= 12) return launch_row_ld<B, 12>(a, st);
+    if (nv <= 16) return launch_row_ld<B, 16>(a, st);
+    if (nv <= 20) return launch_row_ld<B, 20>(a, st);
+    if (nv <= 24) return launch_row_ld<B, 24>(a, st);
+    if (nv <= 28) return launch_row_ld<B, 28>(a, st);
+    return launch_row_ld<B, 32>(a, st);
+}
+
+template <int B, int NV>
+int prepare_row_v() {
+    return (int)cudaFuncSetAttribute(gemv_row_kernel<B, NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kRowMaxXBytes) |
+           (int)cudaFuncSetAttribute(gemv_row_kernel<B, NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kRowMaxXBytes);
+}
+int prepare_row() {
+    return prepare_row_v<1, 4>() | prepare_row_v<1, 8>() | prepare_row_v<1, 12>() | prepare_row_v<1, 16>() |
+           prepare_row_v<1, 20>() | prepare_row_v<1, 24>() | prepare_row_v<1, 28>() | prepare_row_v<1, 32>();
+}
 
 template <int B, int R, int S, int W>
 int launch_v(const SArgs &a, cudaStream_t st) {
@@ -671,9 +994,12 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     a.trace_id = L.trace_id;
     a.timeout_ns = (unsigned long long)(L.timeout_s * 1e9 * dev_timeout_scale());
     a.stamps = g_stamps;
+    a.slot0 = (int32_t)(a.seq0 % a.nslots);
     if (a.P > 1 && (!a.ws || !a.gbar || !a.err || a.gp > kGroupCounters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
+    if (L.batch == 1 && g_row && a.P == 1 && L.K * 2 <= kRowMaxXBytes && a.n_chunks + 2 <= kRowMaxSrc)
+        return launch_row<1>(a, st);
     switch (L.batch) {
         case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
@@ -717,6 +1043,8 @@ int gemv_prepare() {
     if (const char *v = getenv("HG_GEMV_PDL")) g_pdl = atoi(v) != 0;
     if (const char *v = getenv("HG_TC_LONG_K")) g_tc_long_k = atoll(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
+    if (const char *v = getenv("HG_GEMV_ROW")) g_row = atoi(v);
+    e |= prepare_row();
     e |= prepare_b<2>();
     e |= prepare_b<3>();
     e |= prepare_b<4>();
