@@ -276,7 +276,8 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     tc = tcmin > 0 and B >= tcmin
     traffic, traffic_detail = ncu_traffic() if B == 1 else (None, None)
     kernel = ("gemv_tc_stream_kernel (tcgen05 M=128 N=16, TMA 2-D tiles; one persistent launch per linear)" if tc
-              else "gemv_stream_kernel (persistent per-linear GEMV, TMA bulk staged) for K <= 8192; "
+              else "gemv_row_kernel (persistent per-linear GEMV, warp per row, W straight into registers, "
+                   "half-row double buffering, PDL) for K <= 8192; "
                    "gemv_tc_stream_kernel (tcgen05) for the K > 8192 linear (fc2)")
     return {"bound": "hbm", "kernel": kernel,
             "achieved": round(gbps, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4),

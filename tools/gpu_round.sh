@@ -32,12 +32,12 @@ fi
 if has full; then
   # the top kernel: the persistent GEMV inside the timed step (4 launches), and its replay
   timeout 1200 ncu --set full --clock-control none --import-source on --nvtx --nvtx-include "hg_timed/" \
-    -k "regex:gemv_(tc_)?stream" -c 4 -o $out/prof_gemv_step \
+    -k "regex:gemv_(row|stream|tc_stream)" -c 4 -o $out/prof_gemv_step \
     python bench.py --layers 4 --steps 1 --warmup 3 --no-breakdown --no-cpu-baseline --no-abench \
     > $out/full_bench.log 2>&1
   echo "full rc=$?"
   python tools/ncu_summary.py full $out/prof_gemv_step.ncu-rep > $out/full_summary_step.md 2>&1
-  ALPHA=0.24 REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k "regex:gemv_(tc_)?stream" \
+  ALPHA=0.24 REPS=1 timeout 600 ncu --set full --clock-control none --import-source on -k "regex:gemv_(row|stream|tc_stream)" \
     -o $out/prof_gemv_replay python tools/prof_replay.py > $out/full_replay.log 2>&1
   python tools/ncu_summary.py full $out/prof_gemv_replay.ncu-rep > $out/full_summary_replay.md 2>&1
   python tools/ncu_summary.py traffic $out/prof_gemv_replay.ncu-rep 0.24 > $out/ncu_gemv_replay_traffic.json 2>&1
