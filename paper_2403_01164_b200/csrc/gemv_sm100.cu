@@ -749,6 +749,150 @@ __global__ void __launch_bounds__(kRowThreads, 3) gemv_row_kernel(const __grid_c
 
 
 
+
+// ---------------------------------------------------------------- part-row kernel (B = 1, 8192 < K <= 32768)
+//
+// Rows longer than one part (P = ceil(K / 8192) parts of `len` elements, e.g. OPT-30B fc2: 4 x 7168) with
+// the warp-per-row kernel's memory behaviour: a CTA of P warps owns rows (dealt round-robin over the
+// CTAs and all sources), warp p reads part p of the row straight into registers (double buffered by
+// halves, the CTA's next row requested while this one is multiplied; the first before
+// griddepcontrol.wait), and the CTA adds the P part sums in part order, y = (((0 + S_0) + S_1) + ...)
+// + bias -- the staged kernel's workspace fold, so the bits are the same as its P > 1 form.  Chunk tags
+// as the row-group rules: one thread spins / counts the CTA in per chunk.
+constexpr int64_t kPartMaxXBytes = 64 * 1024;  // x (B = 1, K <= 32768: up to 4 parts) in shared memory
+
+template <int NV, bool FULL>
+__global__ void __launch_bounds__(128, 3) gemv_prow_kernel(const __grid_constant__ SArgs a) {
+    constexpr int NA = NV / 2, NB = NV - NV / 2;
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint4 *xs = (const uint4 *)smem;  // x [K/8]
+    __shared__ float s_part[2][4];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;  // warp = part
+    const int64_t K = a.K, KV = K >> 3;
+    const int kvp = (int)(a.len >> 3);
+    const int64_t v0 = (int64_t)warp * kvp;
+    const int kv = (int)(KV - v0 < kvp ? KV - v0 : kvp);  // vectors of this warp's part
+    const int s_begin = a.n_res > 0 ? -2 : (a.n_dir > 0 ? -1 : 0);
+    const int s_end = (int)a.n_chunks;
+    const int G = gridDim.x;
+
+    auto arrived = [&](int t) {
+        const Src src = row_source(a, t);
+        return !src.flagged || (int32_t)(ld_acquire(a.arrived + src.slot) - src.tag) >= 0;
+    };
+    auto spin = [&](int t) {  // one thread spins on chunk t's arrival tag
+        const Src src = row_source(a, t);
+        if (!src.flagged) return;
+        const unsigned long long t0 = globaltimer();
+        while ((int32_t)(ld_acquire(a.arrived + src.slot) - src.tag) < 0) {
+            __nanosleep(64);
+            if (globaltimer() - t0 > a.timeout_ns) {
+                *(volatile uint32_t *)a.err = 1u;
+                break;
+            }
+        }
+    };
+    auto release = [&](int t) {  // this CTA holds nothing more of chunk t (thread 0)
+        const Src src = row_source(a, t);
+        if (src.flagged) signal_consumed(a, src.slot, src.tag);
+    };
+    // this CTA's first row (global row index = rows of earlier sources + r, dealt mod G) at or after row
+    // `from` of source t
+    auto next_at = [&](int t, int64_t from, int &rs, int64_t &rr) {
+        int64_t base = 0;
+        for (int u = s_begin; u < t; ++u) base += row_source(a, u).rows;
+        for (; t < s_end; ++t) {
+            const int64_t nr = row_source(a, t).rows;
+            int64_t first = ((int64_t)blockIdx.x - base) % G;
+            if (first < 0) first += G;
+            if (first < from) first += ((from - first + G - 1) / G) * G;
+            if (first < nr) {
+                rs = t;
+                rr = first;
+                return;
+            }
+            base += nr;
+            from = 0;
+        }
+        rs = s_end;
+        rr = 0;
+    };
+    auto part_ptr = [&](int t, int64_t r) { return (const uint4 *)row_source(a, t).base + r * KV + v0; };
+
+    uint4 wa[NA], wb[NB];
+    int s;
+    int64_t r;
+    next_at(s_begin, 0, s, r);
+    bool issued = false;
+    if (s < s_end && arrived(s)) {
+        const uint4 *pp = part_ptr(s, r);
+        half_load<FULL, NA>(wa, pp, 0, kv, lane);
+        half_load<FULL, NB>(wb, pp, NA, kv, lane);
+        issued = true;
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int64_t i = threadIdx.x; i < KV; i += blockDim.x)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem + 16 * i)),
+                     "l"((const uint4 *)a.x + i)
+                     : "memory");
+    asm volatile("cp.async.commit_group;\n cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0)  // sources before the first row hold none of this CTA's rows
+        for (int t = s_begin; t < s; ++t) {
+            spin(t);
+            release(t);
+        }
+    if (s < s_end && !issued) {
+        if (lane == 0) spin(s);
+        __syncwarp();
+        const uint4 *pp = part_ptr(s, r);
+        half_load<FULL, NA>(wa, pp, 0, kv, lane);
+        half_load<FULL, NB>(wb, pp, NA, kv, lane);
+    }
+    const uint4 *xp = xs + v0;  // this warp's part of x
+    int parity = 0;
+    while (s < s_end) {
+        int sn;
+        int64_t rn;
+        next_at(s, r + 1, sn, rn);
+        bool ahead = true;
+        for (int t = s + 1; t <= sn && t < s_end && ahead; ++t) ahead = arrived(t);
+        const uint4 *pn = sn < s_end ? part_ptr(sn, rn) : nullptr;
+        const bool pre = ahead && pn;
+        float acc[1] = {0.f};
+        half_fma<FULL, 1, NA>(acc, wa, xp, KV, 0, kv, lane);
+        if (pre) half_load<FULL, NA>(wa, pn, 0, kv, lane);
+        half_fma<FULL, 1, NB>(acc, wb, xp, KV, NA, kv, lane);
+        if (pre) half_load<FULL, NB>(wb, pn, NA, kv, lane);
+        const float S = warp_sum(acc[0]);
+        if (lane == 0) s_part[parity][warp] = S;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float sum = 0.f;  // ((0 + S_0) + S_1) + ... : the staged kernel's part fold
+            for (int p = 0; p < a.P; ++p) sum += s_part[parity][p];
+            const int64_t g = row_source(a, s).g0 + r;
+            a.y[g] = sum + (a.bias ? a.bias[g] : 0.f);
+            if (sn != s) {  // done with source s; the ones in between hold none of this CTA's rows
+                release(s);
+                for (int t = s + 1; t < sn; ++t) {
+                    spin(t);
+                    release(t);
+                }
+            }
+        }
+        parity ^= 1;
+        if (!pre && pn) {
+            if (lane == 0) spin(sn);
+            __syncwarp();
+            half_load<FULL, NA>(wa, pn, 0, kv, lane);
+            half_load<FULL, NB>(wb, pn, NA, kv, lane);
+        }
+        s = sn;
+        r = rn;
+    }
+}
+
 // ---------------------------------------------------------------- read-BW probe
 __device__ __forceinline__ uint4 ldg_stream(const uint4 *p) {
     uint4 r;
@@ -805,6 +949,62 @@ int launch_row_v(SArgs a, cudaStream_t st) {
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
+
+
+int g_prow = 1;  // B = 1 rows longer than one part take the part-row kernel (HG_GEMV_PROW=0: off)
+
+template <int NV, bool FULL>
+int launch_prow_v(const SArgs &a, cudaStream_t st) {
+    const size_t smem = (size_t)a.K * 2;
+    static thread_local int occ = -1;
+    static thread_local size_t occ_smem = 0;
+    const int threads = 32 * a.P;
+    if (occ < 0 || occ_smem != smem) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemv_prow_kernel<NV, FULL>, threads, smem) !=
+                cudaSuccess ||
+            occ < 1) {
+            (void)cudaGetLastError();
+            occ = 1;
+        }
+        occ_smem = smem;
+    }
+    const int grid = std::min(occ, 4) * g_sms;  // every CTA resident (a chunk may reuse a slot of this launch)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_pdl ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_prow_kernel<NV, FULL>, a);
+    if (e != cudaSuccess) return (int)e;
+    return (int)cudaGetLastError();
+}
+template <int NV>
+int launch_prow_f(const SArgs &a, cudaStream_t st) {
+    // FULL: every part has NV*32 vectors (K = P * 256 * NV)
+    return a.K == (int64_t)a.P * NV * 256 ? launch_prow_v<NV, true>(a, st) : launch_prow_v<NV, false>(a, st);
+}
+int launch_prow(const SArgs &a, cudaStream_t st) {
+    const int64_t nv = ((a.len >> 3) + 31) / 32;
+    if (nv <= 16) return launch_prow_f<16>(a, st);
+    if (nv <= 24) return launch_prow_f<24>(a, st);
+    if (nv <= 28) return launch_prow_f<28>(a, st);
+    return launch_prow_f<32>(a, st);
+}
+template <int NV>
+int prepare_prow_f() {
+    return (int)cudaFuncSetAttribute(gemv_prow_kernel<NV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kPartMaxXBytes) |
+           (int)cudaFuncSetAttribute(gemv_prow_kernel<NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)kPartMaxXBytes);
+}
+int prepare_prow() { return prepare_prow_f<16>() | prepare_prow_f<24>() | prepare_prow_f<28>() | prepare_prow_f<32>(); }
+// B = 1 rows of 2..4 parts with x in shared memory
+bool prow_fits(int batch, int64_t K) { return batch == 1 && K > 8192 && K * 2 <= kPartMaxXBytes; }
 
 // NV = vectors per lane of a full part (len / 8 / 32, rounded up to an instantiated size)
 template <int B, int NV>
@@ -911,6 +1111,7 @@ void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }
 // depends on (batch, K) only, so every partition of a linear runs the same kernel.
 static int64_t g_tc_long_k = 8192;
 bool gemv_use_tc(int batch, int64_t K) {
+    if (g_prow && prow_fits(batch, K)) return false;  // the part-row kernel (SIMT path)
     return g_tc_ok && g_tc_min_batch > 0 && (batch >= g_tc_min_batch || (g_tc_long_k > 0 && K > g_tc_long_k));
 }
 
@@ -1000,6 +1201,7 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     cudaStream_t st = (cudaStream_t)stream;
     if (L.batch == 1 && g_row && a.P == 1 && L.K * 2 <= kRowMaxXBytes && a.n_chunks + 2 <= kRowMaxSrc)
         return launch_row<1>(a, st);
+    if (g_prow && prow_fits(L.batch, L.K) && a.P <= 4 && a.n_chunks + 2 <= kRowMaxSrc) return launch_prow(a, st);
     switch (L.batch) {
         case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
         case 2: return launch_b<2>(a, st);
@@ -1044,6 +1246,8 @@ int gemv_prepare() {
     if (const char *v = getenv("HG_TC_LONG_K")) g_tc_long_k = atoll(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     if (const char *v = getenv("HG_GEMV_ROW")) g_row = atoi(v);
+    if (const char *v = getenv("HG_GEMV_PROW")) g_prow = atoi(v) != 0;
+    e |= prepare_prow();
     e |= prepare_row();
     e |= prepare_b<2>();
     e |= prepare_b<3>();
