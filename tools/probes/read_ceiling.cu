@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <vector>
 
@@ -235,6 +236,17 @@ int main() {
         }
     double total = 0;
     for (size_t i = 0; i < len.size(); ++i) total += (double)len[i];
+    if (getenv("RC_SINGLE")) {  // one launch per size and kernel, L2 flushed before each (for ncu)
+        for (int k = 0; k < 2; ++k)
+            for (int l = 0; l < 4; ++l) {
+                flush_kernel<<<sms * 4, 512, 0, s>>>(fl, (256 << 20) / 16);
+                Args a{(const uint4 *)(buf + off[l]), len[l] / 16, nullptr, 0, out, 0};
+                CK((cudaError_t)launch(false, a, sms * 4, k == 0 ? 512 : 128, s, k == 1));
+                CK(cudaStreamSynchronize(s));
+            }
+        printf("single launches done\n");
+        return 0;
+    }
     printf("sequence: %d launches, %.1f MB; SMs %d; peak %.1f GB/s\n", (int)len.size(), total / 1e6, sms, peak);
     struct V {
         const char *name;
