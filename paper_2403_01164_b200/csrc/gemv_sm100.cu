@@ -917,7 +917,12 @@ bool g_pdl = true;            // launch with programmatic stream serialization (
 bool g_pdl_coop_bad = false;  // set if the driver rejects PDL together with a cooperative launch
 
 int g_row = 1;  // B = 1 takes the warp-per-row kernel (HG_GEMV_ROW=0: the staged kernel, A/B only)
-constexpr int64_t kRowMaxXBytes = 16 * 1024;  // x [B][K] in shared memory (B = 1, K <= 8192: one part)
+int g_row_bmax = 2;  // batches up to this take it too (HG_ROW_BMAX; B = 2: 0.774 vs tcgen05 0.687, B = 3: 0.656 vs 0.669)
+constexpr int64_t kRowMaxXBytes = 64 * 1024;  // x [B][K] in shared memory (K <= 8192: one part)
+// the warp-per-row kernel takes (batch, K): one part of at most 8192 elements, x in shared memory
+bool row_fits(int batch, int64_t K) {
+    return g_row && batch <= g_row_bmax && K <= 8192 && K % 8 == 0 && (int64_t)batch * K * 2 <= kRowMaxXBytes;
+}
 
 template <int B, int NV, bool FULL>
 int launch_row_v(SArgs a, cudaStream_t st) {
@@ -1031,10 +1036,12 @@ int prepare_row_v() {
            (int)cudaFuncSetAttribute(gemv_row_kernel<B, NV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)kRowMaxXBytes);
 }
-int prepare_row() {
-    return prepare_row_v<1, 4>() | prepare_row_v<1, 8>() | prepare_row_v<1, 12>() | prepare_row_v<1, 16>() |
-           prepare_row_v<1, 20>() | prepare_row_v<1, 24>() | prepare_row_v<1, 28>() | prepare_row_v<1, 32>();
+template <int B>
+int prepare_row_b() {
+    return prepare_row_v<B, 4>() | prepare_row_v<B, 8>() | prepare_row_v<B, 12>() | prepare_row_v<B, 16>() |
+           prepare_row_v<B, 20>() | prepare_row_v<B, 24>() | prepare_row_v<B, 28>() | prepare_row_v<B, 32>();
 }
+int prepare_row() { return prepare_row_b<1>() | prepare_row_b<2>() | prepare_row_b<3>() | prepare_row_b<4>(); }
 
 template <int B, int R, int S, int W>
 int launch_v(const SArgs &a, cudaStream_t st) {
@@ -1112,13 +1119,14 @@ void gemv_set_tc_min_batch(int b) { g_tc_min_batch = b; }
 static int64_t g_tc_long_k = 8192;
 bool gemv_use_tc(int batch, int64_t K) {
     if (g_prow && prow_fits(batch, K)) return false;  // the part-row kernel (SIMT path)
+    if (row_fits(batch, K)) return false;              // the warp-per-row kernel
     return g_tc_ok && g_tc_min_batch > 0 && (batch >= g_tc_min_batch || (g_tc_long_k > 0 && K > g_tc_long_k));
 }
 
 GemvGeom gemv_geom(int64_t K, int batch) {
     if (gemv_use_tc(batch, K)) return gemv_tc_geom(K);
     GemvGeom g;
-    const int64_t pm = part_max(batch);
+    const int64_t pm = row_fits(batch, K) ? 8192 : part_max(batch);  // the row kernel: one part
     const int64_t P = (K + pm - 1) / pm;
     int64_t len = (K + P - 1) / P;
     len = (len + 7) / 8 * 8;
@@ -1199,8 +1207,13 @@ int launch_gemv_stream(const StreamLaunch &L, void *stream) {
     if (a.P > 1 && (!a.ws || !a.gbar || !a.err || a.gp > kGroupCounters)) return (int)cudaErrorInvalidValue;
     if (a.arrived && (!a.consumed || !a.slot_cnt || !a.err)) return (int)cudaErrorInvalidValue;
     cudaStream_t st = (cudaStream_t)stream;
-    if (L.batch == 1 && g_row && a.P == 1 && L.K * 2 <= kRowMaxXBytes && a.n_chunks + 2 <= kRowMaxSrc)
-        return launch_row<1>(a, st);
+    if (row_fits(L.batch, L.K) && a.P == 1 && a.n_chunks + 2 <= kRowMaxSrc) switch (L.batch) {
+            case 1: return launch_row<1>(a, st);
+            case 2: return launch_row<2>(a, st);
+            case 3: return launch_row<3>(a, st);
+            case 4: return launch_row<4>(a, st);
+            default: break;
+        }
     if (g_prow && prow_fits(L.batch, L.K) && a.P <= 4 && a.n_chunks + 2 <= kRowMaxSrc) return launch_prow(a, st);
     switch (L.batch) {
         case 1: return cps > 1 ? launch_v<1, 1, 4, 4>(a, st) : launch_b<1>(a, st);
@@ -1246,6 +1259,7 @@ int gemv_prepare() {
     if (const char *v = getenv("HG_TC_LONG_K")) g_tc_long_k = atoll(v);
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     if (const char *v = getenv("HG_GEMV_ROW")) g_row = atoi(v);
+    if (const char *v = getenv("HG_ROW_BMAX")) g_row_bmax = atoi(v);
     if (const char *v = getenv("HG_GEMV_PROW")) g_prow = atoi(v) != 0;
     e |= prepare_prow();
     e |= prepare_row();
