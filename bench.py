@@ -272,13 +272,15 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     if tot_time <= 0:
         return None
     gbps = tot_bytes / tot_time / 1e9
-    tcmin = ctx.config.gemv_tc_min_batch
-    tc = tcmin > 0 and B >= tcmin
     traffic, traffic_detail = ncu_traffic() if B == 1 else (None, None)
-    kernel = ("gemv_tc_stream_kernel (tcgen05 M=128 N=16, TMA 2-D tiles; one persistent launch per linear)" if tc
-              else "gemv_row_kernel (persistent per-linear GEMV, warp per row, W straight into registers, "
-                   "half-row double buffering, PDL) for K <= 8192; "
-                   "gemv_tc_stream_kernel (tcgen05) for the K > 8192 linear (fc2)")
+    # which kernel each linear runs (the library's choice depends on (batch, K) only; R26)
+    if B <= 2:
+        kernel = ("gemv_row_kernel (persistent per-linear GEMV, warp per row, W straight into registers, "
+                  "half-row double buffering, PDL) for K <= 8192; "
+                  + ("gemv_prow_kernel (a CTA of P warps per row, parts in registers) for fc2 (K = 28672)" if B == 1
+                     else "gemv_tc_stream_kernel (tcgen05) for fc2 (K = 28672)"))
+    else:
+        kernel = "gemv_tc_stream_kernel (tcgen05 M=128 N=16, TMA 2-D tiles; one persistent launch per linear)"
     return {"bound": "hbm", "kernel": kernel,
             "achieved": round(gbps, 1), "peak": hbm_peak, "unit": "GB/s", "frac": round(gbps / hbm_peak, 4),
             "traffic": traffic, "traffic_detail": traffic_detail,
