@@ -261,6 +261,27 @@ def test_tags_ring_smaller_than_linear(B):
             assert ok, (n_res, alpha, worst)
 
 
+@pytest.mark.parametrize("B,K", [(1, 7168), (2, 7168), (1, 12288), (1, 28672)])
+def test_tags_ring_smaller_than_linear_row_kernels(B, K):
+    """The warp-per-row (B <= 2, K <= 8192) and part-row (B = 1, K <= 32768) kernels with the ring
+    smaller than the linear (3 slots, >= 9 chunks refilled inside one launch): a warp / CTA counts a
+    chunk out only after it landed (the per-slot count must not mix occupants), with rows of this
+    launch's warps in only some of the chunks; results match the oracle and equal a roomy ring's bits."""
+    N = 1280
+    row = 2 * K
+    chunk = 128 * row  # 128 rows per chunk: most warps have no row in most chunks
+    x, W, b = gen.linear_inputs(35, 0, "fc1", B, N, K)
+    ys = []
+    for ring in (3 * chunk, 64 * chunk):
+        with hg.Context(0, chunk_bytes=chunk, ring_bytes=ring, max_k=K, max_n=N, timeout_s=20.0) as c:
+            for n_res, alpha in ((0, 1.0), (128, 0.8)):
+                y = _linear(c, x, W, b, B, n_res, alpha)
+                ok, worst = oracle.within_tol(y, oracle.linear(x, W, b))
+                assert ok, (ring, n_res, alpha, worst)
+                ys.append(y)
+    assert np.array_equal(ys[0], ys[2]) and np.array_equal(ys[1], ys[3])  # same kernel, same bits
+
+
 @pytest.mark.parametrize("B", [1, 2, 4, 8])
 def test_event_path_equals_tag_path(ctx, B):
     """handshake=0 (host events, one GEMV per chunk) and the default device-tag pipeline compute
