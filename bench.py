@@ -274,9 +274,9 @@ def gemv_roofline(ctx, plans, layers, B, torch, pk, iters=20, W_dev=None):
     gbps = tot_bytes / tot_time / 1e9
     traffic, traffic_detail = ncu_traffic() if B == 1 else (None, None)
     # which kernel each linear runs (the library's choice depends on (batch, K) only; R26)
-    if B <= 2:
+    if B <= 3:
         kernel = ("gemv_row_kernel (persistent per-linear GEMV, warp per row, W straight into registers, "
-                  "half-row double buffering, PDL) for K <= 8192; "
+                  "half-row double buffering, bf16 FMA, PDL) for K <= 8192; "
                   + ("gemv_prow_kernel (a CTA of P warps per row, parts in registers) for fc2 (K = 28672)" if B == 1
                      else "gemv_tc_stream_kernel (tcgen05) for fc2 (K = 28672)"))
     else:

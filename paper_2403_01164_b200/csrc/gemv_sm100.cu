@@ -248,6 +248,24 @@ __device__ __forceinline__ void fma8(float &acc, const uint4 &w, const float (&x
     acc = fmaf(hi_f(w.w), xf[7], acc);
 }
 
+
+// acc += w[e] * x[e] for the 8 bf16 pairs of two 16-byte vectors, e ascending: fma.rn.f32.bf16 takes the
+// bf16 halves of the packed registers as they are (FHFMA.BF16 on sm_100: no conversion instructions).  A
+// bf16 x bf16 product is exact in fp32 and the add rounds once, so this is fmaf(f32(w), f32(x), acc) --
+// the same bits as fma8 with the conversions written out.
+__device__ __forceinline__ void fma_bf16(float &acc, uint32_t w, uint32_t x) {
+    const unsigned short wl = (unsigned short)(w & 0xffffu), wh = (unsigned short)(w >> 16);
+    const unsigned short xl = (unsigned short)(x & 0xffffu), xh = (unsigned short)(x >> 16);
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc) : "h"(wl), "h"(xl));
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(acc) : "h"(wh), "h"(xh));
+}
+__device__ __forceinline__ void fma8_bf16(float &acc, const uint4 &w, const uint4 &x) {
+    fma_bf16(acc, w.x, x.x);
+    fma_bf16(acc, w.y, x.y);
+    fma_bf16(acc, w.z, x.z);
+    fma_bf16(acc, w.w, x.w);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -600,12 +618,7 @@ __device__ __forceinline__ void half_fma(float (&acc)[B], const uint4 (&w)[NH], 
         const int v = lane + 32 * (j0 + j);
         if (FULL || v < kv) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) {
-                const uint4 xv = xs[b * KV + v];
-                const float xf[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
-                                     lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
-                fma8(acc[b], w[j], xf);
-            }
+            for (int b = 0; b < B; ++b) fma8_bf16(acc[b], w[j], xs[b * KV + v]);
         }
     }
 }
@@ -917,7 +930,7 @@ bool g_pdl = true;            // launch with programmatic stream serialization (
 bool g_pdl_coop_bad = false;  // set if the driver rejects PDL together with a cooperative launch
 
 int g_row = 1;  // B = 1 takes the warp-per-row kernel (HG_GEMV_ROW=0: the staged kernel, A/B only)
-int g_row_bmax = 2;  // batches up to this take it too (HG_ROW_BMAX; B = 2: 0.774 vs tcgen05 0.687, B = 3: 0.656 vs 0.669)
+int g_row_bmax = 3;  // batches up to this take it too (HG_ROW_BMAX; B = 2 / 3 / 4: 0.78 / 0.71 / 0.63 vs tcgen05 0.69 / 0.67 / 0.65)
 constexpr int64_t kRowMaxXBytes = 64 * 1024;  // x [B][K] in shared memory (K <= 8192: one part)
 // the warp-per-row kernel takes (batch, K): one part of at most 8192 elements, x in shared memory
 bool row_fits(int batch, int64_t K) {

@@ -38,9 +38,13 @@ print("BAD" if bad else "OK", bad)
     {"HG_TC_LONG_K": "0"},
     {"HG_GEMV_PDL": "0"},
     {"HG_TC_STREAM": "0"},
-    {"HG_GEMV_CPS": "1"},
     {"HG_GEMV_TC_MIN_BATCH": "0"},
     {"HG_TC_CLUSTER": "0"},
+    {"HG_GEMV_ROW": "0"},
+    {"HG_GEMV_ROW": "0", "HG_GEMV_CPS": "1"},
+    {"HG_GEMV_PROW": "0"},
+    {"HG_ROW_BMAX": "1"},
+    {"HG_ROW_BMAX": "4"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_keeps_parity(env):
     code = SCRIPT % {"root": ROOT, "tests": os.path.join(ROOT, "tests")}
