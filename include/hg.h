@@ -143,8 +143,12 @@ typedef struct {
     int32_t collect_stats; /* 1 = time every chunk copy / GEMV with CUDA events          */
     int32_t wrap_prefetch; /* 1 = hg_stack keeps streaming the next call's first chunks */
     double timeout_s;    /* bound on every host wait (default 60 s)                      */
-    int32_t gemv_tc_min_batch; /* batches >= this use the tcgen05 GEMV (default 2; 0 = never); below it,
-                                  rows with K > 8192 also do (HG_TC_LONG_K=0 turns that off) */
+    int32_t gemv_tc_min_batch; /* batches >= this may use the tcgen05 GEMV (default 2; 0 = never);
+                                  the kernel per (batch, K): B <= 3 and K <= 8192 the warp-per-row
+                                  kernel, B = 1 and K <= 32768 the part-row kernel, otherwise tcgen05
+                                  from this batch on (below it, or with 0, the staged SIMT kernel);
+                                  below it rows with K > 8192 also take tcgen05 where the part-row
+                                  kernel does not apply (HG_TC_LONG_K=0 turns that off) */
     int32_t handshake;   /* streamed-chunk synchronisation: 1 = device tags (default): the copy
                             stream writes an arrival tag per chunk (cuStreamWriteValue32) and waits
                             on the slot's consumed tag (cuStreamWaitValue32), one persistent GEMV
@@ -158,9 +162,9 @@ typedef struct {
     int32_t verify_mirror; /* 1: after every mirrored glue step compare the host activation with
                             the device one (synchronising; tests) -> hg_stats.mirror_mismatch     */
     int32_t stream_mode; /* how the streamed slice reaches the SMs: 0 (default) = copy-engine chunks
-                            through the device ring; 1 = zero-copy: the GEMV's TMA bulk copies read
-                            the pinned host rows over the link directly (no ring, no tags; SIMT
-                            batches only -- tcgen05 batches keep mode 0)                          */
+                            through the device ring; 1 = zero-copy: the GEMV reads the pinned host
+                            rows over the link directly (no ring, no tags; SIMT kernels only --
+                            tcgen05 batches keep mode 0)                                          */
     int32_t pageable;    /* 1: W_host may be pageable (not page-locked): streamed chunks of such
                             weights go through the pin lane -- the asynchronous parameter manager of
                             Sec. 4.3 -- into a pinned staging ring; 0 (default): HG_ENOTPINNED     */
@@ -445,8 +449,9 @@ HG_API hg_status hg_gemv_replay(hg_ctx *ctx, const hg_plan_t *plan, const void *
                                 void *stream);
 
 /* Measurement only (tools/gemv_latency.py): from now on every SIMT GEMV launch of this process
- * writes four globaltimer stamps (ns) per CTA -- [cta*4 + 0] entry, [1] first stage full in
- * consumer warp 0, [2] consumer warp 0 done, [3] producer done -- into a mapped pinned host
+ * writes globaltimer stamps (ns) per CTA -- staged kernel: [cta*4 + 0] entry, [1] first stage full
+ * in consumer warp 0, [2] consumer warp 0 done, [3] producer done; warp-per-row kernel: [0] entry,
+ * [1] warp 0's first row written, [2] warp 0 done -- into a mapped pinned host
  * array of 4096*4 uint64 owned by the library (never freed); *out receives its host address.
  * out == NULL turns the stamps off again.
  * Stamps slow each launch slightly (posted writes over the host link); never on in the bench. */
