@@ -20,7 +20,8 @@ def launches(path):
         if r.get("Metric Name") == "gpu__time_duration.sum":
             v = float(r["Metric Value"].replace(",", ""))
             unit = r.get("Metric Unit", "")
-            scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3,
+                     "second": 1e6, "s": 1e6}.get(unit, 1.0)
             rows.append((r["Kernel Name"], v * scale))
     tot = sum(t for _, t in rows) or 1.0
     agg = defaultdict(lambda: [0, 0.0])
