@@ -437,6 +437,26 @@ __global__ void __launch_bounds__(threads_for<kConsumerWarps>(), 1) gemv_stream_
             for (int q = 0; q < R; ++q)
 #pragma unroll
                 for (int b = 0; b < B; ++b) acc[q][b] = 0.f;
+            if constexpr (B == 1 && R == 1) {  // four running sums, vector t -> sum t mod 4 (reading R33)
+                float a4[4] = {0.f, 0.f, 0.f, 0.f};
+                auto step = [&](float &acc1, int vv) {
+                    const uint4 xv = xs[vv];
+                    const float xf1[8] = {lo_f(xv.x), hi_f(xv.x), lo_f(xv.y), hi_f(xv.y),
+                                          lo_f(xv.z), hi_f(xv.z), lo_f(xv.w), hi_f(xv.w)};
+                    fma8(acc1, sw[vv], xf1);
+                };
+                int v = lane;
+                for (; v + 96 < kv; v += 128) {
+                    step(a4[0], v);
+                    step(a4[1], v + 32);
+                    step(a4[2], v + 64);
+                    step(a4[3], v + 96);
+                }
+                if (v < kv) step(a4[0], v);
+                if (v + 32 < kv) step(a4[1], v + 32);
+                if (v + 64 < kv) step(a4[2], v + 64);
+                acc[0][0] = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+            } else
             for (int v = lane; v < kv; v += 32) {
                 float xf[B][8];
 #pragma unroll
@@ -610,17 +630,26 @@ __device__ __forceinline__ void half_load(uint4 (&w)[NH], const uint4 *row, int 
 }
 // acc[b] += the half's vectors against x, in ascending vector order (8 fmaf each, k ascending): the
 // staged kernel's per-lane order.  Branch-free when FULL, so x's shared loads run ahead of the FMAs.
-template <bool FULL, int B, int NH>
-__device__ __forceinline__ void half_fma(float (&acc)[B], const uint4 (&w)[NH], const uint4 *xs, int64_t KV,
-                                         int j0, int kv, int lane) {
+// At B = 1 vector j of the lane (ascending) goes to running sum j mod 4 -- four independent chains of
+// fused multiply-adds instead of one (when a row's last data lands, 56 dependent FMAs instead of 224);
+// the lane total is ((s_0 + s_1) + (s_2 + s_3)), the staged kernel's order at B = 1 (reading R33).  From
+// B = 2 the B rows of x already give independent chains: one running sum per batch row.
+template <bool FULL, int B, int NH, int J0>
+__device__ __forceinline__ void half_fma(float (&acc)[B][4], const uint4 (&w)[NH], const uint4 *xs, int64_t KV,
+                                         int kv, int lane) {
 #pragma unroll
     for (int j = 0; j < NH; ++j) {
-        const int v = lane + 32 * (j0 + j);
+        const int v = lane + 32 * (J0 + j);
         if (FULL || v < kv) {
 #pragma unroll
-            for (int b = 0; b < B; ++b) fma8_bf16(acc[b], w[j], xs[b * KV + v]);
+            for (int b = 0; b < B; ++b) fma8_bf16(acc[b][B == 1 ? (J0 + j) & 3 : 0], w[j], xs[b * KV + v]);
         }
     }
+}
+template <int B>
+__device__ __forceinline__ void lane_total(float (&acc)[B][4], float (&out)[B]) {
+#pragma unroll
+    for (int b = 0; b < B; ++b) out[b] = B == 1 ? (acc[b][0] + acc[b][1]) + (acc[b][2] + acc[b][3]) : acc[b][0];
 }
 
 // Rows of up to 8192 elements (one part, P = 1): NV vectors of 16 bytes per lane.
@@ -725,13 +754,14 @@ __global__ void __launch_bounds__(kRowThreads, 3) gemv_row_kernel(const __grid_c
         for (int q = s + 1; q <= sn && q < s_end && ahead; ++q) ahead = arrived(q);
         const uint4 *rn = sn < s_end ? row_ptr(sn, gn) : nullptr;
         const bool pre = ahead && rn;
-        float acc[B];
+        float acc4[B][4], acc[B];
 #pragma unroll
-        for (int b = 0; b < B; ++b) acc[b] = 0.f;
-        half_fma<FULL, B, NA>(acc, wa, xs, KV, 0, kv, lane);
+        for (int b = 0; b < B; ++b) acc4[b][0] = acc4[b][1] = acc4[b][2] = acc4[b][3] = 0.f;
+        half_fma<FULL, B, NA, 0>(acc4, wa, xs, KV, kv, lane);
         if (pre) half_load<FULL, NA>(wa, rn, 0, kv, lane);
-        half_fma<FULL, B, NB>(acc, wb, xs, KV, NA, kv, lane);
+        half_fma<FULL, B, NB, NA>(acc4, wb, xs, KV, kv, lane);
         if (pre) half_load<FULL, NB>(wb, rn, NA, kv, lane);
+        lane_total<B>(acc4, acc);
 #pragma unroll
         for (int b = 0; b < B; ++b) acc[b] = warp_sum(acc[b]);
         if (lane == 0) {
@@ -873,11 +903,12 @@ __global__ void __launch_bounds__(128, 3) gemv_prow_kernel(const __grid_constant
         for (int t = s + 1; t <= sn && t < s_end && ahead; ++t) ahead = arrived(t);
         const uint4 *pn = sn < s_end ? part_ptr(sn, rn) : nullptr;
         const bool pre = ahead && pn;
-        float acc[1] = {0.f};
-        half_fma<FULL, 1, NA>(acc, wa, xp, KV, 0, kv, lane);
+        float acc4[1][4] = {{0.f, 0.f, 0.f, 0.f}}, acc[1];
+        half_fma<FULL, 1, NA, 0>(acc4, wa, xp, KV, kv, lane);
         if (pre) half_load<FULL, NA>(wa, pn, 0, kv, lane);
-        half_fma<FULL, 1, NB>(acc, wb, xp, KV, NA, kv, lane);
+        half_fma<FULL, 1, NB, NA>(acc4, wb, xp, KV, kv, lane);
         if (pre) half_load<FULL, NB>(wb, pn, NA, kv, lane);
+        lane_total<1>(acc4, acc);
         const float S = warp_sum(acc[0]);
         if (lane == 0) s_part[parity][warp] = S;
         __syncthreads();
