@@ -348,10 +348,8 @@ def placement(args, world, local):
     return node, per, (same.index(local) * per) if world > 1 else -1
 
 
-def make_context(args, rank, world, local, **extra):
-    """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores (those
-    of its GPU's NUMA node when known, SURVEY 8(e))."""
-    from paper_2403_01164_b200 import hg
+def pool_placement(args, world, local):
+    """(NUMA node, cores per rank, first core the CPU-lane pool's workers are pinned from or -1, threads)."""
     node, per, first = placement(args, world, local)
     pin_threads = 4 if args.pageable else 0  # the pin lane's memcpy threads get their own cores
     # leave cores for the API thread (it enqueues the GPU lanes and joins the CPU rows) and the CUDA
@@ -360,6 +358,22 @@ def make_context(args, rank, world, local, **extra):
     # the slow runs with the link at ~46 GB/s -- profiles/r01/threads.md)
     reserve = 2 if per >= 12 else (1 if per >= 4 else 0)
     threads = args.threads or max(1, per - pin_threads - reserve)
+    if world == 1 and first < 0 and args.numa != "off" and reserve == 2 and not args.pageable:
+        # one rank: the pool's workers pinned to the last cores, the first ones left to the API thread,
+        # the driver and the clock sampler (A/B on one box: 283.7 / 281.0 / 278.3 pinned against
+        # 283.2 / 290.0 / 280.6 unpinned, the unpinned runs with p90 up to 307.7 -- profiles/r02/pin_ab.txt)
+        first = per - threads
+    if os.environ.get("HG_BENCH_PIN"):  # development A/B (-1: no pinning)
+        first = int(os.environ["HG_BENCH_PIN"])
+    return node, per, first, threads
+
+
+def make_context(args, rank, world, local, **extra):
+    """The bench's hg context: one per rank, its CPU lane on this rank's share of the host cores (those
+    of its GPU's NUMA node when known, SURVEY 8(e))."""
+    from paper_2403_01164_b200 import hg
+    node, per, first, threads = pool_placement(args, world, local)
+    pin_threads = 4 if args.pageable else 0
     cfg = dict(cpu_threads=threads, cpu_first=first, numa_node=node if first >= 0 else -1,
                chunk_bytes=args.chunk_mb << 20, ring_bytes=args.ring_mb << 20,
                max_k=F, max_n=F, wrap_prefetch=1, collect_stats=0,
@@ -447,7 +461,7 @@ def prepare(args, weights=None, **ctx_extra):
     return {"torch": torch, "dist": dist, "hg": hg, "rank": rank, "world": world, "local": local,
             "threads": threads, "ctx": ctx, "B": B, "host": host, "biases": biases, "biases_h": biases_h,
             "rates": rates, "t_setup": t_setup, "h_host": h_host, "h_dev": h_host.cuda(),
-            "placement": placement(args, world, local),
+            "placement": pool_placement(args, world, local)[:3],
             "h_out": torch.empty_like(h_host, pin_memory=True), "stream": torch.cuda.Stream(), "v_kind": None}
 
 
