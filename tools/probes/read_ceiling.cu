@@ -174,6 +174,34 @@ __global__ void __launch_bounds__(128, 3) gemv_like(const __grid_constant__ Args
     }
 }
 
+
+// thread-per-row: lane i of a warp streams row (32 w + i) in 64 B steps (4 x 16 B loads, all in flight
+// for NS steps) -- the access pattern of loading a W tile row-per-thread for tcgen05.st (TMEM lane = row)
+template <int NS, bool CACHE>
+__global__ void __launch_bounds__(128) tpr_kernel(const __grid_constant__ Args a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int64_t rowbytes = 14336;  // K = 7168 bf16
+    const int64_t rows = a.n16 * 16 / rowbytes;
+    const int64_t tiles = rows / 128;
+    uint32_t acc = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const char *row = (const char *)a.p + (t * 128 + threadIdx.x) * rowbytes;
+        for (int64_t k = 0; k < rowbytes; k += 64 * NS) {
+            uint4 v[4 * NS];
+#pragma unroll
+            for (int j = 0; j < 4 * NS; ++j) {
+                const uint4 *q = (const uint4 *)(row + k) + j;
+                if (CACHE) v[j] = *q;
+                else v[j] = ldnc(q);
+            }
+#pragma unroll
+            for (int j = 0; j < 4 * NS; ++j) acc ^= v[j].x ^ v[j].w;
+        }
+        if (t == blockIdx.x) asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
+    if (acc == 0x12345678u) a.out[blockIdx.x] = acc;
+}
+
 __global__ void flush_kernel(uint4 *p, int64_t n16) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = make_uint4((uint32_t)i, 0, 0, 0);
@@ -191,7 +219,7 @@ int launch(bool pdl, const Args &a, int grid, int block, cudaStream_t s, bool ro
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl ? 1 : 0;
-    if (gmode >= 0) {
+    if (gmode >= 0 && gmode < 10) {
         cfg.dynamicSmemBytes = gmode == 3 ? 28672 : 14336;
         switch (gmode) {
             case 0: return (int)cudaLaunchKernelEx(&cfg, gemv_like<0, 28>, a, g_x, g_y);
@@ -200,6 +228,9 @@ int launch(bool pdl, const Args &a, int grid, int block, cudaStream_t s, bool ro
             default: return (int)cudaLaunchKernelEx(&cfg, gemv_like<3, 28>, a, g_x, g_y);
         }
     }
+    if (gmode == 10) return (int)cudaLaunchKernelEx(&cfg, tpr_kernel<2, false>, a);
+    if (gmode == 11) return (int)cudaLaunchKernelEx(&cfg, tpr_kernel<2, true>, a);
+    if (gmode == 12) return (int)cudaLaunchKernelEx(&cfg, tpr_kernel<4, true>, a);
     if (rowk) return (int)cudaLaunchKernelEx(&cfg, row_kernel<28>, a);
     return (int)(pdl ? cudaLaunchKernelEx(&cfg, read_kernel<true>, a) : cudaLaunchKernelEx(&cfg, read_kernel<false>, a));
 }
@@ -273,6 +304,10 @@ int main() {
         {"row 4x128 no wait", true, 0, 4, 128, 0, true},
         {"gemv-like xor+x 3x128", true, 0, 3, 128, 1, false, false, 0},
         {"gemv-like fma 3x128", true, 0, 3, 128, 1, false, false, 1},
+        {"thread/row nc 2x64B 4x128", true, 0, 4, 128, 0, false, false, 10},
+        {"thread/row L1 2x64B 4x128", true, 0, 4, 128, 0, false, false, 11},
+        {"thread/row L1 4x64B 4x128", true, 0, 4, 128, 0, false, false, 12},
+        {"thread/row L1 4x64B 8x128", true, 0, 8, 128, 0, false, false, 12},
         {"gemv-like fma4acc 3x128", true, 0, 3, 128, 1, false, false, 2},
         {"gemv-like fma xf32 3x128", true, 0, 3, 128, 1, false, false, 3},
         {"gemv-like fma 4x128", true, 0, 4, 128, 1, false, false, 1},
