@@ -1,8 +1,14 @@
 // gemv_sm100.cu -- the GPU lanes of a heterogeneous linear:
-//   y[b, j] = sum_k x[b,k] * W[j,k] (+ bias[j]),   B = 1..8 (SIMT; tcgen05 for B >= 5 lives in
-//   gemv_tc_sm100.cu).
+//   y[b, j] = sum_k x[b,k] * W[j,k] (+ bias[j]),   B = 1..8.
 //
-// One persistent launch per linear covers BOTH GPU lanes: the HBM-resident rows
+// The SIMT kernels (the tcgen05 kernel lives in gemv_tc_sm100.cu); the choice depends on (B, K) only
+// (gemv_use_tc, row_fits, prow_fits; R26):
+//   * gemv_row_kernel  -- B <= 3, K <= 8192: a warp per row, W straight into registers (the default);
+//   * gemv_prow_kernel -- B = 1, 8192 < K <= 32768: a CTA of P warps per row, one part each;
+//   * gemv_stream_kernel -- the staged kernel below (TMA bulk copies into shared-memory stages): the
+//     fallback (tcgen05 off, more than 64 chunks, HG_GEMV_ROW=0) and the bit reference of the first two.
+//
+// Staged kernel.  One persistent launch per linear covers BOTH GPU lanes: the HBM-resident rows
 // [0, n_res) and every streamed chunk of rows [n_res, n_res+n_str) as it lands in
 // the device ring ("The GPU, in turn, generates results once the
 // communication process is completed"; the overlap of Fig. 5c).  At batch
