@@ -566,15 +566,15 @@ bool make_map(CUtensorMap *m, const void *ptr, int64_t inner, int64_t outer, uin
 
 int g_num_sms = 0;
 
-template <int B>
-int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
+template <int B, int ST>
+int launch_tc_stream_st(const TcArgs &a, cudaStream_t st) {
     const int sms = g_num_sms > 0 ? g_num_sms : 148;
     int grid = 2 * sms;  // two 6-stage CTAs per SM (2 x ~112 KB smem)
     if (a.U < grid) grid = (int)a.U;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem_for(kStagesWide);
+    cfg.dynamicSmemBytes = smem_for(ST);
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -589,9 +589,19 @@ int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, kStagesWide>, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, gemv_tc_stream_kernel<B, ST>, a);
     if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
+}
+// From B = 5, 4-stage CTAs (2 x ~76 KB per SM) leave room for a CTA of the NEXT launch on every SM, so
+// back-to-back launches overlap (programmatic dependent launch) and the HBM stream does not drain at the
+// boundary: B = 6 / 8 0.63 / 0.62 -> 0.66 / 0.65; at B = 4 the extra bytes in flight of 6 stages win
+// (0.65-0.67 vs 0.64; profiles/r02/tc_stages.md).  HG_TC_ST=4|6 forces one.
+static const int g_tc_st = getenv("HG_TC_ST") ? atoi(getenv("HG_TC_ST")) : 0;
+template <int B>
+int launch_tc_stream_b(const TcArgs &a, cudaStream_t st) {
+    const bool four = g_tc_st == 4 || (g_tc_st == 0 && B >= 5);
+    return four ? launch_tc_stream_st<B, 4>(a, st) : launch_tc_stream_st<B, kStagesWide>(a, st);
 }
 
 template <int B>
@@ -601,6 +611,9 @@ int prepare_tc_b() {
     // clusters of up to 16 CTAs (one per k-slice of a tile): above the portable 8
     e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, kStagesWide>,
                                    cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem_for(4));
+    e |= (int)cudaFuncSetAttribute(gemv_tc_stream_kernel<B, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     return e;
 }
 
