@@ -970,8 +970,12 @@ int g_row = 1;  // B = 1 takes the warp-per-row kernel (HG_GEMV_ROW=0: the stage
 int g_row_bmax = 3;  // batches up to this take it too (HG_ROW_BMAX; B = 2 / 3 / 4: 0.78 / 0.71 / 0.63 vs tcgen05 0.69 / 0.67 / 0.65)
 constexpr int64_t kRowMaxXBytes = 64 * 1024;  // x [B][K] in shared memory (K <= 8192: one part)
 // the warp-per-row kernel takes (batch, K): one part of at most 8192 elements, x in shared memory
+// B = 4 rows of K <= 5120 take it too: OPT-13B (H = 5120) at B = 4 0.505 vs tcgen05's 0.431 back to back,
+// OPT-6.7B 0.421 vs 0.405, while OPT-30B's K = 7168 stays on tcgen05 (0.63 vs 0.66; profiles/r02/gemv_row.md)
+int g_row_b4_kmax = 5120;
 bool row_fits(int batch, int64_t K) {
-    return g_row && batch <= g_row_bmax && K <= 8192 && K % 8 == 0 && (int64_t)batch * K * 2 <= kRowMaxXBytes;
+    const bool b_ok = batch <= std::min(g_row_bmax, 4) || (batch == 4 && K <= g_row_b4_kmax);
+    return g_row && b_ok && K <= 8192 && K % 8 == 0 && (int64_t)batch * K * 2 <= kRowMaxXBytes;
 }
 
 template <int B, int NV, bool FULL>
@@ -1310,6 +1314,7 @@ int gemv_prepare() {
     if (const char *v = getenv("HG_GEMV_CPS")) g_cps1 = atoi(v) >= 2 ? (atoi(v) >= 3 ? 3 : 2) : 1;
     if (const char *v = getenv("HG_GEMV_ROW")) g_row = atoi(v);
     if (const char *v = getenv("HG_ROW_BMAX")) g_row_bmax = atoi(v);
+    if (const char *v = getenv("HG_ROW_B4_KMAX")) g_row_b4_kmax = atoi(v);
     if (const char *v = getenv("HG_GEMV_PROW")) g_prow = atoi(v) != 0;
     e |= prepare_prow();
     e |= prepare_row();

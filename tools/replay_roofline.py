@@ -12,7 +12,7 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 from paper_2403_01164_b200 import hg  # noqa: E402
 
-H, F = 7168, 28672
+H, F = int(os.environ.get("H", 7168)), int(os.environ.get("F", 0)) or 4 * int(os.environ.get("H", 7168))
 SHAPES = {"qkv": (3 * H, H), "o": (H, H), "fc1": (F, H), "fc2": (H, F)}
 
 
