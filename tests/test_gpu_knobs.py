@@ -20,7 +20,7 @@ from paper_2403_01164_b200 import hg
 from gpu_util import dev, dev_f32, split_weight
 bad = []
 with hg.Context(0, chunk_bytes=1 << 20, ring_bytes=64 << 20, max_k=32768, max_n=8192) as c:
-    for B in (1, 3, 8):
+    for B in (1, 3, 4, 8):
         for (N, K, n_res, alpha) in ((1024, 7168, 128, 0.6), (640, 12288, 0, 1.0), (512, 1000, 256, 0.0)):
             x, W, b = gen.linear_inputs(77, 0, "fc1", B, N, K)
             Wd, Wh = split_weight(W, n_res)
@@ -45,6 +45,9 @@ print("BAD" if bad else "OK", bad)
     {"HG_GEMV_PROW": "0"},
     {"HG_ROW_BMAX": "1"},
     {"HG_ROW_BMAX": "4"},
+    {"HG_ROW_B4_KMAX": "8192"},
+    {"HG_TC_ST": "6"},
+    {"HG_TC_ST": "4"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
 def test_switch_keeps_parity(env):
     code = SCRIPT % {"root": ROOT, "tests": os.path.join(ROOT, "tests")}
