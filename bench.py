@@ -357,11 +357,15 @@ def pool_placement(args, world, local):
     # lane now and then (measured: 14 threads 283.6 / 285.8 ms/token, 16 threads 283.0 / 329.7 / 298.0,
     # the slow runs with the link at ~46 GB/s -- profiles/r01/threads.md)
     reserve = 2 if per >= 12 else (1 if per >= 4 else 0)
+    pinned_one = world == 1 and first < 0 and args.numa != "off" and reserve == 2 and not args.pageable
+    if pinned_one:
+        # one rank: the pool's workers pinned to the last cores, core 0 (and the floating API thread's
+        # share) left to the API thread, the driver and the clock sampler.  Pinned, 15 threads beat 14:
+        # 280.6 vs 285.8 ms/token over seven alternating pairs, without 14's slow episodes (p90 up to
+        # 304); unpinned, 16 threads were bimodal (profiles/r02/pin_ab.txt, profiles/r01/threads.md)
+        reserve = 1
     threads = args.threads or max(1, per - pin_threads - reserve)
-    if world == 1 and first < 0 and args.numa != "off" and reserve == 2 and not args.pageable:
-        # one rank: the pool's workers pinned to the last cores, the first ones left to the API thread,
-        # the driver and the clock sampler (A/B on one box: 283.7 / 281.0 / 278.3 pinned against
-        # 283.2 / 290.0 / 280.6 unpinned, the unpinned runs with p90 up to 307.7 -- profiles/r02/pin_ab.txt)
+    if pinned_one:
         first = per - threads
     if os.environ.get("HG_BENCH_PIN"):  # development A/B (-1: no pinning)
         first = int(os.environ["HG_BENCH_PIN"])
